@@ -1,0 +1,4 @@
+#pragma once
+// Drop-in path of the reference header glu/params.hpp; everything is declared in
+// glu_b200.hpp (same names and signatures).
+#include "glu/glu_b200.hpp"

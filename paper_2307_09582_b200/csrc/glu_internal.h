@@ -1,0 +1,90 @@
+// glu_internal.h -- shared declarations of the CUDA implementation.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "glu_cuda.h"
+
+struct glu_ctx {
+    int device = 0;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    unsigned long long launches = 0;
+    unsigned long long* d_counters = nullptr;  // [0] = fp64 fallback pixels
+    // Grow-only scratch slots (device memory).
+    static constexpr int kSlots = 16;
+    void* buf[kSlots] = {};
+    size_t cap[kSlots] = {};
+    // Grow-only pinned host slots.
+    void* hbuf[4] = {};
+    size_t hcap[4] = {};
+    // Copy streams + events of the host frame pipeline (created lazily).
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev[8] = {};
+};
+
+namespace glu_cu {
+
+// Scratch slot ids.
+enum Slot {
+    S_HIGH = 0, S_LOW, S_PARAMS, S_OUT, S_ERR, S_AUX, S_PIX,
+    S_CCL_LABEL, S_CCL_LIST, S_CCL_OFF, S_CCL_MISC, S_TRIAL, S_TRIAL2, S_TRIAL3,
+    S_SPARE1, S_SPARE2
+};
+
+void set_error(const std::string& msg);
+int fail_cuda(cudaError_t e, const char* where);
+void* scratch(glu_ctx* ctx, int slot, size_t bytes);  // nullptr on OOM (error set)
+
+struct SolveArgs {
+    const float* high;
+    const float* low;
+    int W, H, s, lw, lh, S;
+    double eps;
+    int mode;
+    glu_pixel_params* params;  // may be null when fused with apply
+    const float* lowT;         // apply target (null: no apply)
+    int channels;
+    int clamp;
+    float* out;
+    unsigned long long* fallbacks;
+};
+
+// Launchers (return cudaError_t of the launch).
+cudaError_t launch_grid_downsample(glu_ctx* ctx, const float* high, int W, int H, int s,
+                                   int lw, int lh, float* low);
+cudaError_t launch_solve(glu_ctx* ctx, const SolveArgs& a);
+cudaError_t launch_solve_list(glu_ctx* ctx, const SolveArgs& a, const uint32_t* pixels,
+                              size_t count);
+cudaError_t launch_apply(glu_ctx* ctx, const glu_pixel_params* field, size_t npx,
+                         const float* lowT, int channels, int clamp, float* out);
+cudaError_t launch_error_map(glu_ctx* ctx, const float* high, const float* recon, size_t npx,
+                             float* e);
+cudaError_t launch_self_error(glu_ctx* ctx, const float* high, const glu_pixel_params* field,
+                              size_t npx, const float* low, float* e);
+cudaError_t launch_op_color(glu_ctx* ctx, const float* in, size_t n, const double* M,
+                            const double* bias, double gammaExp, float* out);
+cudaError_t launch_op_matte(glu_ctx* ctx, const float* in, size_t n, float* out);
+cudaError_t launch_ffma_probe(glu_ctx* ctx, float* sink, int iters, int blocks, int threads);
+cudaError_t launch_pixel_batch(glu_ctx* ctx, const float* ip, const uint32_t* offsets,
+                               const uint32_t* candIdx, const float* candRgb, size_t count,
+                               double eps, int mode, glu_pixel_params* out);
+cudaError_t launch_pair_eval(glu_ctx* ctx, const float* ip, const float* ia, const float* ib,
+                             const double* w, size_t count, double eps, double* we,
+                             double* wf, double* obj);
+
+// Joint optimisation (glu_joint.cu).
+int ccl_find_large_error(glu_ctx* ctx, const float* errors, int W, int H, float thr,
+                         uint8_t* mask, uint32_t* label, size_t* count,
+                         const uint32_t** off, const uint32_t** px);
+int trial_one(glu_ctx* ctx, const float* high, float* low, glu_pixel_params* field,
+              float* errors, const glu_grid& g, const glu_config& cfg, int mode,
+              const uint32_t* comp, size_t n, int* accepted);
+int joint_sweep(glu_ctx* ctx, const float* high, float* low, glu_pixel_params* field,
+                float* errors, const glu_grid& g, const glu_config& cfg, int mode,
+                const uint32_t* off, const uint32_t* px, size_t ncomp, int* accepted,
+                int* rejected);
+
+}  // namespace glu_cu

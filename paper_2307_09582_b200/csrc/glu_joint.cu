@@ -1,0 +1,527 @@
+// glu_joint.cu -- joint downsampling optimisation on the device
+// (jointopt.cpp:9-206): large-error connected components and the
+// replace / re-solve / accept-or-rollback trials.
+//
+// find_large_error (jointopt.cpp:9-46) becomes a lock-free union-find whose
+// roots are the smallest pixel index of each component, so the reference's
+// component order ("raster order of the first pixel") is the order of the
+// roots; a stable key sort of the raster-ordered mask pixels by component
+// yields each component's ascending pixel list.
+//
+// The trials of one sweep (jointopt.cpp:195-202) are strictly sequential in
+// the reference.  k_trial_sweep runs them in order inside one CTA: each trial
+// is parallel over its pixels, and the accept test e1 <= e0 on the
+// reference's sequentially rounded double sums (150-165) is decided by a
+// parallel double sum plus a rigorous rounding bound, falling back to the
+// exact sequential order only when the two sums are within that bound.
+#include <cub/cub.cuh>
+
+#include "glu_internal.h"
+#include "glu_math.cuh"
+
+namespace glu_cu {
+
+namespace {
+
+constexpr uint32_t kNone = 0xffffffffu;
+constexpr int kTrialThreads = 1024;
+
+// ---- connected components ---------------------------------------------------
+
+__global__ void k_ccl_init(const float* __restrict__ e, size_t npx, float thr,
+                           uint8_t* __restrict__ mask, uint32_t* __restrict__ parent) {
+    const size_t p = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= npx) return;
+    const bool m = e[p] > thr;  // strict, jointopt.cpp:17
+    mask[p] = m;
+    parent[p] = m ? uint32_t(p) : kNone;
+}
+
+__device__ __forceinline__ uint32_t find_root(const volatile uint32_t* parent, uint32_t x) {
+    uint32_t p = parent[x];
+    while (p != x) {
+        x = p;
+        p = parent[x];
+    }
+    return x;
+}
+
+// Link the larger root under the smaller one; parent[x] <= x always holds.
+__device__ void unite(uint32_t* parent, uint32_t a, uint32_t b) {
+    for (;;) {
+        a = find_root(parent, a);
+        b = find_root(parent, b);
+        if (a == b) return;
+        if (a < b) {
+            const uint32_t t = a;
+            a = b;
+            b = t;
+        }
+        const uint32_t old = atomicMin(parent + a, b);
+        if (old == a) return;
+        a = old;  // a was re-linked meanwhile: keep its old parent connected too
+    }
+}
+
+__global__ void k_ccl_union(const uint8_t* __restrict__ mask, uint32_t* parent, int W, int H) {
+    const size_t p = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= size_t(W) * H || !mask[p]) return;
+    const int x = int(p % W);
+    if (x > 0 && mask[p - 1]) unite(parent, uint32_t(p), uint32_t(p - 1));
+    if (p >= size_t(W) && mask[p - W]) unite(parent, uint32_t(p), uint32_t(p - W));
+}
+
+__global__ void k_ccl_flatten(uint32_t* parent, size_t npx, uint32_t* __restrict__ isRoot) {
+    const size_t p = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= npx) return;
+    const uint32_t q = parent[p];
+    if (q == kNone) {
+        isRoot[p] = 0;
+        return;
+    }
+    const uint32_t r = find_root(parent, q);
+    isRoot[p] = (r == p);
+    parent[p] = r;
+}
+
+// Mask pixels in raster order with their component rank as the sort key.
+__global__ void k_ccl_keys(const uint32_t* __restrict__ parent, const uint32_t* __restrict__ rank,
+                           const uint32_t* __restrict__ slot, size_t npx,
+                           uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    const size_t p = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= npx) return;
+    const uint32_t r = parent[p];
+    if (r == kNone) return;
+    const uint32_t i = slot[p];  // exclusive scan of mask flags
+    keys[i] = rank[r];
+    vals[i] = uint32_t(p);
+}
+
+__global__ void k_mask_flags(const uint32_t* __restrict__ parent, size_t npx,
+                             uint32_t* __restrict__ flags) {
+    const size_t p = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p < npx) flags[p] = parent[p] != kNone;
+}
+
+__global__ void k_ccl_offsets(const uint32_t* __restrict__ keys, size_t n, uint32_t ncomp,
+                              uint32_t* __restrict__ off) {
+    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i == 0) off[ncomp] = uint32_t(n);
+    if (i >= n) return;
+    if (i == 0 || keys[i] != keys[i - 1]) off[keys[i]] = uint32_t(i);
+}
+
+// ---- trials -------------------------------------------------------------------
+
+struct TrialArgs {
+    const float* high;
+    float* low;
+    glu_pixel_params* field;
+    float* errors;
+    int W, H, s, lw, lh, S;
+    double eps;
+    int mode, literal;
+    const uint32_t* off;
+    const uint32_t* px;
+    int ncomp;
+    unsigned long long* cellKey;  // per LR cell, 0 between trials
+    uint32_t* cellFlag;           // per LR cell, 0 between trials
+    uint8_t* affMark;             // per LR cell, 0 between trials
+    uint32_t* touched;            // replaced cells of the current trial
+    float* oldColor;              // 3 floats per touched cell
+    uint32_t* aff;                // affected pixels, reference order
+    glu_pixel_params* bkParams;
+    float* bkE;
+    int* result;  // [0] accepted, [1] rejected, [2] sequential-sum fallbacks, [3] last verdict
+};
+
+struct GlobalLowWindow {
+    const float* low;
+    int lw, x0, y0, nwx;
+    __device__ __forceinline__ const float* operator[](int i) const {
+        const int r = i / nwx, q = i - r * nwx;
+        return low + 3 * (size_t(y0 + r) * lw + x0 + q);
+    }
+};
+
+__global__ void __launch_bounds__(kTrialThreads) k_trial_sweep(TrialArgs t) {
+    using BlockScan = cub::BlockScan<uint32_t, kTrialThreads>;
+    using BlockReduce = cub::BlockReduce<double, kTrialThreads>;
+    __shared__ union {
+        typename BlockScan::TempStorage scan;
+        typename BlockReduce::TempStorage reduce;
+    } tmp;
+    __shared__ uint32_t sTouched, sBase;
+    __shared__ int sBox[4];
+    __shared__ double sE0, sE1;
+    __shared__ int sVerdict;
+    const int tid = threadIdx.x;
+    const int h = t.S / 2;
+    const uint32_t W = uint32_t(t.W), s = uint32_t(t.s);
+
+    for (int c = 0; c < t.ncomp; ++c) {
+        const uint32_t* comp = t.px + t.off[c];
+        const uint32_t n = t.off[c + 1] - t.off[c];
+        if (tid == 0) {
+            sTouched = 0;
+            sBox[0] = t.lw;
+            sBox[1] = t.lh;
+            sBox[2] = -1;
+            sBox[3] = -1;
+        }
+        __syncthreads();
+        // 1. groupByOwnerCell (jointopt.cpp:56-72) + worst pixel per cell: the
+        //    first strict argmax over ascending pixels == max of (E, -pixel).
+        for (uint32_t i = tid; i < n; i += kTrialThreads) {
+            const uint32_t p = comp[i];
+            const uint32_t cx = (p % W) / s, cy = (p / W) / s;
+            const uint32_t cell = cy * uint32_t(t.lw) + cx;
+            const unsigned long long key =
+                (static_cast<unsigned long long>(__float_as_uint(t.errors[p])) << 32) |
+                (0xffffffffu - p);
+            atomicMax(t.cellKey + cell, key);
+            if (atomicExch(t.cellFlag + cell, 1u) == 0) {
+                t.touched[atomicAdd(&sTouched, 1u)] = cell;
+                atomicMin(&sBox[0], int(cx));
+                atomicMin(&sBox[1], int(cy));
+                atomicMax(&sBox[2], int(cx));
+                atomicMax(&sBox[3], int(cy));
+            }
+        }
+        __syncthreads();
+        const uint32_t nt = sTouched;
+        // 2. replace each cell by its worst pixel (jointopt.cpp:130-142) and
+        //    mark the cells whose windows reach it (affectedPixels, 76-110).
+        for (uint32_t i = tid; i < nt; i += kTrialThreads) {
+            const uint32_t cell = t.touched[i];
+            const uint32_t best = 0xffffffffu - uint32_t(t.cellKey[cell] & 0xffffffffu);
+            float* lc = t.low + 3 * size_t(cell);
+            const float* src = t.high + 3 * size_t(best);
+            t.oldColor[3 * i] = lc[0];
+            t.oldColor[3 * i + 1] = lc[1];
+            t.oldColor[3 * i + 2] = lc[2];
+            lc[0] = src[0];
+            lc[1] = src[1];
+            lc[2] = src[2];
+            if (!t.literal) {
+                const int cx = int(cell % uint32_t(t.lw)), cy = int(cell / uint32_t(t.lw));
+                for (int y = max(0, cy - h); y <= min(t.lh - 1, cy + h); ++y)
+                    for (int x = max(0, cx - h); x <= min(t.lw - 1, cx + h); ++x)
+                        t.affMark[size_t(y) * t.lw + x] = 1;
+            }
+        }
+        __syncthreads();
+        // 3. affected pixels in the reference order: dilated bounding box in
+        //    raster cell order, then each footprint in raster order.
+        const uint32_t* aff = comp;
+        uint32_t na = n;
+        if (!t.literal) {
+            const int bx0 = max(0, sBox[0] - h), by0 = max(0, sBox[1] - h);
+            const int bx1 = min(t.lw - 1, sBox[2] + h), by1 = min(t.lh - 1, sBox[3] + h);
+            const int bw = bx1 - bx0 + 1;
+            const uint32_t nbox = uint32_t(bw) * uint32_t(by1 - by0 + 1);
+            if (tid == 0) sBase = 0;
+            __syncthreads();
+            for (uint32_t b0 = 0; b0 < nbox; b0 += kTrialThreads) {
+                const uint32_t k = b0 + tid;
+                uint32_t fs = 0;
+                int x = 0, y = 0;
+                if (k < nbox) {
+                    x = bx0 + int(k % uint32_t(bw));
+                    y = by0 + int(k / uint32_t(bw));
+                    uint8_t* mk = t.affMark + size_t(y) * t.lw + x;
+                    if (*mk) {
+                        *mk = 0;
+                        fs = uint32_t(min(x * t.s + t.s, t.W) - x * t.s) *
+                             uint32_t(min(y * t.s + t.s, t.H) - y * t.s);
+                    }
+                }
+                uint32_t pos, total;
+                BlockScan(tmp.scan).ExclusiveSum(fs, pos, total);
+                if (fs) {
+                    uint32_t o = sBase + pos;
+                    const int px0 = x * t.s, py0 = y * t.s;
+                    const int px1 = min(px0 + t.s, t.W), py1 = min(py0 + t.s, t.H);
+                    for (int py = py0; py < py1; ++py)
+                        for (int pxx = px0; pxx < px1; ++pxx)
+                            t.aff[o++] = uint32_t(py) * W + uint32_t(pxx);
+                }
+                __syncthreads();
+                if (tid == 0) sBase += total;
+                __syncthreads();
+            }
+            aff = t.aff;
+            na = sBase;
+        }
+        // 4. backup and e0 (jointopt.cpp:150-157).
+        double part = 0;
+        for (uint32_t i = tid; i < na; i += kTrialThreads) {
+            const uint32_t p = aff[i];
+            t.bkParams[i] = t.field[p];
+            t.bkE[i] = t.errors[p];
+            part += double(t.bkE[i]);
+        }
+        double e0 = BlockReduce(tmp.reduce).Sum(part);
+        if (tid == 0) sE0 = e0;
+        __syncthreads();
+        // 5. re-solve (optimize_pixels, 159) and re-score (160-165).
+        part = 0;
+        for (uint32_t i = tid; i < na; i += kTrialThreads) {
+            const uint32_t p = aff[i];
+            const int x = int(p % W), y = int(p / W);
+            const float* ip = t.high + 3 * size_t(p);
+            const int cx = x / t.s, cy = y / t.s;
+            const int x0 = max(0, cx - h), y0 = max(0, cy - h);
+            const int nwx = min(t.lw - 1, cx + h) - x0 + 1, nwy = min(t.lh - 1, cy + h) - y0 + 1;
+            const Pick pk = pick64(t.mode, ip, GlobalLowWindow{t.low, t.lw, x0, y0, nwx},
+                                   nwx * nwy, t.eps);
+            const int ar = pk.ai / nwx, br = pk.bi / nwx;
+            glu_pixel_params np;
+            np.a = uint32_t(y0 + ar) * uint32_t(t.lw) + uint32_t(x0 + pk.ai - ar * nwx);
+            np.b = uint32_t(y0 + br) * uint32_t(t.lw) + uint32_t(x0 + pk.bi - br * nwx);
+            np.w = float(pk.w);
+            t.field[p] = np;
+            float r[3];
+            for (int k = 0; k < 3; ++k)
+                r[k] = lerp_clamp(np.w, t.low[3 * size_t(np.a) + k], t.low[3 * size_t(np.b) + k],
+                                  true);
+            const float e = pixel_error(ip, r);
+            t.errors[p] = e;
+            part += double(e);
+        }
+        double e1 = BlockReduce(tmp.reduce).Sum(part);
+        if (tid == 0) {
+            sE1 = e1;
+            e0 = sE0;
+            // |parallel - sequential| <= 2 * gamma_na * sum for non-negative terms.
+            const double bound = 4.0 * (double(na) + 64.0) * 0x1.0p-53 * (e0 + e1);
+            int verdict;
+            if (e1 + bound < e0)
+                verdict = 1;
+            else if (e1 > e0 + bound)
+                verdict = 0;
+            else {  // exact reference order (jointopt.cpp:150-165)
+                double s0 = 0, s1 = 0;
+                for (uint32_t i = 0; i < na; ++i) {
+                    s0 += double(t.bkE[i]);
+                    s1 += double(t.errors[aff[i]]);
+                }
+                verdict = s1 <= s0;
+                ++t.result[2];
+            }
+            sVerdict = verdict;
+            t.result[verdict ? 0 : 1] += 1;
+            t.result[3] = verdict;
+        }
+        __syncthreads();
+        // 6. rollback (jointopt.cpp:169-179) and reset per-cell state.
+        if (!sVerdict) {
+            for (uint32_t i = tid; i < na; i += kTrialThreads) {
+                const uint32_t p = aff[i];
+                t.field[p] = t.bkParams[i];
+                t.errors[p] = t.bkE[i];
+            }
+        }
+        for (uint32_t i = tid; i < nt; i += kTrialThreads) {
+            const uint32_t cell = t.touched[i];
+            if (!sVerdict) {
+                float* lc = t.low + 3 * size_t(cell);
+                lc[0] = t.oldColor[3 * i];
+                lc[1] = t.oldColor[3 * i + 1];
+                lc[2] = t.oldColor[3 * i + 2];
+            }
+            t.cellKey[cell] = 0;
+            t.cellFlag[cell] = 0;
+        }
+        __syncthreads();
+    }
+}
+
+inline unsigned blocks_for(size_t n, int threads) {
+    return unsigned((n + threads - 1) / threads);
+}
+
+struct JointScratch {
+    unsigned long long* cellKey;
+    uint32_t* cellFlag;
+    uint8_t* affMark;
+    uint32_t* touched;
+    float* oldColor;
+    uint32_t* aff;
+    glu_pixel_params* bkParams;
+    float* bkE;
+    int* result;
+};
+
+// Per-context trial scratch: per-LR-cell state (kept zero between trials) and
+// per-HR-pixel backup buffers sized for the worst case (every pixel affected).
+int joint_scratch(glu_ctx* ctx, const glu_grid& g, JointScratch* js, bool reset) {
+    const size_t lowN = size_t(g.lowW) * g.lowH, npx = size_t(g.highW) * g.highH;
+    const size_t cellBytes = lowN * (8 + 4 + 1 + 4 + 12) + 64;
+    char* cells = static_cast<char*>(scratch(ctx, S_TRIAL, cellBytes + 16 * sizeof(int)));
+    char* pix = static_cast<char*>(scratch(ctx, S_TRIAL2, npx * (4 + 12 + 4)));
+    if (!cells || !pix) return GLU_ENOMEM;
+    js->cellKey = reinterpret_cast<unsigned long long*>(cells);
+    js->cellFlag = reinterpret_cast<uint32_t*>(cells + lowN * 8);
+    js->touched = reinterpret_cast<uint32_t*>(cells + lowN * 12);
+    js->oldColor = reinterpret_cast<float*>(cells + lowN * 16);
+    js->affMark = reinterpret_cast<uint8_t*>(cells + lowN * 28);
+    js->result = reinterpret_cast<int*>(cells + ((cellBytes + 15) & ~size_t(15)));
+    js->aff = reinterpret_cast<uint32_t*>(pix);
+    js->bkParams = reinterpret_cast<glu_pixel_params*>(pix + npx * 4);
+    js->bkE = reinterpret_cast<float*>(pix + npx * 16);
+    if (reset) {
+        cudaError_t e = cudaMemsetAsync(cells, 0, cellBytes + 16 * sizeof(int), ctx->stream);
+        if (e != cudaSuccess) return fail_cuda(e, "joint scratch");
+    }
+    return GLU_OK;
+}
+
+}  // namespace
+
+int ccl_find_large_error(glu_ctx* ctx, const float* errors, int W, int H, float thr,
+                         uint8_t* mask, uint32_t* label, size_t* count, const uint32_t** offOut,
+                         const uint32_t** pxOut) {
+    const size_t npx = size_t(W) * H;
+    cudaStream_t st = ctx->stream;
+    uint8_t* dmask = mask ? mask : static_cast<uint8_t*>(scratch(ctx, S_CCL_MISC, npx));
+    uint32_t* parent = label ? label : static_cast<uint32_t*>(scratch(ctx, S_CCL_LABEL, npx * 4));
+    // flags/rank/slot + keys/vals (+ sorted copies) + offsets
+    uint32_t* work = static_cast<uint32_t*>(scratch(ctx, S_CCL_LIST, npx * 4 * 6 + 64));
+    if (!dmask || !parent || !work) return GLU_ENOMEM;
+    uint32_t* flags = work;
+    uint32_t* rank = work + npx;
+    uint32_t* keys = work + 2 * npx;
+    uint32_t* vals = work + 3 * npx;
+    uint32_t* keys2 = work + 4 * npx;
+    uint32_t* vals2 = work + 5 * npx;
+    uint32_t* tot = work + 6 * npx;  // [0] ncomp, [1] nmask
+    cudaError_t e;
+    k_ccl_init<<<blocks_for(npx, 256), 256, 0, st>>>(errors, npx, thr, dmask, parent);
+    k_ccl_union<<<blocks_for(npx, 256), 256, 0, st>>>(dmask, parent, W, H);
+    k_ccl_flatten<<<blocks_for(npx, 256), 256, 0, st>>>(parent, npx, flags);
+    ctx->launches += 3;
+    // rank of each root = component id (raster order of the smallest pixel).
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, flags, rank, int(npx), st);
+    size_t tbSort = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tbSort, keys, keys2, vals, vals2, int(npx), 0, 32,
+                                    st);
+    void* temp = scratch(ctx, S_CCL_OFF, std::max(tb, tbSort) + npx * 4 + 64);
+    if (!temp) return GLU_ENOMEM;
+    uint32_t* off = reinterpret_cast<uint32_t*>(static_cast<char*>(temp) +
+                                                ((std::max(tb, tbSort) + 255) & ~size_t(255)));
+    e = cub::DeviceScan::ExclusiveSum(temp, tb, flags, rank, int(npx), st);
+    if (e != cudaSuccess) return fail_cuda(e, "ccl scan");
+    // totals: ncomp = rank[last] + flags[last]
+    uint32_t hostTot[2];
+    {
+        uint32_t lastRank, lastFlag;
+        e = cudaMemcpyAsync(&lastRank, rank + npx - 1, 4, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(&lastFlag, flags + npx - 1, 4, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return fail_cuda(e, "ccl count");
+        hostTot[0] = lastRank + lastFlag;
+    }
+    // mask slots
+    k_mask_flags<<<blocks_for(npx, 256), 256, 0, st>>>(parent, npx, flags);
+    ++ctx->launches;
+    e = cub::DeviceScan::ExclusiveSum(temp, tb, flags, keys2, int(npx), st);  // keys2 = slots
+    if (e != cudaSuccess) return fail_cuda(e, "ccl slots");
+    {
+        uint32_t lastSlot, lastFlag;
+        e = cudaMemcpyAsync(&lastSlot, keys2 + npx - 1, 4, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(&lastFlag, flags + npx - 1, 4, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return fail_cuda(e, "ccl count");
+        hostTot[1] = lastSlot + lastFlag;
+    }
+    (void)tot;
+    const uint32_t ncomp = hostTot[0], nmask = hostTot[1];
+    *count = ncomp;
+    if (ncomp == 0) {
+        if (offOut) *offOut = off;
+        if (pxOut) *pxOut = vals2;
+        return GLU_OK;
+    }
+    k_ccl_keys<<<blocks_for(npx, 256), 256, 0, st>>>(parent, rank, keys2, npx, keys, vals);
+    ++ctx->launches;
+    int bits = 1;
+    while (bits < 32 && (uint64_t(1) << bits) <= ncomp) ++bits;
+    e = cub::DeviceRadixSort::SortPairs(temp, tbSort, keys, keys2, vals, vals2, int(nmask), 0,
+                                        bits, st);
+    if (e != cudaSuccess) return fail_cuda(e, "ccl sort");
+    k_ccl_offsets<<<blocks_for(nmask, 256), 256, 0, st>>>(keys2, nmask, ncomp, off);
+    ++ctx->launches;
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return fail_cuda(e, "ccl");
+    if (offOut) *offOut = off;
+    if (pxOut) *pxOut = vals2;
+    return GLU_OK;
+}
+
+int joint_sweep(glu_ctx* ctx, const float* high, float* low, glu_pixel_params* field,
+                float* errors, const glu_grid& g, const glu_config& cfg, int mode,
+                const uint32_t* off, const uint32_t* px, size_t ncomp, int* accepted,
+                int* rejected) {
+    JointScratch js;
+    int rc = joint_scratch(ctx, g, &js, true);
+    if (rc) return rc;
+    TrialArgs t;
+    t.high = high;
+    t.low = low;
+    t.field = field;
+    t.errors = errors;
+    t.W = g.highW;
+    t.H = g.highH;
+    t.s = g.scale;
+    t.lw = g.lowW;
+    t.lh = g.lowH;
+    t.S = cfg.windowSide;
+    t.eps = double(cfg.epsilon);
+    t.mode = mode;
+    t.literal = cfg.literalComponentUpdate;
+    t.off = off;
+    t.px = px;
+    t.ncomp = int(ncomp);
+    t.cellKey = js.cellKey;
+    t.cellFlag = js.cellFlag;
+    t.affMark = js.affMark;
+    t.touched = js.touched;
+    t.oldColor = js.oldColor;
+    t.aff = js.aff;
+    t.bkParams = js.bkParams;
+    t.bkE = js.bkE;
+    t.result = js.result;
+    k_trial_sweep<<<1, kTrialThreads, 0, ctx->stream>>>(t);
+    ++ctx->launches;
+    int res[4];
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(res, js.result, sizeof(res), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return fail_cuda(e, "trial sweep");
+    *accepted = res[0];
+    *rejected = res[1];
+    return GLU_OK;
+}
+
+int trial_one(glu_ctx* ctx, const float* high, float* low, glu_pixel_params* field,
+              float* errors, const glu_grid& g, const glu_config& cfg, int mode,
+              const uint32_t* comp, size_t n, int* accepted) {
+    uint32_t* off = static_cast<uint32_t*>(scratch(ctx, S_TRIAL3, 2 * sizeof(uint32_t)));
+    if (!off) return GLU_ENOMEM;
+    const uint32_t h[2] = {0, uint32_t(n)};
+    cudaError_t e = cudaMemcpyAsync(off, h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream);
+    if (e != cudaSuccess) return fail_cuda(e, "trial");
+    int acc = 0, rej = 0;
+    const int rc = joint_sweep(ctx, high, low, field, errors, g, cfg, mode, off, comp, 1, &acc,
+                               &rej);
+    if (rc) return rc;
+    *accepted = acc;
+    return GLU_OK;
+}
+
+}  // namespace glu_cu

@@ -1,0 +1,174 @@
+// glu_math.cuh -- per-pixel selection maths, bit-compatible with the reference.
+//
+// The reference evaluates every selection quantity in IEEE double with FP
+// contraction disabled (proj/CMakeLists.txt:15-18; upsample.cpp:28-42,
+// 49-104, 158-176).  These functions restate those expressions in the same
+// operation order.  The whole library is compiled with -fmad=false, so no
+// double (or float) expression here is contracted into an FMA; the fp32 search
+// kernels request FMAs explicitly with __fmaf_rn where the maths is only a
+// filter.  Division and sqrt are the IEEE round-to-nearest operators, so the
+// results are bit-identical to the x86-64 SSE2 reference.
+#pragma once
+
+#include <stdint.h>
+
+#include "glu_cuda.h"
+
+#if defined(__CUDACC__)
+#define GLU_HD __host__ __device__ __forceinline__
+#else
+#define GLU_HD inline
+#include <cmath>
+#endif
+
+namespace glu_cu {
+
+GLU_HD double dsqrt(double x) { return sqrt(x); }
+
+// dist(p, q): upsample.cpp:28-33.
+GLU_HD double dist64(const float* p, const float* q) {
+    const double d0 = double(p[0]) - double(q[0]);
+    const double d1 = double(p[1]) - double(q[1]);
+    const double d2 = double(p[2]) - double(q[2]);
+    return dsqrt(d0 * d0 + d1 * d1 + d2 * d2);
+}
+
+// Squared distance before the sqrt (same sums as dist64).
+GLU_HD double dist2_64(const float* p, const float* q) {
+    const double d0 = double(p[0]) - double(q[0]);
+    const double d1 = double(p[1]) - double(q[1]);
+    const double d2 = double(p[2]) - double(q[2]);
+    return d0 * d0 + d1 * d1 + d2 * d2;
+}
+
+// objective(ip, ia, ib, w, eps): upsample.cpp:35-42.
+GLU_HD double objective64(const float* ip, const float* ia, const float* ib, double w,
+                          double eps) {
+    double r = 0;
+    for (int c = 0; c < 3; ++c) {
+        const double v = w * double(ia[c]) + (1.0 - w) * double(ib[c]) - double(ip[c]);
+        r += v * v;
+    }
+    return r + eps * w * w;
+}
+
+// weight_exact: upsample.cpp:158-167.
+GLU_HD double weight_exact64(const float* ip, const float* ia, const float* ib, double eps) {
+    double num = 0, den = 0;
+    for (int c = 0; c < 3; ++c) {
+        const double pb = double(ip[c]) - double(ib[c]);
+        const double ab = double(ia[c]) - double(ib[c]);
+        num += pb * ab;
+        den += ab * ab;
+    }
+    return num / (den + eps);
+}
+
+// weight_fast: upsample.cpp:169-172.
+GLU_HD double weight_fast64(const float* ip, const float* ia, const float* ib, double eps) {
+    const double db = dist64(ip, ib);
+    return db / (dist64(ip, ia) + db + eps);
+}
+
+// Candidate access: any type whose operator[](i) returns candidate i's colour
+// (3 floats); candidates are indexed in the reference's raster list order.
+struct StridedCands {
+    const float* rgb;
+    int stride;
+    GLU_HD const float* operator[](int i) const { return rgb + i * stride; }
+};
+
+struct Pick {
+    int ai, bi;
+    double w;
+};
+
+// pixelFast: upsample.cpp:49-71.  Distances are recomputed in the second loop
+// instead of kept in a scratch array; the value is bitwise the same.
+template <class Cands>
+GLU_HD Pick pick_fast64(const float* ip, Cands c, int n, double eps) {
+    int ai = 0;
+    double da = dist64(ip, c[0]);
+    for (int i = 1; i < n; ++i) {
+        const double d = dist64(ip, c[i]);
+        if (d < da) {
+            da = d;
+            ai = i;
+        }
+    }
+    const float* ia = c[ai];
+    int bi = 0;
+    double bestW = 0, bestObj = 0;
+    for (int j = 0; j < n; ++j) {
+        const double dj = dist64(ip, c[j]);
+        const double w = dj / (da + dj + eps);
+        const double obj = objective64(ip, ia, c[j], w, eps);
+        if (j == 0 || obj < bestObj) {
+            bestObj = obj;
+            bestW = w;
+            bi = j;
+        }
+    }
+    return {ai, bi, bestW};
+}
+
+// pixelExact: upsample.cpp:73-91 (pairs i <= j, lexicographic, first argmin).
+template <class Cands>
+GLU_HD Pick pick_exact64(const float* ip, Cands c, int n, double eps) {
+    Pick best{0, 0, 0.0};
+    double bestObj = 0;
+    bool first = true;
+    for (int i = 0; i < n; ++i) {
+        for (int j = i; j < n; ++j) {
+            const double w = weight_exact64(ip, c[i], c[j], eps);
+            const double obj = objective64(ip, c[i], c[j], w, eps);
+            if (first || obj < bestObj) {
+                first = false;
+                bestObj = obj;
+                best = {i, j, w};
+            }
+        }
+    }
+    return best;
+}
+
+// pixelGnu: upsample.cpp:93-104.
+template <class Cands>
+GLU_HD Pick pick_gnu64(const float* ip, Cands c, int n) {
+    int ai = 0;
+    double best = dist64(ip, c[0]);
+    for (int i = 1; i < n; ++i) {
+        const double d = dist64(ip, c[i]);
+        if (d < best) {
+            best = d;
+            ai = i;
+        }
+    }
+    return {ai, ai, 1.0};
+}
+
+template <class Cands>
+GLU_HD Pick pick64(int mode, const float* ip, Cands c, int n, double eps) {
+    if (mode == GLU_MODE_EXACT) return pick_exact64(ip, c, n, eps);
+    if (mode == GLU_MODE_GNU) return pick_gnu64(ip, c, n);
+    return pick_fast64(ip, c, n, eps);
+}
+
+// reconstruct_pixel, one channel (upsample.hpp:54-65): float maths, no FMA.
+GLU_HD float lerp_clamp(float w, float la, float lb, bool clampOutput) {
+    float v = w * la + (1.0f - w) * lb;
+    if (clampOutput) v = v < 0.0f ? 0.0f : (v > 1.0f ? 1.0f : v);
+    return v;
+}
+
+// pixel_error (upsample.hpp:67-74).
+GLU_HD float pixel_error(const float* t, const float* r) {
+    double s = 0;
+    for (int c = 0; c < 3; ++c) {
+        const double d = double(t[c]) - double(r[c]);
+        s += d * d;
+    }
+    return float(dsqrt(s));
+}
+
+}  // namespace glu_cu

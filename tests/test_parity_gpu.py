@@ -1,0 +1,236 @@
+"""Parity of the CUDA path (through the C-ABI) with the reference.
+
+Bit-exact against the reference's golden vectors and against the pinned oracle
+on fresh seeded inputs; size-independent properties at BASELINE sizes.
+Tolerance: none -- indices, weights, images and error maps must match
+bit for bit (stronger than north_star's 1e-5 / 1e-4 bars).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import EPS_DEFAULT, PARAMS_DTYPE, TAU_DEFAULT
+
+pytestmark = pytest.mark.gpu
+
+SOLVES = ["mix67x45_s4", "mix41x33_s4", "photo40x28_s4", "mix37x29_s4_S5", "mix50x38_s3_S7",
+          "mix45x45_s5_S9", "mix33x21_s2", "scene96x64_s8", "scene100x70_s16"]
+JOINTS = ["joint_missed_line", "joint_missed_line_literal", "joint_mix72x60_s6",
+          "joint_mix64x56_s8", "joint_mix48_s6_tau05", "joint_mix128_s8", "joint_mix60x52_s4_S5",
+          "joint_scene160x96_s8", "joint_harmful"]
+
+
+def dev(a):
+    a = np.ascontiguousarray(a)
+    if a.dtype == PARAMS_DTYPE:
+        a = a.view(np.int32).reshape(a.shape + (3,))
+    elif a.dtype == np.uint32:
+        a = a.view(np.int32)
+    return torch.from_numpy(a.copy()).cuda()
+
+
+def host_params(t):
+    return t.cpu().numpy().view(PARAMS_DTYPE)[..., 0]
+
+
+def same(a, b):
+    a, b = np.ascontiguousarray(a), np.ascontiguousarray(b)
+    return a.nbytes == b.nbytes and a.tobytes() == b.tobytes()
+
+
+def mode_of(glu, m):
+    return glu.mode_from_name(m)
+
+
+@pytest.mark.parametrize("name", SOLVES)
+def test_solve_apply_error_golden(glu, golden, name):
+    img, (s, S) = golden[f"{name}/high"], golden[f"{name}/meta"]
+    high = dev(img)
+    low, grid = glu.grid_downsample(high, int(s))
+    assert same(low.cpu().numpy(), golden[f"{name}/low"])
+    cfg = glu.GluConfig(windowSide=int(S))
+    for m in ("fast", "exact", "gnu"):
+        field = glu.optimize_field(high, low, grid, cfg, mode_of(glu, m))
+        want = golden[f"{name}/params_{m}"]
+        got = host_params(field.params)
+        assert same(got, want), (m, int((got != want.view(PARAMS_DTYPE).reshape(
+            got.shape)).sum()))
+        rec = glu.apply_field(field, low)
+        assert same(rec.cpu().numpy(), golden[f"{name}/apply_{m}"]), m
+        assert same(glu.error_map(high, rec).cpu().numpy(), golden[f"{name}/errors_{m}"]), m
+        assert same(glu.self_error_map(high, field, low).cpu().numpy(),
+                    golden[f"{name}/errors_{m}"]), m
+        out, pf = glu.solve_apply(high, low, grid, low, cfg, mode_of(glu, m), keep_params=True)
+        assert same(out.cpu().numpy(), golden[f"{name}/apply_{m}"]), m
+        assert same(host_params(pf.params), want), m
+    field = glu.optimize_field(high, low, grid, cfg, glu.Mode.Fast)
+    half = glu.apply_field(field, low * 0.5, clampOutput=False)
+    assert same(half.cpu().numpy(), golden[f"{name}/apply_fast_noclamp_half"])
+
+
+@pytest.mark.parametrize("name", JOINTS)
+def test_joint_golden(glu, golden, name):
+    img, (s, S, lit) = golden[f"{name}/high"], golden[f"{name}/meta"]
+    tau = float(golden[f"{name}/tau"][0])
+    cfg = glu.GluConfig(windowSide=int(S), errorThreshold=tau, literalComponentUpdate=bool(lit))
+    modes = ("fast", "exact", "gnu") if name == "joint_mix72x60_s6" else ("fast",)
+    for m in modes:
+        r = glu.joint_optimize(dev(img), int(s), cfg, mode_of(glu, m))
+        key = f"{name}/{m}"
+        assert [r.iterations, r.trialsAccepted, r.trialsRejected] == \
+            golden[f"{key}/counts"].tolist(), m
+        assert same(r.low.cpu().numpy(), golden[f"{key}/low"]), m
+        assert same(host_params(r.field.params), golden[f"{key}/params"]), m
+        assert same(r.errors.cpu().numpy(), golden[f"{key}/errors"]), m
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_trial_sequence_golden(glu, golden, seed):
+    """Per-trial verdicts, bitwise rollback (jointopt_test.cpp:76-109)."""
+    img = golden[f"trials_mix48_{seed}/high"]
+    s = 6
+    cfg = glu.GluConfig(errorThreshold=0.05)
+    high = dev(img)
+    low, grid = glu.grid_downsample(high, s)
+    field = glu.optimize_field(high, low, grid, cfg)
+    errors = glu.error_map(high, glu.apply_field(field, low))
+    les = glu.find_large_error(errors, 0.05)
+    verdicts = []
+    for comp in les.components:
+        before = (low.clone(), field.params.clone(), errors.clone())
+        ok = glu.trial_update_component(high, low, field, errors, comp, cfg)
+        verdicts.append(ok)
+        if not ok:
+            assert torch.equal(low, before[0]) and torch.equal(field.params, before[1])
+            assert torch.equal(errors, before[2])
+    assert verdicts == golden[f"trials_mix48_{seed}/verdicts"].astype(bool).tolist()
+    assert same(low.cpu().numpy(), golden[f"trials_mix48_{seed}/low"])
+    assert same(host_params(field.params), golden[f"trials_mix48_{seed}/params"])
+    assert same(errors.cpu().numpy(), golden[f"trials_mix48_{seed}/errors"])
+
+
+@pytest.mark.parametrize("name", ["ccl_pin", "ccl_scene"])
+def test_find_large_error_golden(glu, golden, name):
+    les = glu.find_large_error(dev(golden[f"{name}/errors"]), float(golden[f"{name}/tau"][0]))
+    assert same(les.mask.cpu().numpy(), golden[f"{name}/mask"])
+    assert same(les.offsets.cpu().numpy().astype(np.uint32), golden[f"{name}/offsets"])
+    assert same(les.pixels.cpu().numpy().view(np.uint32), golden[f"{name}/pixels"])
+
+
+@pytest.mark.parametrize("mode", ["fast", "exact", "gnu"])
+def test_pixel_batch_golden(glu, golden, mode):
+    ip, rgb, idx, off = (golden[f"pixels/{k}"] for k in ("ip", "rgb", "idx", "off"))
+    cands = [(idx[off[k]:off[k + 1]], rgb[off[k]:off[k + 1]]) for k in range(len(ip))]
+    got = glu.optimize_pixel_batch(ip, cands, 1e-3, mode_of(glu, mode))
+    assert same(got.view(np.uint32).reshape(-1, 3), golden[f"pixels/{mode}"])
+
+
+def test_scalar_pins(glu):
+    # upsample_test.cpp:39-63, 134-159, 178-189
+    assert glu.weight_exact([0.25, 0, 0], [1, 0, 0], [0, 0, 0], 1e-3) == pytest.approx(
+        0.25 / 1.001, rel=1e-9)
+    assert glu.weight_fast([0.5] * 3, [1] * 3, [0] * 3, 1e-3) == pytest.approx(0.4997, rel=1e-4)
+    rng = np.random.default_rng(424242)
+    w = glu.weight_fast(rng.random((5000, 3)), rng.random((5000, 3)), rng.random((5000, 3)), 1e-3)
+    assert (w >= 0).all() and (w < 1).all()
+    p = glu.optimize_pixel_exact([0.9, 0.1, 0.5], (np.arange(6) + 40,
+                                                   np.tile([0.3, 0.7, 0.2], (6, 1))), 1e-3)
+    assert (int(p["a"]), int(p["b"]), float(p["w"])) == (40, 40, 0.0)
+    p = glu.optimize_pixel_exact([1.0] * 3, ([0, 1], [[0.8] * 3, [0.4] * 3]), 1e-3)
+    assert float(p["w"]) > 1.0
+    with pytest.raises(ValueError):
+        glu.optimize_pixel_gnu([0, 0, 0], ([], np.zeros((0, 3))))
+
+
+CASES = [  # (W, H, s, S, seed): ragged sizes, every supported window class
+    (131, 77, 4, 3, 11), (200, 120, 8, 3, 12), (97, 203, 3, 5, 13), (160, 90, 5, 7, 14),
+    (64, 64, 2, 9, 15), (257, 129, 16, 3, 16), (33, 300, 6, 11, 17),
+]
+
+
+@pytest.mark.parametrize("W,H,s,S,seed", CASES)
+def test_solve_vs_oracle_seeded(glu, oracle, W, H, s, S, seed):
+    from paper_2307_09582_b200 import workloads
+    img = workloads.scene(W, H, seed)
+    high = dev(img)
+    low, grid = glu.grid_downsample(high, s)
+    lo = oracle.grid_downsample(img, s)
+    assert same(low.cpu().numpy(), lo)
+    for m in ("fast", "exact", "gnu"):
+        f = glu.optimize_field(high, low, grid, glu.GluConfig(windowSide=S), mode_of(glu, m))
+        want = oracle.optimize_field(img, lo, s, S, EPS_DEFAULT, m)
+        assert same(host_params(f.params), want), m
+
+
+def test_optimize_pixels_matches_field(glu):
+    # upsample_test.cpp:226-237: sparse re-solve of every pixel == optimize_field
+    from paper_2307_09582_b200 import workloads
+    img = dev(workloads.scene(123, 77, 5))
+    low, grid = glu.grid_downsample(img, 4)
+    full = glu.optimize_field(img, low, grid)
+    sparse = full.clone()
+    sparse.params.fill_(-1)
+    order = torch.randperm(123 * 77, device="cuda").to(torch.int32)
+    glu.optimize_pixels(img, low, grid, None, glu.Mode.Fast, order, sparse)
+    assert torch.equal(full.params, sparse.params)
+
+
+def test_single_channel_apply_matches_rgb(glu, oracle):
+    from paper_2307_09582_b200 import workloads
+    img = workloads.scene(240, 136, 6)
+    high = dev(img)
+    low, grid = glu.grid_downsample(high, 8)
+    matte = glu.op_matte(low)
+    field = glu.optimize_field(high, low, grid)
+    one = glu.apply_field(field, matte).cpu().numpy()
+    rgb = oracle.apply_field(host_params(field.params),
+                             np.repeat(matte.cpu().numpy()[..., None], 3, axis=2))
+    assert same(one, np.ascontiguousarray(rgb[..., 0]))
+    fused, _ = glu.solve_apply(high, low, grid, matte)
+    assert same(fused.cpu().numpy(), one)
+
+
+def test_joint_vs_oracle_seeded(glu, oracle):
+    from paper_2307_09582_b200 import workloads
+    for (W, H, s, seed) in ((256, 192, 8, 21), (300, 170, 6, 22)):
+        img = workloads.scene(W, H, seed)
+        r = glu.joint_optimize(dev(img), s)
+        o = oracle.joint_optimize(img, s)
+        assert [r.iterations, r.trialsAccepted, r.trialsRejected] == \
+            [o["iterations"], o["accepted"], o["rejected"]]
+        assert same(r.low.cpu().numpy(), o["low"])
+        assert same(host_params(r.field.params), o["field"])
+        assert same(r.errors.cpu().numpy(), o["errors"])
+
+
+def test_full_size_properties(glu, oracle):
+    """C3 size (3840x2160, s=8): determinism, oracle rows, gain linearity."""
+    from paper_2307_09582_b200 import workloads
+    img = workloads.scene(3840, 2160, 3, 0)
+    high = dev(img)
+    low, grid = glu.grid_downsample(high, 8)
+    f1 = glu.optimize_field(high, low, grid)
+    f2 = glu.optimize_field(high, low, grid)
+    assert torch.equal(f1.params, f2.params)
+    # every pixel against the oracle (fast mode, the reference default)
+    want = oracle.optimize_field(img, low.cpu().numpy(), 8)
+    assert same(host_params(f1.params), want)
+    out = glu.apply_field(f1, low, clampOutput=False)
+    half = glu.apply_field(f1, low * 0.5, clampOutput=False)
+    assert torch.equal(half, out * 0.5)
+
+
+def test_validation_messages(glu):
+    img = torch.zeros((16, 16, 3), device="cuda")
+    low, grid = glu.grid_downsample(img, 4)
+    with pytest.raises(ValueError, match="windowSide must be odd"):
+        glu.optimize_field(img, low, grid, glu.GluConfig(windowSide=4))
+    with pytest.raises(ValueError, match="epsilon must be > 0"):
+        glu.optimize_field(img, low, grid, glu.GluConfig(epsilon=0.0))
+    with pytest.raises(ValueError, match="low-res image does not match grid"):
+        glu.optimize_field(img, torch.zeros((4, 3, 3), device="cuda"), grid)
+    with pytest.raises(ValueError, match="image dimensions differ"):
+        glu.error_map(img, torch.zeros((4, 4, 3), device="cuda"))
+    with pytest.raises(ValueError, match="empty component"):
+        f = glu.optimize_field(img, low, grid)
+        glu.trial_update_component(img, low, f, torch.zeros((16, 16), device="cuda"), [])
