@@ -97,6 +97,14 @@ int glu_ctx_destroy(glu_ctx* ctx);
 int glu_ctx_set_stream(glu_ctx* ctx, void* cuda_stream);
 void* glu_ctx_stream(glu_ctx* ctx);
 int glu_ctx_synchronize(glu_ctx* ctx);
+/* Context options.  GLU_OPT_SOLVER selects the solve kernel:
+ *   0 (default) fp32 filter + fp64 verify where supported (Fast/GNU, S 3 or 5),
+ *     the fp64 reference-order kernel otherwise;
+ *   1 the fp64 reference-order kernel everywhere;
+ *   2 fp32 filter with every pixel forced through the fp64 verify (testing).
+ * All settings produce bit-identical results. */
+enum glu_option { GLU_OPT_SOLVER = 1 };
+int glu_ctx_set_option(glu_ctx* ctx, int option, int value);
 /* Number of kernels this context has launched (bench.py's gpu_launches). */
 unsigned long long glu_ctx_launch_count(glu_ctx* ctx);
 /* Pixels the last solve/joint call re-evaluated on the exact fp64 path. */

@@ -50,6 +50,7 @@ SIGNATURES: dict[str, tuple] = {
     "glu_ctx_destroy": (I, [P]),
     "glu_ctx_set_stream": (I, [P, P]),
     "glu_ctx_stream": (P, [P]),
+    "glu_ctx_set_option": (I, [P, I, I]),
     "glu_ctx_synchronize": (I, [P]),
     "glu_ctx_launch_count": (U64, [P]),
     "glu_ctx_fallback_count": (U64, [P]),

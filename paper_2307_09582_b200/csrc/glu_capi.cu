@@ -228,6 +228,16 @@ int glu_ctx_set_stream(glu_ctx* ctx, void* s) {
 
 void* glu_ctx_stream(glu_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
 
+int glu_ctx_set_option(glu_ctx* ctx, int option, int value) {
+    if (!ctx) return einval("ctx must not be null");
+    if (option == GLU_OPT_SOLVER) {
+        if (value < 0 || value > 2) return einval("GLU_OPT_SOLVER: value must be 0, 1 or 2");
+        ctx->solver = value;
+        return GLU_OK;
+    }
+    return einval("unknown option");
+}
+
 int glu_ctx_synchronize(glu_ctx* ctx) {
     if (!ctx) return einval("ctx must not be null");
     GLU_CUDA(cudaStreamSynchronize(ctx->stream), "synchronize");

@@ -20,6 +20,9 @@ struct glu_ctx {
     // Grow-only pinned host slots.
     void* hbuf[4] = {};
     size_t hcap[4] = {};
+    // GLU_OPT_SOLVER: 0 auto, 1 fp64 reference-order kernel only, 2 fp32
+    // filter with every pixel forced through the fp64 verify path (testing).
+    int solver = 0;
     // Copy streams + events of the host frame pipeline (created lazily).
     cudaStream_t h2d = nullptr, d2h = nullptr;
     cudaEvent_t ev[8] = {};
@@ -56,6 +59,9 @@ struct SolveArgs {
 cudaError_t launch_grid_downsample(glu_ctx* ctx, const float* high, int W, int H, int s,
                                    int lw, int lh, float* low);
 cudaError_t launch_solve(glu_ctx* ctx, const SolveArgs& a);
+// glu_solve32.cu: fp32 filter + fp64 verify (Fast / GNU, S in {3, 5}).
+bool solve32_supported(int mode, int S);
+cudaError_t launch_solve32(glu_ctx* ctx, const SolveArgs& a, int forceFallback);
 cudaError_t launch_solve_list(glu_ctx* ctx, const SolveArgs& a, const uint32_t* pixels,
                               size_t count);
 cudaError_t launch_apply(glu_ctx* ctx, const glu_pixel_params* field, size_t npx,

@@ -272,6 +272,8 @@ cudaError_t launch_grid_downsample(glu_ctx* ctx, const float* high, int W, int H
 }
 
 cudaError_t launch_solve(glu_ctx* ctx, const SolveArgs& a) {
+    if (ctx->solver != 1 && solve32_supported(a.mode, a.S))
+        return launch_solve32(ctx, a, ctx->solver == 2);
     const int h = a.S / 2;
     const int ncx = (kTX - 1) / a.s + 2 + 2 * h, ncy = (kTY - 1) / a.s + 2 + 2 * h;
     const size_t smem = size_t(ncx) * ncy * 3 * sizeof(float);

@@ -162,7 +162,15 @@ class Context:
 
     def bind_stream(self) -> None:
         s = torch.cuda.current_stream(self.device).cuda_stream
-        N.check(N.lib().glu_ctx_set_stream(self.handle, C.c_void_p(s)))
+        # torch's default stream is the legacy NULL stream; the C-ABI reads NULL
+        # as "the context's own stream", so name the legacy stream explicitly
+        # (cudaStreamLegacy == 0x1) to stay ordered with torch work and events.
+        N.check(N.lib().glu_ctx_set_stream(self.handle, C.c_void_p(s if s else 1)))
+
+    def set_solver(self, value: int) -> None:
+        """GLU_OPT_SOLVER: 0 auto (fp32 filter + fp64 verify), 1 fp64 kernel only,
+        2 fp32 filter with every pixel forced through the fp64 verify."""
+        N.check(N.lib().glu_ctx_set_option(self.handle, 1, int(value)))
 
     @property
     def launches(self) -> int:
@@ -383,11 +391,13 @@ def optimize_pixel_batch(ips, cand_lists, eps: float, mode: Mode) -> np.ndarray:
     T = lambda a: torch.as_tensor(np.ascontiguousarray(a).view(np.int32)
                                   if a.dtype == np.uint32 else np.ascontiguousarray(a),
                                   device=dev)
-    ip = T(np.asarray(ips, np.float32).reshape(-1, 3))
+    # keep every device buffer referenced until the (asynchronous) kernel has run
+    ip, doff, didx, drgb = (T(np.asarray(ips, np.float32).reshape(-1, 3)), T(off), T(idx),
+                            T(rgb))
     out = torch.empty((len(counts), 3), dtype=torch.int32, device=dev)
     ctx = context()
-    N.check(N.lib().glu_cu_optimize_pixel_batch(ctx.handle, _ptr(ip), _ptr(T(off)), _ptr(T(idx)),
-                                                _ptr(T(rgb)), len(counts), float(eps), int(mode),
+    N.check(N.lib().glu_cu_optimize_pixel_batch(ctx.handle, _ptr(ip), _ptr(doff), _ptr(didx),
+                                                _ptr(drgb), len(counts), float(eps), int(mode),
                                                 _ptr(out)))
     return out.cpu().numpy().view(PARAMS_DTYPE).reshape(-1)
 

@@ -234,3 +234,37 @@ def test_validation_messages(glu):
     with pytest.raises(ValueError, match="empty component"):
         f = glu.optimize_field(img, low, grid)
         glu.trial_update_component(img, low, f, torch.zeros((16, 16), device="cuda"), [])
+
+
+def _stress_images():
+    """Inputs built to provoke near-ties in the fp32 filter: quantised colours
+    (exact duplicate candidates), smooth colinear ramps, pure noise, tiny values."""
+    from paper_2307_09582_b200 import workloads
+    rng = np.random.default_rng(7)
+    base = workloads.scene(320, 200, 31)
+    yield "scene", base
+    yield "quantised", (np.round(base * 4) / 4).astype(np.float32)
+    yy, xx = np.mgrid[0:200, 0:320].astype(np.float32)
+    ramp = np.stack([xx / 320, yy / 200, (xx + yy) / 520], axis=2).astype(np.float32)
+    yield "ramp", ramp
+    yield "noise", rng.random((200, 320, 3), dtype=np.float32)
+    yield "tiny", (rng.random((200, 320, 3)) * 1e-6).astype(np.float32)
+    yield "two_level", (rng.random((200, 320, 1)) < 0.5).repeat(3, 2).astype(np.float32)
+
+
+@pytest.mark.parametrize("mode", ["fast", "gnu"])
+@pytest.mark.parametrize("S", [3, 5])
+def test_fp32_filter_matches_oracle_on_stress_images(glu, oracle, mode, S):
+    ctx = glu.glu.context()
+    for name, img in _stress_images():
+        for s in (4, 8):
+            high = dev(img)
+            low, grid = glu.grid_downsample(high, s)
+            want = oracle.optimize_field(img, low.cpu().numpy(), s, S, EPS_DEFAULT, mode)
+            for solver in (0, 1, 2):
+                ctx.set_solver(solver)
+                f = glu.optimize_field(high, low, grid, glu.GluConfig(windowSide=S),
+                                       mode_of(glu, mode))
+                got = host_params(f.params)
+                ctx.set_solver(0)
+                assert same(got, want), (name, s, solver, int((got != want).sum()))
