@@ -14,7 +14,7 @@ struct glu_ctx {
     unsigned long long launches = 0;
     unsigned long long* d_counters = nullptr;  // [0] = fp64 fallback pixels
     // Grow-only scratch slots (device memory).
-    static constexpr int kSlots = 16;
+    static constexpr int kSlots = 20;
     void* buf[kSlots] = {};
     size_t cap[kSlots] = {};
     // Grow-only pinned host slots.
@@ -34,7 +34,7 @@ namespace glu_cu {
 enum Slot {
     S_HIGH = 0, S_LOW, S_PARAMS, S_OUT, S_ERR, S_AUX, S_PIX,
     S_CCL_LABEL, S_CCL_LIST, S_CCL_OFF, S_CCL_MISC, S_TRIAL, S_TRIAL2, S_TRIAL3,
-    S_SPARE1, S_SPARE2
+    S_SPARE1, S_SPARE2, S_PACKED
 };
 
 void set_error(const std::string& msg);
@@ -53,6 +53,8 @@ struct SolveArgs {
     int clamp;
     float* out;
     unsigned long long* fallbacks;
+    unsigned sdiv;  // ceil(2^32 / s) when W, H < 2^16 (x / s = umulhi(x, sdiv)), else 0
+    float epsf;     // (float)eps for the fp32 filter
 };
 
 // Launchers (return cudaError_t of the launch).

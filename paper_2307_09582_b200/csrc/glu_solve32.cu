@@ -7,11 +7,21 @@
 // candidate of a different colour by more than the bound is provably the
 // reference's choice (candidates of identical colour evaluate identically in
 // any precision, and the first-index tie-break keeps the earliest of them).
-// Otherwise the pixel is queued in shared memory and re-solved at the end of
-// the CTA with the reference's exact double-precision expressions
-// (glu_math.cuh), one pixel per thread, so the rare fallbacks do not diverge
-// the main pass.  The stored weight is always recomputed in double in the
-// reference's operation order, so params are bit-identical.
+// Otherwise the pixel takes the reference's exact double-precision path
+// (glu_math.cuh) in place; such pixels are rare (~0.05% on the BASELINE
+// scenes), so the divergence costs nothing measurable.  The stored weight is
+// always recomputed in double in the reference's operation order, so params
+// are bit-identical.
+//
+// Layout: the LR image is first packed (k_pack_low) into float4 cells with a
+// border of h = S/2 cells holding +inf on every side.  Out-of-grid candidates
+// then have inf distances and NaN objectives, which never win or tie, so every
+// window is a full S x S block read with LDG.128 at compile-time offsets (the
+// packed LR image is small and L1/L2-resident; neighbouring pixels share
+// cells).  No shared memory, no barriers: every warp is independent.  Each
+// stage tracks the best and the second-best value in the same pass; only when
+// the second is inside the error bound of the best does a (rare) scan check
+// whether the close candidates have the winner's exact colour.
 //
 // Error bounds (u = 2^-24, derivation in DESIGN.md "fp32 filter"):
 //   stage A  q_j = |I_j - I_p|^2:            |q32 - q| <= 6u q
@@ -27,26 +37,36 @@ namespace glu_cu {
 
 namespace {
 
-constexpr int kTX = 32, kTY = 8, kThreads = kTX * kTY;
+constexpr int kThreads = 128;
+#ifndef GLU_SOLVE_MIN_BLOCKS
+#define GLU_SOLVE_MIN_BLOCKS 8
+#endif
 constexpr float kU = 5.9604645e-08f;  // 2^-24
 constexpr float kCA = 32.0f;          // stage A relative margin (in u)
 constexpr float kC1 = 128.0f, kC2 = 32.0f, kC3 = 64.0f;
-
-struct Tile4 {
-    const float4* tile;
-    int ncx, nwx, tx0, ty0;
-    __device__ __forceinline__ const float* operator[](int i) const {
-        const int r = i / nwx, q = i - r * nwx;
-        return reinterpret_cast<const float*>(tile + (ty0 + r) * ncx + tx0 + q);
-    }
-};
+constexpr float kInf = __builtin_huge_valf();
 
 __device__ __forceinline__ bool same_rgb(float4 a, float4 b) {
     return a.x == b.x && a.y == b.y && a.z == b.z;
 }
 
+// MUFU approximations (rel. error <= 2^-22.9); arguments are kept normal by
+// the callers, so flush-to-zero never applies.
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+// MUFU.SQRT: sqrt(0) = 0, sqrt(inf) = inf (the sentinel's weight is then NaN).
 __device__ __forceinline__ float fast_sqrt(float q) {
-    return q * rsqrtf(fmaxf(q, 1e-37f));  // q = 0 -> 0
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(q));
+    return r;
 }
 
 // Exact reference weight for the chosen pair (upsample.cpp:28-33, 61).
@@ -56,188 +76,193 @@ __device__ __forceinline__ float weight64(const float* ip, float4 ca, float4 cb,
     return float(db / (da + db + eps));
 }
 
-template <int S, int MODE>
-__global__ void __launch_bounds__(kThreads) k_solve32(SolveArgs a, int forceFallback) {
-    constexpr int N = S * S;
-    constexpr int h = S / 2;
-    extern __shared__ float4 tile[];
-    __shared__ int fbList[kThreads];
-    __shared__ int fbCount;
+__device__ __forceinline__ int div_s(int v, const SolveArgs& a) {
+    return a.sdiv ? int(__umulhi(unsigned(v), a.sdiv)) : v / a.s;
+}
 
-    const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
-    const int cx0 = max(0, x0 / a.s - h), cy0 = max(0, y0 / a.s - h);
-    const int cx1 = min(a.lw - 1, min(x0 + kTX - 1, a.W - 1) / a.s + h);
-    const int cy1 = min(a.lh - 1, min(y0 + kTY - 1, a.H - 1) / a.s + h);
-    const int ncx = cx1 - cx0 + 1, ncy = cy1 - cy0 + 1;
-    if (threadIdx.x == 0) fbCount = 0;
-    for (int i = threadIdx.x; i < ncx * ncy; i += kThreads) {
-        const int ty = i / ncx, tx = i - ty * ncx;
-        const float* src = a.low + 3 * (size_t(cy0 + ty) * a.lw + cx0 + tx);
-        tile[i] = make_float4(__ldg(src), __ldg(src + 1), __ldg(src + 2), 0.0f);
-    }
-    __syncthreads();
+// Candidate (r, c) of the window whose top-left is `win` (packed pitch `pw`).
+template <int S>
+__device__ __forceinline__ float4 cand(const float4* win, int pw, int j) {
+    return __ldg(win + (j / S) * pw + (j % S));
+}
 
-    const int x = x0 + (threadIdx.x % kTX), y = y0 + (threadIdx.x / kTX);
-    const bool live = x < a.W && y < a.H;
-    const size_t p = size_t(y) * a.W + x;
-    const int cx = x / a.s, cy = y / a.s;
-    const int wx0 = max(0, cx - h), wy0 = max(0, cy - h);
-    const int nwx = min(a.lw - 1, cx + h) - wx0 + 1, nwy = min(a.lh - 1, cy + h) - wy0 + 1;
-    const float4* win = tile + (wy0 - cy0) * ncx + (wx0 - cx0);
+// The truncated window of the packed image as the reference's raster list.
+struct PackedWindow {
+    const float4* win;  // packed cell of (x0, y0)
+    int pw, nwx;
+    __device__ __forceinline__ const float* operator[](int i) const {
+        const int r = i / nwx, q = i - r * nwx;
+        return reinterpret_cast<const float*>(win + r * pw + q);
+    }
+};
 
-    if (live) {
-        const float ip[3] = {__ldg(a.high + 3 * p), __ldg(a.high + 3 * p + 1),
-                             __ldg(a.high + 3 * p + 2)};
-        // ---- stage A: a = first argmin |I_j - I_p| (compared as squares) ----
-        float q[N];
-        float qa = __int_as_float(0x7f800000), qmax = 0.0f;
-        int ja = 0;
-#pragma unroll
-        for (int r = 0; r < S; ++r)
-#pragma unroll
-            for (int c = 0; c < S; ++c) {
-                const int j = r * S + c;
-                q[j] = __int_as_float(0x7f800000);
-                if (r < nwy && c < nwx) {
-                    const float4 v = win[r * ncx + c];
-                    const float e0 = v.x - ip[0], e1 = v.y - ip[1], e2 = v.z - ip[2];
-                    const float qq = __fmaf_rn(e2, e2, __fmaf_rn(e1, e1, __fmul_rn(e0, e0)));
-                    q[j] = qq;
-                    if (qq < qa) {
-                        qa = qq;
-                        ja = j;
-                    }
-                    qmax = fmaxf(qmax, qq);
-                }
-            }
-        const float4 ca = win[(ja / S) * ncx + (ja % S)];
-        const float ea0 = ca.x - ip[0], ea1 = ca.y - ip[1], ea2 = ca.z - ip[2];
-        bool ok = !forceFallback;
-        if (qa < 1e-27f && !(ea0 == 0.0f && ea1 == 0.0f && ea2 == 0.0f)) ok = false;
-        {
-            const float lim = __fmaf_rn(qa, kCA * kU, qa) + 1e-36f;
-#pragma unroll
-            for (int j = 0; j < N; ++j)
-                if (j != ja && q[j] <= lim && !same_rgb(win[(j / S) * ncx + (j % S)], ca))
-                    ok = false;
-        }
-        int jb = ja;
-        float w = 1.0f;
-        if (MODE == GLU_MODE_FAST && ok) {
-            // ---- stage B: b = first argmin of the objective at w_j ----------
-            const float da = fast_sqrt(qa);
-            const float eps = float(a.eps);
-            float obj[N];
-            float best = __int_as_float(0x7f800000);
-#pragma unroll
-            for (int r = 0; r < S; ++r)
-#pragma unroll
-                for (int c = 0; c < S; ++c) {
-                    const int j = r * S + c;
-                    obj[j] = __int_as_float(0x7f800000);
-                    if (r < nwy && c < nwx) {
-                        const float4 v = win[r * ncx + c];
-                        const float e0 = v.x - ip[0], e1 = v.y - ip[1], e2 = v.z - ip[2];
-                        const float dj = fast_sqrt(q[j]);
-                        const float wj = __fdividef(dj, da + dj + eps);
-                        const float v0 = __fmaf_rn(wj, ea0 - e0, e0);
-                        const float v1 = __fmaf_rn(wj, ea1 - e1, e1);
-                        const float v2 = __fmaf_rn(wj, ea2 - e2, e2);
-                        const float o = __fmaf_rn(eps * wj, wj,
-                                                  __fmaf_rn(v2, v2, __fmaf_rn(v1, v1, v0 * v0)));
-                        obj[j] = o;
-                        if (o < best) {
-                            best = o;
-                            jb = j;
-                        }
-                    }
-                }
-            const float4 cb = win[(jb / S) * ncx + (jb % S)];
-            if (best == 0.0f) {
-                // exact zero: only an exact colour match (w = 0, v = 0) gets there
-                ok = cb.x == ip[0] && cb.y == ip[1] && cb.z == ip[2];
-            } else {
-                const float smax = da + fast_sqrt(qmax);
-                const float rt = rsqrtf(best), st = best * rt;
-                const float mb = kU * (kC1 * st * smax + kC2 * best + kC3 * eps);
-                const float alpha = 1.0f - kU * (0.5f * kC1 * smax * rt + kC2);
-                const float rhs = best + mb + kU * (0.5f * kC1 * smax * st + kC3 * eps);
-#pragma unroll
-                for (int j = 0; j < N; ++j)
-                    if (j != jb && obj[j] * alpha <= rhs &&
-                        !same_rgb(win[(j / S) * ncx + (j % S)], cb))
-                        ok = false;
-            }
-            if (ok) w = weight64(ip, ca, cb, a.eps);
-        }
-        if (ok) {
-            const uint32_t ia = uint32_t(wy0 + ja / S) * uint32_t(a.lw) + uint32_t(wx0 + ja % S);
-            const uint32_t ib = uint32_t(wy0 + jb / S) * uint32_t(a.lw) + uint32_t(wx0 + jb % S);
-            if (a.params) {
-                unsigned* o = reinterpret_cast<unsigned*>(a.params + p);
-                o[0] = ia;
-                o[1] = ib;
-                o[2] = __float_as_uint(w);
-            }
-            if (a.lowT) {
-                const int C = a.channels;
-                for (int k = 0; k < C; ++k)
-                    a.out[C * p + k] = lerp_clamp(w, __ldg(a.lowT + size_t(C) * ia + k),
-                                                  __ldg(a.lowT + size_t(C) * ib + k),
-                                                  a.clamp != 0);
-            }
-        } else {
-            fbList[atomicAdd(&fbCount, 1)] = threadIdx.x;
-        }
+__global__ void k_pack_low(const float* __restrict__ low, int lw, int lh, int h,
+                           float4* __restrict__ packed) {
+    const int pw = lw + 2 * h, ph = lh + 2 * h;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= pw * ph) return;
+    const int y = i / pw - h, x = i % pw - h;
+    float4 v = make_float4(kInf, kInf, kInf, 0.0f);
+    if (x >= 0 && y >= 0 && x < lw && y < lh) {
+        const float* s = low + 3 * (size_t(y) * lw + x);
+        v = make_float4(s[0], s[1], s[2], 0.0f);
     }
-    __syncthreads();
-    // ---- exact double-precision re-solve of the uncertain pixels ---------------
-    const int nfb = fbCount;
-    for (int i = threadIdx.x; i < nfb; i += kThreads) {
-        const int t = fbList[i];
-        const int fx = x0 + (t % kTX), fy = y0 + (t / kTX);
-        const size_t fp = size_t(fy) * a.W + fx;
-        const int fcx = fx / a.s, fcy = fy / a.s;
-        const int fwx0 = max(0, fcx - h), fwy0 = max(0, fcy - h);
-        const int fnwx = min(a.lw - 1, fcx + h) - fwx0 + 1;
-        const int fnwy = min(a.lh - 1, fcy + h) - fwy0 + 1;
-        const float ip[3] = {a.high[3 * fp], a.high[3 * fp + 1], a.high[3 * fp + 2]};
-        Tile4 tw{tile, ncx, fnwx, fwx0 - cx0, fwy0 - cy0};
-        const Pick pk = MODE == GLU_MODE_GNU ? pick_gnu64(ip, tw, fnwx * fnwy)
-                                             : pick_fast64(ip, tw, fnwx * fnwy, a.eps);
-        const int ar = pk.ai / fnwx, br = pk.bi / fnwx;
-        const uint32_t ia = uint32_t(fwy0 + ar) * uint32_t(a.lw) + uint32_t(fwx0 + pk.ai - ar * fnwx);
-        const uint32_t ib = uint32_t(fwy0 + br) * uint32_t(a.lw) + uint32_t(fwx0 + pk.bi - br * fnwx);
-        const float w = float(pk.w);
-        if (a.params) {
-            unsigned* o = reinterpret_cast<unsigned*>(a.params + fp);
-            o[0] = ia;
-            o[1] = ib;
-            o[2] = __float_as_uint(w);
-        }
-        if (a.lowT) {
-            const int C = a.channels;
-            for (int k = 0; k < C; ++k)
-                a.out[C * fp + k] = lerp_clamp(w, a.lowT[size_t(C) * ia + k],
-                                               a.lowT[size_t(C) * ib + k], a.clamp != 0);
-        }
-    }
-    if (threadIdx.x == 0 && nfb > 0 && a.fallbacks) atomicAdd(a.fallbacks, (unsigned long long)nfb);
+    packed[i] = v;
 }
 
 template <int S, int MODE>
-cudaError_t launch_t(glu_ctx* ctx, const SolveArgs& a, int force) {
-    const int h = S / 2;
-    const int ncx = (kTX - 1) / a.s + 2 + 2 * h, ncy = (kTY - 1) / a.s + 2 + 2 * h;
-    const size_t smem = size_t(ncx) * ncy * sizeof(float4);
-    if (smem > 40 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(k_solve32<S, MODE>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(smem) + 4096);
-        if (e != cudaSuccess) return e;
+__global__ void __launch_bounds__(kThreads, GLU_SOLVE_MIN_BLOCKS) k_solve32(SolveArgs a, const float4* packed,
+                                                          int forceFallback) {
+    constexpr int N = S * S;
+    constexpr int h = S / 2;
+    constexpr int NE = S == 3 ? N : 1;  // S = 3 keeps e_j in registers; S = 5 reloads
+    const int pw = a.lw + 2 * h;
+    // 32 x 4 pixel tiles: a warp covers 32 consecutive pixels of one row
+    const int x = blockIdx.x * 32 + (threadIdx.x & 31);
+    const int y = blockIdx.y * (kThreads / 32) + (threadIdx.x >> 5);
+    if (x >= a.W || y >= a.H) return;
+    const size_t p = size_t(y) * a.W + x;
+    const int cx = div_s(x, a), cy = div_s(y, a);
+    // packed cell (cx - h, cy - h) is at padded (cx, cy)
+    const float4* win = packed + size_t(cy) * pw + cx;
+
+    const float ip0 = __ldg(a.high + 3 * p), ip1 = __ldg(a.high + 3 * p + 1),
+                ip2 = __ldg(a.high + 3 * p + 2);
+    // ---- stage A: a = first argmin |I_j - I_p| (compared as squares) --------
+    float q[N], e0[NE], e1[NE], e2[NE];
+    float m1 = kInf, m2 = kInf;
+    int ja = 0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        const float4 v = cand<S>(win, pw, j);
+        const float d0 = v.x - ip0, d1 = v.y - ip1, d2 = v.z - ip2;
+        if (S == 3) {
+            e0[j % NE] = d0;
+            e1[j % NE] = d1;
+            e2[j % NE] = d2;
+        }
+        const float qq = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmul_rn(d0, d0)));
+        q[j] = qq;
+        const bool lt = qq < m1;
+        m2 = lt ? m1 : fminf(m2, qq);
+        m1 = lt ? qq : m1;
+        ja = lt ? j : ja;
     }
-    dim3 grid((a.W + kTX - 1) / kTX, (a.H + kTY - 1) / kTY);
-    k_solve32<S, MODE><<<grid, kThreads, smem, ctx->stream>>>(a, force);
+    const float4 ca = cand<S>(win, pw, ja);
+    const float ea0 = ca.x - ip0, ea1 = ca.y - ip1, ea2 = ca.z - ip2;
+    const bool exactA = ca.x == ip0 && ca.y == ip1 && ca.z == ip2;
+    // NaN inputs and underflow-sized distances go to the exact path.
+    bool ok = !forceFallback && m1 < kInf && ip0 == ip0 && ip1 == ip1 && ip2 == ip2 &&
+              (m1 >= 1e-27f || exactA);
+    if (ok && m2 <= __fmaf_rn(m1, kCA * kU, m1) + 1e-36f) {
+        const float lim = __fmaf_rn(m1, kCA * kU, m1) + 1e-36f;
+        for (int j = 0; j < N; ++j)
+            if (j != ja && !(q[j] > lim) && !same_rgb(cand<S>(win, pw, j), ca)) ok = false;
+    }
+    int jb = ja;
+    float w = 1.0f;
+    if (MODE == GLU_MODE_FAST && ok) {
+        // ---- stage B: b = first argmin of the objective at w_j --------------
+        const float da = fast_sqrt(m1);
+        const float eps = a.epsf;
+        float b1 = kInf, b2 = kInf, dmax = 0.0f;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            float d0, d1, d2;
+            if (S == 3) {
+                d0 = e0[j % NE];
+                d1 = e1[j % NE];
+                d2 = e2[j % NE];
+            } else {
+                const float4 v = cand<S>(win, pw, j);
+                d0 = v.x - ip0;
+                d1 = v.y - ip1;
+                d2 = v.z - ip2;
+            }
+            const float dj = fast_sqrt(q[j]);
+            dmax = fmaxf(dmax, dj);  // NaN (outside the grid) is ignored
+            const float wj = dj * rcp_approx((da + dj) + eps);
+            const float v0 = __fmaf_rn(wj, ea0 - d0, d0);
+            const float v1 = __fmaf_rn(wj, ea1 - d1, d1);
+            const float v2 = __fmaf_rn(wj, ea2 - d2, d2);
+            const float o =
+                __fmaf_rn(eps * wj, wj, __fmaf_rn(v2, v2, __fmaf_rn(v1, v1, v0 * v0)));
+            const bool lt = o < b1;
+            b2 = lt ? b1 : fminf(b2, o);
+            b1 = lt ? o : b1;
+            jb = lt ? j : jb;
+        }
+        const float4 cb = cand<S>(win, pw, jb);
+        if (b1 == 0.0f) {
+            // exact zero: only an exact colour match (w = 0, v = 0) gets there
+            ok = cb.x == ip0 && cb.y == ip1 && cb.z == ip2;
+        } else {
+            const float smax = da + dmax;
+            const float bb = fmaxf(b1, 1e-30f);
+            const float rt = rsqrt_approx(bb), st = bb * rt;
+            const float mb = kU * (kC1 * st * smax + kC2 * b1 + kC3 * eps);
+            // near(o): o (1 - u(C1 smax / (2 sqrt b1) + C2)) <= b1 + mb + u(C1 smax sqrt(b1)/2 + C3 eps)
+            const float alpha = 1.0f - kU * (0.5f * kC1 * smax * rt + kC2);
+            const float rhs = b1 + mb + kU * (0.5f * kC1 * smax * st + kC3 * eps);
+            if (b2 * alpha <= rhs || alpha <= 0.0f) {
+                // rare: recompute the objectives and compare colours
+                for (int j = 0; j < N; ++j) {
+                    if (j == jb) continue;
+                    const float4 v = cand<S>(win, pw, j);
+                    const float d0 = v.x - ip0, d1 = v.y - ip1, d2 = v.z - ip2;
+                    const float dj = fast_sqrt(q[j]);
+                    const float wj = dj * rcp_approx((da + dj) + eps);
+                    const float v0 = __fmaf_rn(wj, ea0 - d0, d0);
+                    const float v1 = __fmaf_rn(wj, ea1 - d1, d1);
+                    const float v2 = __fmaf_rn(wj, ea2 - d2, d2);
+                    const float o = __fmaf_rn(eps * wj, wj,
+                                              __fmaf_rn(v2, v2, __fmaf_rn(v1, v1, v0 * v0)));
+                    if ((o * alpha <= rhs || alpha <= 0.0f) && !same_rgb(v, cb)) ok = false;
+                }
+            }
+        }
+        if (ok) {
+            const float ip[3] = {ip0, ip1, ip2};
+            w = weight64(ip, ca, cb, a.eps);
+        }
+    }
+    uint32_t ia, ib;
+    if (ok) {
+        ia = uint32_t(cy - h + ja / S) * uint32_t(a.lw) + uint32_t(cx - h + ja % S);
+        ib = uint32_t(cy - h + jb / S) * uint32_t(a.lw) + uint32_t(cx - h + jb % S);
+    } else {
+        // ---- exact double-precision path (upsample.cpp:49-71, 93-104) -------
+        const int wx0 = max(0, cx - h), wy0 = max(0, cy - h);
+        const int nwx = min(a.lw - 1, cx + h) - wx0 + 1;
+        const int nwy = min(a.lh - 1, cy + h) - wy0 + 1;
+        const float ip[3] = {ip0, ip1, ip2};
+        PackedWindow pwin{packed + size_t(wy0 + h) * pw + (wx0 + h), pw, nwx};
+        const Pick pk = MODE == GLU_MODE_GNU ? pick_gnu64(ip, pwin, nwx * nwy)
+                                             : pick_fast64(ip, pwin, nwx * nwy, a.eps);
+        const int ar = pk.ai / nwx, br = pk.bi / nwx;
+        ia = uint32_t(wy0 + ar) * uint32_t(a.lw) + uint32_t(wx0 + pk.ai - ar * nwx);
+        ib = uint32_t(wy0 + br) * uint32_t(a.lw) + uint32_t(wx0 + pk.bi - br * nwx);
+        w = float(pk.w);
+        if (a.fallbacks) atomicAdd(a.fallbacks, 1ull);
+    }
+    if (a.params) {
+        unsigned* o = reinterpret_cast<unsigned*>(a.params + p);
+        o[0] = ia;
+        o[1] = ib;
+        o[2] = __float_as_uint(w);
+    }
+    if (a.lowT) {
+        const int C = a.channels;
+        for (int k = 0; k < C; ++k)
+            a.out[C * p + k] = lerp_clamp(w, __ldg(a.lowT + size_t(C) * ia + k),
+                                          __ldg(a.lowT + size_t(C) * ib + k), a.clamp != 0);
+    }
+}
+
+template <int S, int MODE>
+cudaError_t launch_t(glu_ctx* ctx, const SolveArgs& a, const float4* packed, int force) {
+    dim3 grid((a.W + 31) / 32, (a.H + kThreads / 32 - 1) / (kThreads / 32));
+    k_solve32<S, MODE><<<grid, kThreads, 0, ctx->stream>>>(a, packed, force);
     ++ctx->launches;
     return cudaGetLastError();
 }
@@ -248,12 +273,25 @@ bool solve32_supported(int mode, int S) {
     return (mode == GLU_MODE_FAST || mode == GLU_MODE_GNU) && (S == 3 || S == 5);
 }
 
-cudaError_t launch_solve32(glu_ctx* ctx, const SolveArgs& a, int forceFallback) {
+cudaError_t launch_solve32(glu_ctx* ctx, const SolveArgs& a0, int forceFallback) {
+    SolveArgs a = a0;
+    // x / s as a multiply-high: exact for x, s < 2^16 with m = ceil(2^32 / s).
+    a.sdiv = (a.W < 65536 && a.H < 65536)
+                 ? unsigned((0x100000000ull + unsigned(a.s) - 1) / unsigned(a.s))
+                 : 0u;
+    a.epsf = float(a.eps);
+    const int h = a.S / 2;
+    const size_t cells = size_t(a.lw + 2 * h) * (a.lh + 2 * h);
+    float4* packed = static_cast<float4*>(scratch(ctx, S_PACKED, cells * sizeof(float4)));
+    if (!packed) return cudaErrorMemoryAllocation;
+    k_pack_low<<<unsigned((cells + 255) / 256), 256, 0, ctx->stream>>>(a.low, a.lw, a.lh, h,
+                                                                        packed);
+    ++ctx->launches;
     if (a.mode == GLU_MODE_GNU)
-        return a.S == 3 ? launch_t<3, GLU_MODE_GNU>(ctx, a, forceFallback)
-                        : launch_t<5, GLU_MODE_GNU>(ctx, a, forceFallback);
-    return a.S == 3 ? launch_t<3, GLU_MODE_FAST>(ctx, a, forceFallback)
-                    : launch_t<5, GLU_MODE_FAST>(ctx, a, forceFallback);
+        return a.S == 3 ? launch_t<3, GLU_MODE_GNU>(ctx, a, packed, forceFallback)
+                        : launch_t<5, GLU_MODE_GNU>(ctx, a, packed, forceFallback);
+    return a.S == 3 ? launch_t<3, GLU_MODE_FAST>(ctx, a, packed, forceFallback)
+                    : launch_t<5, GLU_MODE_FAST>(ctx, a, packed, forceFallback);
 }
 
 }  // namespace glu_cu

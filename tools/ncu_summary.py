@@ -1,0 +1,136 @@
+"""Summarise ncu outputs into profiles/ (tracked).
+
+  python tools/ncu_summary.py launches <launches.csv> <out.md>
+  python tools/ncu_summary.py kernel <report.ncu-rep> <out.md> [--traffic-key KEY]
+
+`launches`: per-kernel launch count, total / mean device time and share of the
+captured launches (ncu's launch list is cold-cache and serialised: compare
+shares, not absolutes).  `kernel`: the SOL / occupancy / instruction / DRAM
+metrics of one `--set full` capture plus the executed-instruction mix from the
+SASS source page; with --traffic-key the per-launch DRAM bytes are also stored
+in profiles/traffic.json for bench.py's roofline.traffic.
+"""
+from __future__ import annotations
+
+import collections
+import csv
+import io
+import json
+import os
+import re
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def short(name: str) -> str:
+    name = re.sub(r"\(.*$", "", name)
+    name = name.replace("glu_cu::<unnamed>::", "").replace("unnamed>::", "")
+    return name.strip()
+
+
+def launches(path: str, out: str) -> None:
+    rows = [r for r in csv.reader(open(path)) if len(r) > 10]
+    hdr = rows[0]
+    ik, iv = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    agg = collections.defaultdict(list)
+    for r in rows[1:]:
+        try:
+            agg[short(r[ik])].append(float(r[iv]) / 1e3)
+        except ValueError:
+            pass
+    total = sum(sum(v) for v in agg.values())
+    lines = [f"# ncu launch list: `{os.path.basename(path)}`", "",
+             "gpu__time_duration.sum per launch, --clock-control none (cold-cache, serialised).",
+             "", "| kernel | launches | total us | mean us | share |", "|---|---:|---:|---:|---:|"]
+    for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
+        lines.append(f"| `{k}` | {len(v)} | {sum(v):.1f} | {sum(v) / len(v):.2f} | "
+                     f"{100 * sum(v) / total:.1f}% |")
+    lines.append(f"| **total** | {sum(len(v) for v in agg.values())} | {total:.1f} | | 100% |")
+    open(out, "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
+WANT = [
+    "Duration", "SM Frequency", "Elapsed Cycles", "Compute (SM) Throughput", "Memory Throughput",
+    "DRAM Throughput", "L1/TEX Hit Rate", "L2 Hit Rate", "Executed Ipc Active", "Issue Slots Busy",
+    "Registers Per Thread", "Theoretical Occupancy", "Achieved Occupancy", "Executed Instructions",
+    "Warp Cycles Per Issued Instruction", "Eligible Warps Per Scheduler", "No Eligible",
+    "Avg. Active Threads Per Warp", "Grid Size", "Block Size",
+]
+
+
+def kernel(rep: str, out: str, traffic_key: str | None) -> None:
+    det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(det)))
+    hdr = rows[0]
+    im, iu, iv, ik = (hdr.index("Metric Name"), hdr.index("Metric Unit"),
+                      hdr.index("Metric Value"), hdr.index("Kernel Name"))
+    kname = short(rows[1][ik]) if len(rows) > 1 else "?"
+    vals = {}
+    for r in rows[1:]:
+        if r[im] in WANT and r[im] not in vals:
+            vals[r[im]] = (r[iv], r[iu])
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rr = list(csv.reader(io.StringIO(raw)))
+    rawd = dict(zip(rr[0], rr[2])) if len(rr) > 2 else {}
+    units = dict(zip(rr[0], rr[1])) if len(rr) > 1 else {}
+
+    def rawval(name):
+        v = rawd.get(name)
+        if v is None:
+            return None
+        v = float(v.replace(",", ""))
+        u = units.get(name, "")
+        return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+
+    dram_r, dram_w = rawval("dram__bytes_read.sum"), rawval("dram__bytes_write.sum")
+    sass = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"],
+                          capture_output=True, text=True).stdout
+    srows = list(csv.reader(io.StringIO(sass)))
+    mix = collections.Counter()
+    if len(srows) > 2:
+        h2 = srows[1]
+        ie, isrc = h2.index("Instructions Executed"), h2.index("Source")
+        for r in srows[2:]:
+            try:
+                n = int(r[ie])
+            except (ValueError, IndexError):
+                continue
+            toks = r[isrc].split()
+            if not toks:
+                continue
+            op = toks[1] if toks[0].startswith("@") and len(toks) > 1 else toks[0]
+            mix[op.split(".")[0]] += n
+    lines = [f"# ncu --set full: `{kname}` ({os.path.basename(rep)})", "",
+             "| metric | value |", "|---|---|"]
+    for k in WANT:
+        if k in vals:
+            lines.append(f"| {k} | {vals[k][0]} {vals[k][1]} |")
+    if dram_r is not None:
+        lines.append(f"| dram__bytes_read.sum | {dram_r:.4g} B |")
+        lines.append(f"| dram__bytes_write.sum | {dram_w:.4g} B |")
+    tot = sum(mix.values())
+    if tot:
+        lines += ["", f"Executed warp instructions by opcode (total {tot}):", "",
+                  "| opcode | warp instr | share |", "|---|---:|---:|"]
+        for op, n in mix.most_common(20):
+            lines.append(f"| {op} | {n} | {100 * n / tot:.1f}% |")
+    open(out, "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+    if traffic_key and dram_r is not None:
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        d = json.load(open(tp)) if os.path.exists(tp) else {}
+        d[traffic_key] = dram_r + dram_w
+        json.dump(d, open(tp, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "launches":
+        launches(sys.argv[2], sys.argv[3])
+    else:
+        key = sys.argv[sys.argv.index("--traffic-key") + 1] if "--traffic-key" in sys.argv else None
+        kernel(sys.argv[2], sys.argv[3], key)
