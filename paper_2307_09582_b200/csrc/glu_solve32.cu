@@ -180,8 +180,9 @@ __global__ void __launch_bounds__(kThreads, GLU_SOLVE_MIN_BLOCKS) k_solve32(Solv
                 d2 = v.z - ip2;
             }
             const float dj = fast_sqrt(q[j]);
-            dmax = fmaxf(dmax, dj);  // NaN (outside the grid) is ignored
             const float wj = dj * rcp_approx((da + dj) + eps);
+            // outside the grid dj = inf and wj = inf * 0 = NaN, which fmaxf ignores
+            dmax = fmaxf(dmax, __fmaf_rn(wj, 0.0f, dj));
             const float v0 = __fmaf_rn(wj, ea0 - d0, d0);
             const float v1 = __fmaf_rn(wj, ea1 - d1, d1);
             const float v2 = __fmaf_rn(wj, ea2 - d2, d2);

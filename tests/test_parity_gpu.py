@@ -268,3 +268,21 @@ def test_fp32_filter_matches_oracle_on_stress_images(glu, oracle, mode, S):
                 got = host_params(f.params)
                 ctx.set_solver(0)
                 assert same(got, want), (name, s, solver, int((got != want).sum()))
+
+
+def test_reference_unit_tests_pass_against_dropin_api(glu):
+    """The reference's own unit tests (proj/tests/unit/{grid,upsample,jointopt,
+    parallel}_test.cpp, 47 cases) compiled UNCHANGED against include/glu and
+    linked with lib/libglu.so (oracle/Makefile `reftests`, built where
+    /root/reference exists; the binary travels with the tree)."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "oracle", "_ref", "ref_unit_tests_b200")
+    if not os.path.exists(exe):
+        if not os.path.isdir("/root/reference/proj/tests/unit"):
+            pytest.skip("ref_unit_tests_b200 not built and /root/reference absent")
+        subprocess.run(["make", "-s", "-C", os.path.join(root, "oracle"), "reftests"], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "47 passed | 0 failed" in r.stdout, r.stdout
