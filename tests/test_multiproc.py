@@ -1,0 +1,84 @@
+"""World-size-2 CPU (gloo) tests of the multi-GPU host logic: frame sharding,
+row bands with LR halos, and the max-over-ranks timing reduction bench.py uses."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2307_09582_b200 import sharding
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # frame sharding: disjoint clips, nothing exchanged on the data path
+        mine = sharding.frame_seeds(rank, world, 16, 3)
+        got = [None] * world
+        dist.all_gather_object(got, mine)
+        flat = [x for r in got for x in r]
+        assert len(set(flat)) == 16 * world
+        # bands: every rank derives the same partition; owned rows tile the grid
+        bands = sharding.row_bands(4320, 16, 3, world)
+        allb = [None] * world
+        dist.all_gather_object(allb, bands[rank])
+        assert [b.lr_rows for b in allb] == [b.lr_rows for b in bands]
+        # halo exchange of LR rows: each rank sends its edge rows to neighbours
+        lw = 480
+        me = bands[rank]
+        block = torch.full(((me.lr_rows[1] - me.lr_rows[0]), lw), float(rank))
+        halo = {}
+        reqs = []
+        for nb in (rank - 1, rank + 1):
+            if 0 <= nb < world:
+                edge = block[:1] if nb < rank else block[-1:]
+                reqs.append(dist.isend(edge.contiguous(), nb))
+                buf = torch.empty((1, lw))
+                reqs.append(dist.irecv(buf, nb))
+                halo[nb] = buf
+        for r in reqs:
+            r.wait()
+        for nb, buf in halo.items():
+            assert torch.all(buf == float(nb))
+        # max-over-ranks timing (bench.py)
+        t = torch.tensor([10.0 + rank])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        q.put((rank, float(t.item())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_sharding_and_halo_exchange():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=10) for _ in range(2))
+    assert res == [(0, 11.0), (1, 11.0)]
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_row_bands_partition_c4(world):
+    bands = sharding.row_bands(4320, 16, 3, world)
+    rows = [r for b in bands for r in range(*b.lr_rows)]
+    assert rows == list(range(270))
+    assert all(b.hr_rows[0] % 16 == 0 for b in bands)
+    sizes = [b.lr_rows[1] - b.lr_rows[0] for b in bands]
+    assert max(sizes) - min(sizes) <= 1
+    if world == 8:
+        assert sizes == [34] * 6 + [33] * 2
+        assert sharding.halo_bytes(bands[3], 480) == 2 * 480 * 12  # 5,760 B per side
