@@ -102,8 +102,11 @@ int glu_ctx_synchronize(glu_ctx* ctx);
  *     the fp64 reference-order kernel otherwise;
  *   1 the fp64 reference-order kernel everywhere;
  *   2 fp32 filter with every pixel forced through the fp64 verify (testing).
+ * GLU_OPT_TRIALS selects the joint-loop trial schedule:
+ *   0 (default) conflict-aware parallel schedule over all SMs;
+ *   1 one CTA runs the trials in sweep order.
  * All settings produce bit-identical results. */
-enum glu_option { GLU_OPT_SOLVER = 1 };
+enum glu_option { GLU_OPT_SOLVER = 1, GLU_OPT_TRIALS = 2 };
 int glu_ctx_set_option(glu_ctx* ctx, int option, int value);
 /* Number of kernels this context has launched (bench.py's gpu_launches). */
 unsigned long long glu_ctx_launch_count(glu_ctx* ctx);

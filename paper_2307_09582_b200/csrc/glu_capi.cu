@@ -235,6 +235,11 @@ int glu_ctx_set_option(glu_ctx* ctx, int option, int value) {
         ctx->solver = value;
         return GLU_OK;
     }
+    if (option == GLU_OPT_TRIALS) {
+        if (value < 0 || value > 1) return einval("GLU_OPT_TRIALS: value must be 0 or 1");
+        ctx->trials = value;
+        return GLU_OK;
+    }
     return einval("unknown option");
 }
 

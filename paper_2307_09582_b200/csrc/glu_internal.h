@@ -23,6 +23,8 @@ struct glu_ctx {
     // GLU_OPT_SOLVER: 0 auto, 1 fp64 reference-order kernel only, 2 fp32
     // filter with every pixel forced through the fp64 verify path (testing).
     int solver = 0;
+    // GLU_OPT_TRIALS: 0 conflict-aware parallel schedule, 1 one CTA in order.
+    int trials = 0;
     // Copy streams + events of the host frame pipeline (created lazily).
     cudaStream_t h2d = nullptr, d2h = nullptr;
     cudaEvent_t ev[8] = {};
@@ -34,7 +36,7 @@ namespace glu_cu {
 enum Slot {
     S_HIGH = 0, S_LOW, S_PARAMS, S_OUT, S_ERR, S_AUX, S_PIX,
     S_CCL_LABEL, S_CCL_LIST, S_CCL_OFF, S_CCL_MISC, S_TRIAL, S_TRIAL2, S_TRIAL3,
-    S_SPARE1, S_SPARE2, S_PACKED
+    S_SPARE1, S_SPARE2, S_PACKED, S_SCHED, S_SCHED_META
 };
 
 void set_error(const std::string& msg);

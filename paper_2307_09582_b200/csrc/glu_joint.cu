@@ -8,12 +8,25 @@
 // roots; a stable key sort of the raster-ordered mask pixels by component
 // yields each component's ascending pixel list.
 //
-// The trials of one sweep (jointopt.cpp:195-202) are strictly sequential in
-// the reference.  k_trial_sweep runs them in order inside one CTA: each trial
-// is parallel over its pixels, and the accept test e1 <= e0 on the
-// reference's sequentially rounded double sums (150-165) is decided by a
-// parallel double sum plus a rigorous rounding bound, falling back to the
-// exact sequential order only when the two sums are within that bound.
+// Trials (jointopt.cpp:114-180, the loop 195-202) are strictly sequential in
+// the reference.  A trial T_i writes the LR cells Q_i it replaces and the
+// params / errors of the footprints of dilate(Q_i, h); it reads LR cells in
+// dilate(Q_i, 2h) and errors in footprints of dilate(Q_i, h).  Two trials whose
+// cell bounding boxes are more than 2h apart (Chebyshev) therefore touch
+// disjoint state and commute.  k_trial_sched is a persistent, cooperatively
+// launched kernel: CTAs claim trials in sweep order from an atomic counter,
+// wait (acquire) until every earlier trial whose box is within 2h has
+// published its result (release), and run the trial with the whole CTA.
+// Claims are in order and every CTA is resident, so the smallest unfinished
+// trial never waits: no deadlock, and the final state is bit-identical to the
+// sequential loop.  Trials too large for a CTA's private buffers get a
+// whole-grid box (they conflict with everything, so they run alone) and use
+// the global worst-case buffers.
+//
+// The accept test e1 <= e0 compares the reference's sequentially rounded
+// double sums (150-165): the CTA forms parallel fp64 sums and decides when
+// |e1 - e0| exceeds a rigorous bound on parallel-vs-sequential rounding;
+// otherwise one thread redoes both sums in the exact reference order.
 #include <cub/cub.cuh>
 
 #include "glu_internal.h"
@@ -24,7 +37,10 @@ namespace glu_cu {
 namespace {
 
 constexpr uint32_t kNone = 0xffffffffu;
-constexpr int kTrialThreads = 1024;
+constexpr int kSchedThreads = 256;   // CTA size of the parallel trial scheduler
+constexpr int kSeqThreads = 1024;    // CTA size of the sequential (single-CTA) sweep
+constexpr uint32_t kCtaPixels = 16384;  // per-CTA affected-pixel capacity
+constexpr uint32_t kCtaCells = 4096;    // per-CTA replaced-cell capacity
 
 // ---- connected components ---------------------------------------------------
 
@@ -113,7 +129,7 @@ __global__ void k_ccl_offsets(const uint32_t* __restrict__ keys, size_t n, uint3
 
 // ---- trials -------------------------------------------------------------------
 
-struct TrialArgs {
+struct TrialState {
     const float* high;
     float* low;
     glu_pixel_params* field;
@@ -121,18 +137,18 @@ struct TrialArgs {
     int W, H, s, lw, lh, S;
     double eps;
     int mode, literal;
-    const uint32_t* off;
-    const uint32_t* px;
-    int ncomp;
     unsigned long long* cellKey;  // per LR cell, 0 between trials
     uint32_t* cellFlag;           // per LR cell, 0 between trials
     uint8_t* affMark;             // per LR cell, 0 between trials
-    uint32_t* touched;            // replaced cells of the current trial
-    float* oldColor;              // 3 floats per touched cell
-    uint32_t* aff;                // affected pixels, reference order
+    int* result;  // [0] accepted, [1] rejected, [2] sequential-sum fallbacks, [3] last verdict
+};
+
+struct TrialBuffers {
+    uint32_t* touched;  // replaced cells
+    float* oldColor;    // 3 floats per replaced cell
+    uint32_t* aff;      // affected pixels, reference order
     glu_pixel_params* bkParams;
     float* bkE;
-    int* result;  // [0] accepted, [1] rejected, [2] sequential-sum fallbacks, [3] last verdict
 };
 
 struct GlobalLowWindow {
@@ -144,196 +160,304 @@ struct GlobalLowWindow {
     }
 };
 
-__global__ void __launch_bounds__(kTrialThreads) k_trial_sweep(TrialArgs t) {
-    using BlockScan = cub::BlockScan<uint32_t, kTrialThreads>;
-    using BlockReduce = cub::BlockReduce<double, kTrialThreads>;
-    __shared__ union {
+template <int NT>
+struct TrialSmem {
+    using BlockScan = cub::BlockScan<uint32_t, NT>;
+    using BlockReduce = cub::BlockReduce<double, NT>;
+    union {
         typename BlockScan::TempStorage scan;
         typename BlockReduce::TempStorage reduce;
     } tmp;
-    __shared__ uint32_t sTouched, sBase;
-    __shared__ int sBox[4];
-    __shared__ double sE0, sE1;
-    __shared__ int sVerdict;
+    uint32_t touched, base;
+    int box[4];
+    double e0;
+    int verdict;
+};
+
+// One trial (jointopt.cpp:114-180) executed by the whole CTA.  Returns the
+// verdict (1 accepted) in every thread.
+template <int NT>
+__device__ int run_trial(const TrialState& t, const TrialBuffers& b, TrialSmem<NT>& sm,
+                         const uint32_t* comp, uint32_t n) {
+    using BlockScan = typename TrialSmem<NT>::BlockScan;
+    using BlockReduce = typename TrialSmem<NT>::BlockReduce;
     const int tid = threadIdx.x;
     const int h = t.S / 2;
     const uint32_t W = uint32_t(t.W), s = uint32_t(t.s);
-
-    for (int c = 0; c < t.ncomp; ++c) {
-        const uint32_t* comp = t.px + t.off[c];
-        const uint32_t n = t.off[c + 1] - t.off[c];
-        if (tid == 0) {
-            sTouched = 0;
-            sBox[0] = t.lw;
-            sBox[1] = t.lh;
-            sBox[2] = -1;
-            sBox[3] = -1;
+    if (tid == 0) {
+        sm.touched = 0;
+        sm.box[0] = t.lw;
+        sm.box[1] = t.lh;
+        sm.box[2] = -1;
+        sm.box[3] = -1;
+    }
+    __syncthreads();
+    // 1. groupByOwnerCell (jointopt.cpp:56-72) + worst pixel per cell: the
+    //    first strict argmax over ascending pixels == max of (E, -pixel).
+    for (uint32_t i = tid; i < n; i += NT) {
+        const uint32_t p = comp[i];
+        const uint32_t cx = (p % W) / s, cy = (p / W) / s;
+        const uint32_t cell = cy * uint32_t(t.lw) + cx;
+        const unsigned long long key =
+            (static_cast<unsigned long long>(__float_as_uint(t.errors[p])) << 32) |
+            (0xffffffffu - p);
+        atomicMax(t.cellKey + cell, key);
+        if (atomicExch(t.cellFlag + cell, 1u) == 0) {
+            b.touched[atomicAdd(&sm.touched, 1u)] = cell;
+            atomicMin(&sm.box[0], int(cx));
+            atomicMin(&sm.box[1], int(cy));
+            atomicMax(&sm.box[2], int(cx));
+            atomicMax(&sm.box[3], int(cy));
         }
-        __syncthreads();
-        // 1. groupByOwnerCell (jointopt.cpp:56-72) + worst pixel per cell: the
-        //    first strict argmax over ascending pixels == max of (E, -pixel).
-        for (uint32_t i = tid; i < n; i += kTrialThreads) {
-            const uint32_t p = comp[i];
-            const uint32_t cx = (p % W) / s, cy = (p / W) / s;
-            const uint32_t cell = cy * uint32_t(t.lw) + cx;
-            const unsigned long long key =
-                (static_cast<unsigned long long>(__float_as_uint(t.errors[p])) << 32) |
-                (0xffffffffu - p);
-            atomicMax(t.cellKey + cell, key);
-            if (atomicExch(t.cellFlag + cell, 1u) == 0) {
-                t.touched[atomicAdd(&sTouched, 1u)] = cell;
-                atomicMin(&sBox[0], int(cx));
-                atomicMin(&sBox[1], int(cy));
-                atomicMax(&sBox[2], int(cx));
-                atomicMax(&sBox[3], int(cy));
-            }
-        }
-        __syncthreads();
-        const uint32_t nt = sTouched;
-        // 2. replace each cell by its worst pixel (jointopt.cpp:130-142) and
-        //    mark the cells whose windows reach it (affectedPixels, 76-110).
-        for (uint32_t i = tid; i < nt; i += kTrialThreads) {
-            const uint32_t cell = t.touched[i];
-            const uint32_t best = 0xffffffffu - uint32_t(t.cellKey[cell] & 0xffffffffu);
-            float* lc = t.low + 3 * size_t(cell);
-            const float* src = t.high + 3 * size_t(best);
-            t.oldColor[3 * i] = lc[0];
-            t.oldColor[3 * i + 1] = lc[1];
-            t.oldColor[3 * i + 2] = lc[2];
-            lc[0] = src[0];
-            lc[1] = src[1];
-            lc[2] = src[2];
-            if (!t.literal) {
-                const int cx = int(cell % uint32_t(t.lw)), cy = int(cell / uint32_t(t.lw));
-                for (int y = max(0, cy - h); y <= min(t.lh - 1, cy + h); ++y)
-                    for (int x = max(0, cx - h); x <= min(t.lw - 1, cx + h); ++x)
-                        t.affMark[size_t(y) * t.lw + x] = 1;
-            }
-        }
-        __syncthreads();
-        // 3. affected pixels in the reference order: dilated bounding box in
-        //    raster cell order, then each footprint in raster order.
-        const uint32_t* aff = comp;
-        uint32_t na = n;
+    }
+    __syncthreads();
+    const uint32_t nt = sm.touched;
+    // 2. replace each cell by its worst pixel (jointopt.cpp:130-142) and mark
+    //    the cells whose windows reach it (affectedPixels, 76-110).
+    for (uint32_t i = tid; i < nt; i += NT) {
+        const uint32_t cell = b.touched[i];
+        const uint32_t best = 0xffffffffu - uint32_t(t.cellKey[cell] & 0xffffffffu);
+        float* lc = t.low + 3 * size_t(cell);
+        const float* src = t.high + 3 * size_t(best);
+        b.oldColor[3 * i] = lc[0];
+        b.oldColor[3 * i + 1] = lc[1];
+        b.oldColor[3 * i + 2] = lc[2];
+        lc[0] = src[0];
+        lc[1] = src[1];
+        lc[2] = src[2];
         if (!t.literal) {
-            const int bx0 = max(0, sBox[0] - h), by0 = max(0, sBox[1] - h);
-            const int bx1 = min(t.lw - 1, sBox[2] + h), by1 = min(t.lh - 1, sBox[3] + h);
-            const int bw = bx1 - bx0 + 1;
-            const uint32_t nbox = uint32_t(bw) * uint32_t(by1 - by0 + 1);
-            if (tid == 0) sBase = 0;
+            const int cx = int(cell % uint32_t(t.lw)), cy = int(cell / uint32_t(t.lw));
+            for (int y = max(0, cy - h); y <= min(t.lh - 1, cy + h); ++y)
+                for (int x = max(0, cx - h); x <= min(t.lw - 1, cx + h); ++x)
+                    t.affMark[size_t(y) * t.lw + x] = 1;
+        }
+    }
+    __syncthreads();
+    // 3. affected pixels in the reference order: dilated bounding box in raster
+    //    cell order, then each footprint in raster order.
+    const uint32_t* aff = comp;
+    uint32_t na = n;
+    if (!t.literal) {
+        const int bx0 = max(0, sm.box[0] - h), by0 = max(0, sm.box[1] - h);
+        const int bx1 = min(t.lw - 1, sm.box[2] + h), by1 = min(t.lh - 1, sm.box[3] + h);
+        const int bw = bx1 - bx0 + 1;
+        const uint32_t nbox = uint32_t(bw) * uint32_t(by1 - by0 + 1);
+        if (tid == 0) sm.base = 0;
+        __syncthreads();
+        for (uint32_t b0 = 0; b0 < nbox; b0 += NT) {
+            const uint32_t k = b0 + tid;
+            uint32_t fs = 0;
+            int x = 0, y = 0;
+            if (k < nbox) {
+                x = bx0 + int(k % uint32_t(bw));
+                y = by0 + int(k / uint32_t(bw));
+                uint8_t* mk = t.affMark + size_t(y) * t.lw + x;
+                if (*mk) {
+                    *mk = 0;
+                    fs = uint32_t(min(x * t.s + t.s, t.W) - x * t.s) *
+                         uint32_t(min(y * t.s + t.s, t.H) - y * t.s);
+                }
+            }
+            uint32_t pos, total;
+            BlockScan(sm.tmp.scan).ExclusiveSum(fs, pos, total);
+            if (fs) {
+                uint32_t o = sm.base + pos;
+                const int px0 = x * t.s, py0 = y * t.s;
+                const int px1 = min(px0 + t.s, t.W), py1 = min(py0 + t.s, t.H);
+                for (int py = py0; py < py1; ++py)
+                    for (int pxx = px0; pxx < px1; ++pxx)
+                        b.aff[o++] = uint32_t(py) * W + uint32_t(pxx);
+            }
             __syncthreads();
-            for (uint32_t b0 = 0; b0 < nbox; b0 += kTrialThreads) {
-                const uint32_t k = b0 + tid;
-                uint32_t fs = 0;
-                int x = 0, y = 0;
-                if (k < nbox) {
-                    x = bx0 + int(k % uint32_t(bw));
-                    y = by0 + int(k / uint32_t(bw));
-                    uint8_t* mk = t.affMark + size_t(y) * t.lw + x;
-                    if (*mk) {
-                        *mk = 0;
-                        fs = uint32_t(min(x * t.s + t.s, t.W) - x * t.s) *
-                             uint32_t(min(y * t.s + t.s, t.H) - y * t.s);
-                    }
-                }
-                uint32_t pos, total;
-                BlockScan(tmp.scan).ExclusiveSum(fs, pos, total);
-                if (fs) {
-                    uint32_t o = sBase + pos;
-                    const int px0 = x * t.s, py0 = y * t.s;
-                    const int px1 = min(px0 + t.s, t.W), py1 = min(py0 + t.s, t.H);
-                    for (int py = py0; py < py1; ++py)
-                        for (int pxx = px0; pxx < px1; ++pxx)
-                            t.aff[o++] = uint32_t(py) * W + uint32_t(pxx);
-                }
-                __syncthreads();
-                if (tid == 0) sBase += total;
-                __syncthreads();
-            }
-            aff = t.aff;
-            na = sBase;
+            if (tid == 0) sm.base += total;
+            __syncthreads();
         }
-        // 4. backup and e0 (jointopt.cpp:150-157).
-        double part = 0;
-        for (uint32_t i = tid; i < na; i += kTrialThreads) {
+        aff = b.aff;
+        na = sm.base;
+    }
+    // 4. backup and e0 (jointopt.cpp:150-157).
+    double part = 0;
+    for (uint32_t i = tid; i < na; i += NT) {
+        const uint32_t p = aff[i];
+        b.bkParams[i] = t.field[p];
+        b.bkE[i] = t.errors[p];
+        part += double(b.bkE[i]);
+    }
+    const double e0 = BlockReduce(sm.tmp.reduce).Sum(part);
+    if (tid == 0) sm.e0 = e0;
+    __syncthreads();
+    // 5. re-solve (optimize_pixels, 159) and re-score (160-165).
+    part = 0;
+    for (uint32_t i = tid; i < na; i += NT) {
+        const uint32_t p = aff[i];
+        const int x = int(p % W), y = int(p / W);
+        const float* ip = t.high + 3 * size_t(p);
+        const int cx = x / t.s, cy = y / t.s;
+        const int x0 = max(0, cx - h), y0 = max(0, cy - h);
+        const int nwx = min(t.lw - 1, cx + h) - x0 + 1, nwy = min(t.lh - 1, cy + h) - y0 + 1;
+        const Pick pk = pick64(t.mode, ip, GlobalLowWindow{t.low, t.lw, x0, y0, nwx}, nwx * nwy,
+                               t.eps);
+        const int ar = pk.ai / nwx, br = pk.bi / nwx;
+        glu_pixel_params np;
+        np.a = uint32_t(y0 + ar) * uint32_t(t.lw) + uint32_t(x0 + pk.ai - ar * nwx);
+        np.b = uint32_t(y0 + br) * uint32_t(t.lw) + uint32_t(x0 + pk.bi - br * nwx);
+        np.w = float(pk.w);
+        t.field[p] = np;
+        float r[3];
+        for (int k = 0; k < 3; ++k)
+            r[k] = lerp_clamp(np.w, t.low[3 * size_t(np.a) + k], t.low[3 * size_t(np.b) + k],
+                              true);
+        const float e = pixel_error(ip, r);
+        t.errors[p] = e;
+        part += double(e);
+    }
+    const double e1 = BlockReduce(sm.tmp.reduce).Sum(part);
+    if (tid == 0) {
+        const double s0 = sm.e0;
+        // |parallel - sequential| <= 2 * gamma_na * sum for non-negative terms.
+        const double bound = 4.0 * (double(na) + 64.0) * 0x1.0p-53 * (s0 + e1);
+        int verdict;
+        if (e1 + bound < s0)
+            verdict = 1;
+        else if (e1 > s0 + bound)
+            verdict = 0;
+        else {  // exact reference order (jointopt.cpp:150-165)
+            double q0 = 0, q1 = 0;
+            for (uint32_t i = 0; i < na; ++i) {
+                q0 += double(b.bkE[i]);
+                q1 += double(t.errors[aff[i]]);
+            }
+            verdict = q1 <= q0;
+            atomicAdd(t.result + 2, 1);
+        }
+        sm.verdict = verdict;
+    }
+    __syncthreads();
+    const int verdict = sm.verdict;
+    // 6. rollback (jointopt.cpp:169-179) and reset per-cell state.
+    if (!verdict) {
+        for (uint32_t i = tid; i < na; i += NT) {
             const uint32_t p = aff[i];
-            t.bkParams[i] = t.field[p];
-            t.bkE[i] = t.errors[p];
-            part += double(t.bkE[i]);
+            t.field[p] = b.bkParams[i];
+            t.errors[p] = b.bkE[i];
         }
-        double e0 = BlockReduce(tmp.reduce).Sum(part);
-        if (tid == 0) sE0 = e0;
+    }
+    for (uint32_t i = tid; i < nt; i += NT) {
+        const uint32_t cell = b.touched[i];
+        if (!verdict) {
+            float* lc = t.low + 3 * size_t(cell);
+            lc[0] = b.oldColor[3 * i];
+            lc[1] = b.oldColor[3 * i + 1];
+            lc[2] = b.oldColor[3 * i + 2];
+        }
+        t.cellKey[cell] = 0;
+        t.cellFlag[cell] = 0;
+    }
+    __syncthreads();
+    return verdict;
+}
+
+// Sequential sweep: one CTA runs the components in order (used for single
+// trials and as the reference schedule in tests, GLU_OPT_TRIALS = 1).
+__global__ void __launch_bounds__(kSeqThreads) k_trial_sweep(TrialState t, TrialBuffers b,
+                                                             const uint32_t* off,
+                                                             const uint32_t* px, int ncomp) {
+    __shared__ TrialSmem<kSeqThreads> sm;
+    for (int c = 0; c < ncomp; ++c) {
+        const int v = run_trial<kSeqThreads>(t, b, sm, px + off[c], off[c + 1] - off[c]);
+        if (threadIdx.x == 0) {
+            t.result[v ? 0 : 1] += 1;
+            t.result[3] = v;
+        }
+    }
+}
+
+// Cell bounding box of every component; components whose worst-case
+// affected set exceeds a CTA's private buffers get the whole grid.
+__global__ void k_trial_boxes(const uint32_t* __restrict__ off, const uint32_t* __restrict__ px,
+                              int ncomp, int W, int s, int lw, int lh, int h, int literal,
+                              int4* __restrict__ boxes) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= ncomp) return;
+    const uint32_t b0 = off[warp], b1 = off[warp + 1];
+    int x0 = lw, y0 = lh, x1 = -1, y1 = -1;
+    for (uint32_t i = b0 + lane; i < b1; i += 32) {
+        const uint32_t p = px[i];
+        const int cx = int((p % uint32_t(W)) / uint32_t(s)), cy = int((p / uint32_t(W)) / uint32_t(s));
+        x0 = min(x0, cx);
+        y0 = min(y0, cy);
+        x1 = max(x1, cx);
+        y1 = max(y1, cy);
+    }
+    for (int o = 16; o; o >>= 1) {
+        x0 = min(x0, __shfl_xor_sync(0xffffffffu, x0, o));
+        y0 = min(y0, __shfl_xor_sync(0xffffffffu, y0, o));
+        x1 = max(x1, __shfl_xor_sync(0xffffffffu, x1, o));
+        y1 = max(y1, __shfl_xor_sync(0xffffffffu, y1, o));
+    }
+    if (lane == 0) {
+        const uint64_t cells = uint64_t(x1 - x0 + 1) * uint64_t(y1 - y0 + 1);
+        const uint64_t dil = uint64_t(min(lw - 1, x1 + h) - max(0, x0 - h) + 1) *
+                             uint64_t(min(lh - 1, y1 + h) - max(0, y0 - h) + 1);
+        const uint64_t affPx = literal ? uint64_t(b1 - b0) : dil * uint64_t(s) * uint64_t(s);
+        const bool big = cells > kCtaCells || affPx > kCtaPixels;
+        boxes[warp] = big ? make_int4(-(1 << 28), -(1 << 28), 1 << 28, 1 << 28)
+                          : make_int4(x0, y0, x1, y1);
+    }
+}
+
+__device__ __forceinline__ bool boxes_conflict(int4 a, int4 b, int reach) {
+    const int dx = max(0, max(a.x - b.z, b.x - a.z));
+    const int dy = max(0, max(a.y - b.w, b.y - a.w));
+    return max(dx, dy) <= reach;
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Persistent conflict-aware trial scheduler (see the file comment).
+__global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
+    TrialState t, TrialBuffers big, char* ctaBufs, const uint32_t* off, const uint32_t* px,
+    int ncomp, const int4* boxes, int* done, int* next, int reach) {
+    __shared__ TrialSmem<kSchedThreads> sm;
+    __shared__ int sIdx;
+    // this CTA's private buffers
+    char* mine = ctaBufs + size_t(blockIdx.x) *
+                               (size_t(kCtaCells) * 16 + size_t(kCtaPixels) * 20);
+    TrialBuffers local;
+    local.touched = reinterpret_cast<uint32_t*>(mine);
+    local.oldColor = reinterpret_cast<float*>(mine + size_t(kCtaCells) * 4);
+    local.aff = reinterpret_cast<uint32_t*>(mine + size_t(kCtaCells) * 16);
+    local.bkParams = reinterpret_cast<glu_pixel_params*>(mine + size_t(kCtaCells) * 16 +
+                                                         size_t(kCtaPixels) * 4);
+    local.bkE = reinterpret_cast<float*>(mine + size_t(kCtaCells) * 16 + size_t(kCtaPixels) * 16);
+    for (;;) {
+        if (threadIdx.x == 0) sIdx = atomicAdd(next, 1);
         __syncthreads();
-        // 5. re-solve (optimize_pixels, 159) and re-score (160-165).
-        part = 0;
-        for (uint32_t i = tid; i < na; i += kTrialThreads) {
-            const uint32_t p = aff[i];
-            const int x = int(p % W), y = int(p / W);
-            const float* ip = t.high + 3 * size_t(p);
-            const int cx = x / t.s, cy = y / t.s;
-            const int x0 = max(0, cx - h), y0 = max(0, cy - h);
-            const int nwx = min(t.lw - 1, cx + h) - x0 + 1, nwy = min(t.lh - 1, cy + h) - y0 + 1;
-            const Pick pk = pick64(t.mode, ip, GlobalLowWindow{t.low, t.lw, x0, y0, nwx},
-                                   nwx * nwy, t.eps);
-            const int ar = pk.ai / nwx, br = pk.bi / nwx;
-            glu_pixel_params np;
-            np.a = uint32_t(y0 + ar) * uint32_t(t.lw) + uint32_t(x0 + pk.ai - ar * nwx);
-            np.b = uint32_t(y0 + br) * uint32_t(t.lw) + uint32_t(x0 + pk.bi - br * nwx);
-            np.w = float(pk.w);
-            t.field[p] = np;
-            float r[3];
-            for (int k = 0; k < 3; ++k)
-                r[k] = lerp_clamp(np.w, t.low[3 * size_t(np.a) + k], t.low[3 * size_t(np.b) + k],
-                                  true);
-            const float e = pixel_error(ip, r);
-            t.errors[p] = e;
-            part += double(e);
-        }
-        double e1 = BlockReduce(tmp.reduce).Sum(part);
-        if (tid == 0) {
-            sE1 = e1;
-            e0 = sE0;
-            // |parallel - sequential| <= 2 * gamma_na * sum for non-negative terms.
-            const double bound = 4.0 * (double(na) + 64.0) * 0x1.0p-53 * (e0 + e1);
-            int verdict;
-            if (e1 + bound < e0)
-                verdict = 1;
-            else if (e1 > e0 + bound)
-                verdict = 0;
-            else {  // exact reference order (jointopt.cpp:150-165)
-                double s0 = 0, s1 = 0;
-                for (uint32_t i = 0; i < na; ++i) {
-                    s0 += double(t.bkE[i]);
-                    s1 += double(t.errors[aff[i]]);
-                }
-                verdict = s1 <= s0;
-                ++t.result[2];
-            }
-            sVerdict = verdict;
-            t.result[verdict ? 0 : 1] += 1;
-            t.result[3] = verdict;
-        }
+        const int i = sIdx;
+        if (i >= ncomp) break;
+        const int4 bi = boxes[i];
+        // wait for every earlier trial this one conflicts with
+        for (int j = threadIdx.x; j < i; j += kSchedThreads)
+            if (boxes_conflict(boxes[j], bi, reach))
+                while (ld_acquire(done + j) == 0) __nanosleep(64);
         __syncthreads();
-        // 6. rollback (jointopt.cpp:169-179) and reset per-cell state.
-        if (!sVerdict) {
-            for (uint32_t i = tid; i < na; i += kTrialThreads) {
-                const uint32_t p = aff[i];
-                t.field[p] = t.bkParams[i];
-                t.errors[p] = t.bkE[i];
-            }
+        __threadfence();
+        const bool isBig = bi.x < 0;
+        const int v = run_trial<kSchedThreads>(t, isBig ? big : local, sm, px + off[i],
+                                               off[i + 1] - off[i]);
+        if (threadIdx.x == 0) {
+            atomicAdd(t.result + (v ? 0 : 1), 1);
+            __threadfence();
+            st_release(done + i, 1);
         }
-        for (uint32_t i = tid; i < nt; i += kTrialThreads) {
-            const uint32_t cell = t.touched[i];
-            if (!sVerdict) {
-                float* lc = t.low + 3 * size_t(cell);
-                lc[0] = t.oldColor[3 * i];
-                lc[1] = t.oldColor[3 * i + 1];
-                lc[2] = t.oldColor[3 * i + 2];
-            }
-            t.cellKey[cell] = 0;
-            t.cellFlag[cell] = 0;
-        }
-        __syncthreads();
     }
 }
 
@@ -345,11 +469,7 @@ struct JointScratch {
     unsigned long long* cellKey;
     uint32_t* cellFlag;
     uint8_t* affMark;
-    uint32_t* touched;
-    float* oldColor;
-    uint32_t* aff;
-    glu_pixel_params* bkParams;
-    float* bkE;
+    TrialBuffers big;
     int* result;
 };
 
@@ -363,18 +483,53 @@ int joint_scratch(glu_ctx* ctx, const glu_grid& g, JointScratch* js, bool reset)
     if (!cells || !pix) return GLU_ENOMEM;
     js->cellKey = reinterpret_cast<unsigned long long*>(cells);
     js->cellFlag = reinterpret_cast<uint32_t*>(cells + lowN * 8);
-    js->touched = reinterpret_cast<uint32_t*>(cells + lowN * 12);
-    js->oldColor = reinterpret_cast<float*>(cells + lowN * 16);
+    js->big.touched = reinterpret_cast<uint32_t*>(cells + lowN * 12);
+    js->big.oldColor = reinterpret_cast<float*>(cells + lowN * 16);
     js->affMark = reinterpret_cast<uint8_t*>(cells + lowN * 28);
     js->result = reinterpret_cast<int*>(cells + ((cellBytes + 15) & ~size_t(15)));
-    js->aff = reinterpret_cast<uint32_t*>(pix);
-    js->bkParams = reinterpret_cast<glu_pixel_params*>(pix + npx * 4);
-    js->bkE = reinterpret_cast<float*>(pix + npx * 16);
+    js->big.aff = reinterpret_cast<uint32_t*>(pix);
+    js->big.bkParams = reinterpret_cast<glu_pixel_params*>(pix + npx * 4);
+    js->big.bkE = reinterpret_cast<float*>(pix + npx * 16);
     if (reset) {
         cudaError_t e = cudaMemsetAsync(cells, 0, cellBytes + 16 * sizeof(int), ctx->stream);
         if (e != cudaSuccess) return fail_cuda(e, "joint scratch");
     }
     return GLU_OK;
+}
+
+TrialState trial_state(const float* high, float* low, glu_pixel_params* field, float* errors,
+                       const glu_grid& g, const glu_config& cfg, int mode,
+                       const JointScratch& js) {
+    TrialState t;
+    t.high = high;
+    t.low = low;
+    t.field = field;
+    t.errors = errors;
+    t.W = g.highW;
+    t.H = g.highH;
+    t.s = g.scale;
+    t.lw = g.lowW;
+    t.lh = g.lowH;
+    t.S = cfg.windowSide;
+    t.eps = double(cfg.epsilon);
+    t.mode = mode;
+    t.literal = cfg.literalComponentUpdate;
+    t.cellKey = js.cellKey;
+    t.cellFlag = js.cellFlag;
+    t.affMark = js.affMark;
+    t.result = js.result;
+    return t;
+}
+
+int sched_grid(glu_ctx* ctx) {
+    static thread_local int cached = -1, cachedDev = -1;
+    if (cached > 0 && cachedDev == ctx->device) return cached;
+    int sms = 0, per = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_trial_sched, kSchedThreads, 0);
+    cached = sms * std::max(1, std::min(per, 2));
+    cachedDev = ctx->device;
+    return cached;
 }
 
 }  // namespace
@@ -386,7 +541,7 @@ int ccl_find_large_error(glu_ctx* ctx, const float* errors, int W, int H, float 
     cudaStream_t st = ctx->stream;
     uint8_t* dmask = mask ? mask : static_cast<uint8_t*>(scratch(ctx, S_CCL_MISC, npx));
     uint32_t* parent = label ? label : static_cast<uint32_t*>(scratch(ctx, S_CCL_LABEL, npx * 4));
-    // flags/rank/slot + keys/vals (+ sorted copies) + offsets
+    // flags/rank/slot + keys/vals (+ sorted copies)
     uint32_t* work = static_cast<uint32_t*>(scratch(ctx, S_CCL_LIST, npx * 4 * 6 + 64));
     if (!dmask || !parent || !work) return GLU_ENOMEM;
     uint32_t* flags = work;
@@ -395,7 +550,6 @@ int ccl_find_large_error(glu_ctx* ctx, const float* errors, int W, int H, float 
     uint32_t* vals = work + 3 * npx;
     uint32_t* keys2 = work + 4 * npx;
     uint32_t* vals2 = work + 5 * npx;
-    uint32_t* tot = work + 6 * npx;  // [0] ncomp, [1] nmask
     cudaError_t e;
     k_ccl_init<<<blocks_for(npx, 256), 256, 0, st>>>(errors, npx, thr, dmask, parent);
     k_ccl_union<<<blocks_for(npx, 256), 256, 0, st>>>(dmask, parent, W, H);
@@ -414,7 +568,7 @@ int ccl_find_large_error(glu_ctx* ctx, const float* errors, int W, int H, float 
     e = cub::DeviceScan::ExclusiveSum(temp, tb, flags, rank, int(npx), st);
     if (e != cudaSuccess) return fail_cuda(e, "ccl scan");
     // totals: ncomp = rank[last] + flags[last]
-    uint32_t hostTot[2];
+    uint32_t ncomp = 0, nmask = 0;
     {
         uint32_t lastRank, lastFlag;
         e = cudaMemcpyAsync(&lastRank, rank + npx - 1, 4, cudaMemcpyDeviceToHost, st);
@@ -422,7 +576,7 @@ int ccl_find_large_error(glu_ctx* ctx, const float* errors, int W, int H, float 
             e = cudaMemcpyAsync(&lastFlag, flags + npx - 1, 4, cudaMemcpyDeviceToHost, st);
         if (e == cudaSuccess) e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) return fail_cuda(e, "ccl count");
-        hostTot[0] = lastRank + lastFlag;
+        ncomp = lastRank + lastFlag;
     }
     // mask slots
     k_mask_flags<<<blocks_for(npx, 256), 256, 0, st>>>(parent, npx, flags);
@@ -436,10 +590,8 @@ int ccl_find_large_error(glu_ctx* ctx, const float* errors, int W, int H, float 
             e = cudaMemcpyAsync(&lastFlag, flags + npx - 1, 4, cudaMemcpyDeviceToHost, st);
         if (e == cudaSuccess) e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) return fail_cuda(e, "ccl count");
-        hostTot[1] = lastSlot + lastFlag;
+        nmask = lastSlot + lastFlag;
     }
-    (void)tot;
-    const uint32_t ncomp = hostTot[0], nmask = hostTot[1];
     *count = ncomp;
     if (ncomp == 0) {
         if (offOut) *offOut = off;
@@ -469,36 +621,37 @@ int joint_sweep(glu_ctx* ctx, const float* high, float* low, glu_pixel_params* f
     JointScratch js;
     int rc = joint_scratch(ctx, g, &js, true);
     if (rc) return rc;
-    TrialArgs t;
-    t.high = high;
-    t.low = low;
-    t.field = field;
-    t.errors = errors;
-    t.W = g.highW;
-    t.H = g.highH;
-    t.s = g.scale;
-    t.lw = g.lowW;
-    t.lh = g.lowH;
-    t.S = cfg.windowSide;
-    t.eps = double(cfg.epsilon);
-    t.mode = mode;
-    t.literal = cfg.literalComponentUpdate;
-    t.off = off;
-    t.px = px;
-    t.ncomp = int(ncomp);
-    t.cellKey = js.cellKey;
-    t.cellFlag = js.cellFlag;
-    t.affMark = js.affMark;
-    t.touched = js.touched;
-    t.oldColor = js.oldColor;
-    t.aff = js.aff;
-    t.bkParams = js.bkParams;
-    t.bkE = js.bkE;
-    t.result = js.result;
-    k_trial_sweep<<<1, kTrialThreads, 0, ctx->stream>>>(t);
-    ++ctx->launches;
+    const TrialState t = trial_state(high, low, field, errors, g, cfg, mode, js);
+    cudaError_t e;
+    if (ctx->trials == 1 || ncomp == 1) {
+        k_trial_sweep<<<1, kSeqThreads, 0, ctx->stream>>>(t, js.big, off, px, int(ncomp));
+        ++ctx->launches;
+        e = cudaGetLastError();
+    } else {
+        const int grid = sched_grid(ctx);
+        const size_t per = size_t(kCtaCells) * 16 + size_t(kCtaPixels) * 20;
+        char* ctaBufs = static_cast<char*>(scratch(ctx, S_SCHED, per * grid));
+        // boxes (int4 per component) | done flags | next counter
+        char* meta = static_cast<char*>(scratch(ctx, S_SCHED_META, ncomp * 20 + 64));
+        if (!ctaBufs || !meta) return GLU_ENOMEM;
+        int4* boxes = reinterpret_cast<int4*>(meta);
+        int* done = reinterpret_cast<int*>(meta + ncomp * 16);
+        int* next = done + ncomp;
+        e = cudaMemsetAsync(done, 0, (ncomp + 1) * sizeof(int), ctx->stream);
+        if (e != cudaSuccess) return fail_cuda(e, "trial sweep");
+        k_trial_boxes<<<blocks_for(ncomp * 32, 256), 256, 0, ctx->stream>>>(
+            off, px, int(ncomp), g.highW, g.scale, g.lowW, g.lowH, cfg.windowSide / 2,
+            cfg.literalComponentUpdate, boxes);
+        ++ctx->launches;
+        TrialState ts = t;
+        TrialBuffers big = js.big;
+        int nc = int(ncomp), reach = 2 * (cfg.windowSide / 2);
+        void* args[] = {&ts, &big, &ctaBufs, &off, &px, &nc, &boxes, &done, &next, &reach};
+        e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_trial_sched), grid,
+                                        kSchedThreads, args, 0, ctx->stream);
+        ++ctx->launches;
+    }
     int res[4];
-    cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(res, js.result, sizeof(res), cudaMemcpyDeviceToHost, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);

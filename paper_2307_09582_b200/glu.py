@@ -172,6 +172,10 @@ class Context:
         2 fp32 filter with every pixel forced through the fp64 verify."""
         N.check(N.lib().glu_ctx_set_option(self.handle, 1, int(value)))
 
+    def set_trials(self, value: int) -> None:
+        """GLU_OPT_TRIALS: 0 conflict-aware parallel schedule, 1 one CTA in order."""
+        N.check(N.lib().glu_ctx_set_option(self.handle, 2, int(value)))
+
     @property
     def launches(self) -> int:
         return int(N.lib().glu_ctx_launch_count(self.handle))

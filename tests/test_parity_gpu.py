@@ -286,3 +286,25 @@ def test_reference_unit_tests_pass_against_dropin_api(glu):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "47 passed | 0 failed" in r.stdout, r.stdout
+
+
+@pytest.mark.parametrize("W,H,s,S,literal", [(512, 384, 8, 3, False), (640, 360, 4, 3, False),
+                                             (480, 320, 6, 5, False), (400, 300, 8, 3, True)])
+def test_parallel_trial_schedule_matches_sequential(glu, W, H, s, S, literal):
+    """The conflict-aware parallel trial schedule is bit-identical to the
+    reference's sequential component loop (jointopt.cpp:195-202)."""
+    from paper_2307_09582_b200 import workloads
+    high = dev(workloads.scene(W, H, 40 + s))
+    cfg = glu.GluConfig(windowSide=S, literalComponentUpdate=literal)
+    ctx = glu.glu.context()
+    out = []
+    for trials in (1, 0):
+        ctx.set_trials(trials)
+        out.append(glu.joint_optimize(high, s, cfg))
+    ctx.set_trials(0)
+    a, b = out
+    assert a.trialsAccepted + a.trialsRejected > 10
+    assert (a.iterations, a.trialsAccepted, a.trialsRejected) == \
+        (b.iterations, b.trialsAccepted, b.trialsRejected)
+    assert torch.equal(a.low, b.low) and torch.equal(a.field.params, b.field.params)
+    assert torch.equal(a.errors, b.errors)
