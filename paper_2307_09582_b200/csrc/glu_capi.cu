@@ -307,7 +307,7 @@ int glu_cu_apply_field(glu_ctx* ctx, const glu_pixel_params* field, const glu_gr
     if (!ctx) return einval("ctx must not be null");
     GLU_TRY(check_grid(g));
     if (channels != 1 && channels != 3) return einval("apply_field: channels must be 1 or 3");
-    GLU_CUDA(launch_apply(ctx, field, npx_of(g), lowTarget, channels, clampOutput, out),
+    GLU_CUDA(launch_apply(ctx, field, npx_of(g), lowTarget, lown_of(g), channels, clampOutput, out),
              "apply_field");
     return GLU_OK;
 }

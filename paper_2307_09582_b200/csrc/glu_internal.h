@@ -69,7 +69,7 @@ cudaError_t launch_solve32(glu_ctx* ctx, const SolveArgs& a, int forceFallback);
 cudaError_t launch_solve_list(glu_ctx* ctx, const SolveArgs& a, const uint32_t* pixels,
                               size_t count);
 cudaError_t launch_apply(glu_ctx* ctx, const glu_pixel_params* field, size_t npx,
-                         const float* lowT, int channels, int clamp, float* out);
+                         const float* lowT, size_t lowN, int channels, int clamp, float* out);
 cudaError_t launch_error_map(glu_ctx* ctx, const float* high, const float* recon, size_t npx,
                              float* e);
 cudaError_t launch_self_error(glu_ctx* ctx, const float* high, const glu_pixel_params* field,

@@ -138,18 +138,50 @@ __global__ void k_solve_list(SolveArgs a, const uint32_t* __restrict__ pixels, s
 
 // ---- apply_field (upsample.cpp:235-252) -------------------------------------
 
+// HBM-bound gather-lerp: each thread handles 4 consecutive pixels, so its 48
+// bytes of params are three 16-byte streaming loads and its 48 (RGB) or 16
+// (1-channel) output bytes are 16-byte streaming stores; the LR target
+// (<= 1.6 MB) stays in L1/L2 for the gathers.  Indices outside the LR image
+// (corrupt params) produce NaN instead of faulting.
 template <int C>
-__global__ void k_apply(const glu_pixel_params* __restrict__ field, size_t npx,
-                        const float* __restrict__ lowT, int clamp, float* __restrict__ out) {
-    const size_t p = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (p >= npx) return;
-    const unsigned* f = reinterpret_cast<const unsigned*>(field + p);
-    const unsigned a = __ldg(f), b = __ldg(f + 1);
-    const float w = __uint_as_float(__ldg(f + 2));
+__device__ __forceinline__ void apply_px(unsigned a, unsigned b, float w,
+                                         const float* __restrict__ lowT, unsigned lowN,
+                                         bool clamp, float* o) {
+    if (a < lowN && b < lowN) {
 #pragma unroll
-    for (int c = 0; c < C; ++c)
-        out[C * p + c] = lerp_clamp(w, __ldg(lowT + size_t(C) * a + c),
-                                    __ldg(lowT + size_t(C) * b + c), clamp != 0);
+        for (int c = 0; c < C; ++c)
+            o[c] = lerp_clamp(w, __ldg(lowT + size_t(C) * a + c), __ldg(lowT + size_t(C) * b + c),
+                              clamp);
+    } else {
+#pragma unroll
+        for (int c = 0; c < C; ++c) o[c] = __int_as_float(0x7fc00000);
+    }
+}
+
+template <int C>
+__global__ void __launch_bounds__(256) k_apply(const glu_pixel_params* __restrict__ field,
+                                               size_t npx, const float* __restrict__ lowT,
+                                               unsigned lowN, int clamp, float* __restrict__ out) {
+    const size_t t = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t p0 = 4 * t;
+    if (p0 >= npx) return;
+    if (p0 + 4 <= npx) {
+        const uint4* f = reinterpret_cast<const uint4*>(field + p0);
+        const uint4 r0 = __ldcs(f), r1 = __ldcs(f + 1), r2 = __ldcs(f + 2);
+        float o[4 * C];
+        apply_px<C>(r0.x, r0.y, __uint_as_float(r0.z), lowT, lowN, clamp != 0, o);
+        apply_px<C>(r0.w, r1.x, __uint_as_float(r1.y), lowT, lowN, clamp != 0, o + C);
+        apply_px<C>(r1.z, r1.w, __uint_as_float(r2.x), lowT, lowN, clamp != 0, o + 2 * C);
+        apply_px<C>(r2.y, r2.z, __uint_as_float(r2.w), lowT, lowN, clamp != 0, o + 3 * C);
+        float4* d = reinterpret_cast<float4*>(out + C * p0);
+#pragma unroll
+        for (int k = 0; k < C; ++k) __stcs(d + k, make_float4(o[4 * k], o[4 * k + 1], o[4 * k + 2], o[4 * k + 3]));
+    } else {
+        for (size_t p = p0; p < npx; ++p) {
+            const unsigned* f = reinterpret_cast<const unsigned*>(field + p);
+            apply_px<C>(f[0], f[1], __uint_as_float(f[2]), lowT, lowN, clamp != 0, out + C * p);
+        }
+    }
 }
 
 // ---- error maps (upsample.cpp:254-267) --------------------------------------
@@ -298,11 +330,12 @@ cudaError_t launch_solve_list(glu_ctx* ctx, const SolveArgs& a, const uint32_t* 
 }
 
 cudaError_t launch_apply(glu_ctx* ctx, const glu_pixel_params* field, size_t npx,
-                         const float* lowT, int channels, int clamp, float* out) {
+                         const float* lowT, size_t lowN, int channels, int clamp, float* out) {
+    const unsigned blocks = blocks_for((npx + 3) / 4, 256);
     if (channels == 1)
-        k_apply<1><<<blocks_for(npx, 256), 256, 0, ctx->stream>>>(field, npx, lowT, clamp, out);
+        k_apply<1><<<blocks, 256, 0, ctx->stream>>>(field, npx, lowT, unsigned(lowN), clamp, out);
     else
-        k_apply<3><<<blocks_for(npx, 256), 256, 0, ctx->stream>>>(field, npx, lowT, clamp, out);
+        k_apply<3><<<blocks, 256, 0, ctx->stream>>>(field, npx, lowT, unsigned(lowN), clamp, out);
     ++ctx->launches;
     return cudaGetLastError();
 }
