@@ -314,7 +314,8 @@ def run_ours(args, ws, rank, local):
     roofline = {
         "bound": "fp32", "achieved": achieved, "peak": fp32_tflops, "unit": "TFLOP/s",
         "frac": achieved / fp32_tflops, "traffic": traffic,
-        "kernel": "k_solve32<3,Fast> (fused optimize_field + 1-ch apply_field)",
+        "kernel": {"fast": "k_solve32<3,Fast>", "gnu": "k_solve32<3,Gnu>",
+                   "exact": "k_solve32x"}[args.mode] + " (fused optimize_field + 1-ch apply_field)",
         "fp64_verify_fraction": fallback_px / (args.steps * px_step),
         "kernel_ms": k_ms, "kernel_share_of_step": sum(kernel_ms) / elapsed_ms,
         "algorithmic_flops_per_launch": flops, "algorithmic_bytes_per_launch": nbytes,

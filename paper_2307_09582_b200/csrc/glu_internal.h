@@ -63,9 +63,13 @@ struct SolveArgs {
 cudaError_t launch_grid_downsample(glu_ctx* ctx, const float* high, int W, int H, int s,
                                    int lw, int lh, float* low);
 cudaError_t launch_solve(glu_ctx* ctx, const SolveArgs& a);
-// glu_solve32.cu: fp32 filter + fp64 verify (Fast / GNU, S in {3, 5}).
-bool solve32_supported(int mode, int S);
+// glu_solve32.cu: fp32 filter + fp64 verify (Fast / GNU, S in {3, 5}; Exact
+// S = 3, s >= 3 via glu_solve32x.cu).
+bool solve32_supported(int mode, int S, int s);
 cudaError_t launch_solve32(glu_ctx* ctx, const SolveArgs& a, int forceFallback);
+bool solve32x_supported(int mode, int S, int s);
+cudaError_t launch_solve32x(glu_ctx* ctx, const SolveArgs& a, const float4* packed,
+                            int forceFallback);
 cudaError_t launch_solve_list(glu_ctx* ctx, const SolveArgs& a, const uint32_t* pixels,
                               size_t count);
 cudaError_t launch_apply(glu_ctx* ctx, const glu_pixel_params* field, size_t npx,

@@ -304,7 +304,7 @@ cudaError_t launch_grid_downsample(glu_ctx* ctx, const float* high, int W, int H
 }
 
 cudaError_t launch_solve(glu_ctx* ctx, const SolveArgs& a) {
-    if (ctx->solver != 1 && solve32_supported(a.mode, a.S))
+    if (ctx->solver != 1 && solve32_supported(a.mode, a.S, a.s))
         return launch_solve32(ctx, a, ctx->solver == 2);
     const int h = a.S / 2;
     const int ncx = (kTX - 1) / a.s + 2 + 2 * h, ncy = (kTY - 1) / a.s + 2 + 2 * h;

@@ -270,8 +270,9 @@ cudaError_t launch_t(glu_ctx* ctx, const SolveArgs& a, const float4* packed, int
 
 }  // namespace
 
-bool solve32_supported(int mode, int S) {
-    return (mode == GLU_MODE_FAST || mode == GLU_MODE_GNU) && (S == 3 || S == 5);
+bool solve32_supported(int mode, int S, int s) {
+    return ((mode == GLU_MODE_FAST || mode == GLU_MODE_GNU) && (S == 3 || S == 5)) ||
+           solve32x_supported(mode, S, s);
 }
 
 cudaError_t launch_solve32(glu_ctx* ctx, const SolveArgs& a0, int forceFallback) {
@@ -288,6 +289,7 @@ cudaError_t launch_solve32(glu_ctx* ctx, const SolveArgs& a0, int forceFallback)
     k_pack_low<<<unsigned((cells + 255) / 256), 256, 0, ctx->stream>>>(a.low, a.lw, a.lh, h,
                                                                         packed);
     ++ctx->launches;
+    if (a.mode == GLU_MODE_EXACT) return launch_solve32x(ctx, a, packed, forceFallback);
     if (a.mode == GLU_MODE_GNU)
         return a.S == 3 ? launch_t<3, GLU_MODE_GNU>(ctx, a, packed, forceFallback)
                         : launch_t<5, GLU_MODE_GNU>(ctx, a, packed, forceFallback);

@@ -1,0 +1,232 @@
+// glu_solve32x.cu -- fp32 filter + fp64 verify solve for Exact mode (S = 3).
+//
+// The reference's pixelExact (upsample.cpp:73-91) scans the 45 unordered pairs
+// (i <= j, lexicographic) of the window with the closed-form weight
+// w = (Ip - Ij).(Ii - Ij) / (|Ii - Ij|^2 + eps) (158-167) and keeps the first
+// argmin of |w Ii + (1 - w) Ij - Ip|^2 + eps w^2, all in double.
+//
+// At its own optimum the objective has the closed form
+//     obj_ij = |e_j|^2 - num^2 / den,   e = I - I_p, num = -e_j.D, D = I_i - I_j,
+//                                       den = |D|^2 + eps,
+// (and obj_ii = |e_i|^2 exactly, since w = 0).  D and 1/den depend only on the
+// owner cell's window, so each CTA tabulates them once per owner cell in
+// shared memory; a pixel then spends ~10 FP32 instructions per pair.  The
+// fp32 error of obj_ij is below 17 u |e_j|^2 (u = 2^-24); the
+// kernel uses 64 u q_max as a uniform bound, re-checks close calls with the
+// per-pair bound, and sends the remaining ties between differently coloured
+// pairs to the reference's exact double-precision path.  The stored weight is
+// recomputed in double in the reference's order.
+#include <cuda_runtime.h>
+
+#include "glu_internal.h"
+#include "glu_math.cuh"
+
+namespace glu_cu {
+
+namespace {
+
+constexpr int kTX = 32, kTY = 8, kThreads = kTX * kTY;
+constexpr int kPairs = 36;       // i < j over 9 candidates
+constexpr int kCellStride = 37;  // float4 per owner cell (592 B: bank-spread)
+constexpr int kMaxCells = 48;    // (31/3 + 2) x (7/3 + 2) owner cells for s >= 3
+constexpr float kU = 5.9604645e-08f;
+constexpr float kCE = 64.0f;  // objective error bound, in u * |e_j|^2
+constexpr float kCA = 32.0f;
+constexpr float kInf = __builtin_huge_valf();
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+__device__ __forceinline__ int div_s(int v, const SolveArgs& a) {
+    return a.sdiv ? int(__umulhi(unsigned(v), a.sdiv)) : v / a.s;
+}
+
+__device__ __forceinline__ bool same_rgb(float4 a, float4 b) {
+    return a.x == b.x && a.y == b.y && a.z == b.z;
+}
+
+struct PackedWindow {
+    const float4* win;
+    int pw, nwx;
+    __device__ __forceinline__ const float* operator[](int i) const {
+        const int r = i / nwx, q = i - r * nwx;
+        return reinterpret_cast<const float*>(win + r * pw + q);
+    }
+};
+
+// pair index (i < j) -> i, j
+__device__ __forceinline__ void pair_ij(int k, int& i, int& j) {
+    i = 0;
+    int rem = k;
+    while (rem >= 8 - i) {
+        rem -= 8 - i;
+        ++i;
+    }
+    j = i + 1 + rem;
+}
+
+__global__ void __launch_bounds__(kThreads, 2) k_solve32x(SolveArgs a, const float4* packed,
+                                                          int forceFallback) {
+    __shared__ float4 table[kMaxCells * kCellStride];
+    const int pw = a.lw + 2;  // h = 1
+    const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
+    const int ocx0 = div_s(x0, a), ocy0 = div_s(y0, a);
+    const int ncw = div_s(min(x0 + kTX - 1, a.W - 1), a) - ocx0 + 1;
+    const int nch = div_s(min(y0 + kTY - 1, a.H - 1), a) - ocy0 + 1;
+    const float eps = a.epsf;
+    for (int idx = threadIdx.x; idx < ncw * nch * kPairs; idx += kThreads) {
+        const int cell = idx / kPairs, pr = idx - cell * kPairs;
+        const int cx = ocx0 + cell % ncw, cy = ocy0 + cell / ncw;
+        int i, j;
+        pair_ij(pr, i, j);
+        const float4* win = packed + size_t(cy) * pw + cx;
+        const float4 ci = __ldg(win + (i / 3) * pw + i % 3), cj = __ldg(win + (j / 3) * pw + j % 3);
+        const float d0 = ci.x - cj.x, d1 = ci.y - cj.y, d2 = ci.z - cj.z;
+        const float den = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmaf_rn(d0, d0, eps)));
+        table[cell * kCellStride + pr] = make_float4(d0, d1, d2, rcp_approx(den));
+    }
+    __syncthreads();
+
+    const int x = x0 + (threadIdx.x % kTX), y = y0 + (threadIdx.x / kTX);
+    if (x >= a.W || y >= a.H) return;
+    const size_t p = size_t(y) * a.W + x;
+    const int cx = div_s(x, a), cy = div_s(y, a);
+    const float4* win = packed + size_t(cy) * pw + cx;
+    const float4* tab = table + ((cy - ocy0) * ncw + (cx - ocx0)) * kCellStride;
+    const float ip0 = __ldg(a.high + 3 * p), ip1 = __ldg(a.high + 3 * p + 1),
+                ip2 = __ldg(a.high + 3 * p + 2);
+
+    float e0[9], e1[9], e2[9], q[9];
+    float qmax = 0.0f, qmin = kInf;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        const float4 v = __ldg(win + (k / 3) * pw + k % 3);
+        e0[k] = v.x - ip0;
+        e1[k] = v.y - ip1;
+        e2[k] = v.z - ip2;
+        q[k] = __fmaf_rn(e2[k], e2[k], __fmaf_rn(e1[k], e1[k], __fmul_rn(e0[k], e0[k])));
+        qmax = fmaxf(qmax, q[k] < kInf ? q[k] : 0.0f);
+        qmin = fminf(qmin, q[k]);
+    }
+    // lexicographic scan over (i <= j), first strict argmin + second best
+    float b1 = kInf, b2 = kInf;
+    int bi = 0, bj = 0;
+    {
+        int pr = 0;
+#pragma unroll
+        for (int i = 0; i < 9; ++i) {
+            {
+                const float o = q[i];  // (i, i): w = 0
+                const bool lt = o < b1;
+                b2 = lt ? b1 : fminf(b2, o);
+                b1 = lt ? o : b1;
+                bi = lt ? i : bi;
+                bj = lt ? i : bj;
+            }
+#pragma unroll
+            for (int j = i + 1; j < 9; ++j, ++pr) {
+                const float4 t = tab[pr];
+                const float num = -__fmaf_rn(e0[j], t.x, __fmaf_rn(e1[j], t.y, e2[j] * t.z));
+                const float o = __fmaf_rn(-num * num, t.w, q[j]);
+                const bool lt = o < b1;
+                b2 = lt ? b1 : fminf(b2, o);
+                b1 = lt ? o : b1;
+                bi = lt ? i : bi;
+                bj = lt ? j : bj;
+            }
+        }
+    }
+    const float4 ci = __ldg(win + (bi / 3) * pw + bi % 3), cj = __ldg(win + (bj / 3) * pw + bj % 3);
+    bool ok = !forceFallback && b1 < kInf && ip0 == ip0 && ip1 == ip1 && ip2 == ip2 &&
+              (qmin >= 1e-27f || qmin == 0.0f);
+    const float M = kCE * kU * qmax + 1e-36f;
+    // An exact zero with I_bj == I_p is exact in double too (w = 0, v = 0);
+    // every other true zero also has e_j = 0 and evaluates to exactly 0 in
+    // fp32, so the first zero in lexicographic order is the reference's pick.
+    // (Every LR sample pixel lands here: all pairs (i, k) with I_k = I_p tie.)
+    const bool exactZero = b1 == 0.0f && cj.x == ip0 && cj.y == ip1 && cj.z == ip2;
+    if (ok && !exactZero && b2 <= b1 + 2.0f * M) {
+        // rare: per-pair bounds; a close pair must have the winner's colours
+        const float mb = kCE * kU * q[bj] + 1e-36f;
+        int pr = 0;
+#pragma unroll
+        for (int i = 0; i < 9; ++i) {
+#pragma unroll
+            for (int j = i; j < 9; ++j) {
+                float o;
+                if (j == i) {
+                    o = q[i];
+                } else {
+                    const float4 t = tab[pr++];
+                    const float num = -__fmaf_rn(e0[j], t.x, __fmaf_rn(e1[j], t.y, e2[j] * t.z));
+                    o = __fmaf_rn(-num * num, t.w, q[j]);
+                }
+                if (i == bi && j == bj) continue;
+                if (!(o <= kInf)) continue;  // NaN: outside the grid
+                if (o - (kCE * kU * q[j] + 1e-36f) <= b1 + mb) {
+                    const float4 vi = __ldg(win + (i / 3) * pw + i % 3);
+                    const float4 vj = __ldg(win + (j / 3) * pw + j % 3);
+                    if (!(same_rgb(vi, ci) && same_rgb(vj, cj))) ok = false;
+                }
+            }
+        }
+    }
+    // stage-A style guard: an exact-zero distance must be a true colour match
+    if (ok && qmin == 0.0f) {
+        for (int k = 0; k < 9; ++k)
+            if (q[k] == 0.0f && !(e0[k] == 0.0f && e1[k] == 0.0f && e2[k] == 0.0f)) ok = false;
+    }
+    (void)kCA;
+    uint32_t ia, ib;
+    float w;
+    if (ok) {
+        ia = uint32_t(cy - 1 + bi / 3) * uint32_t(a.lw) + uint32_t(cx - 1 + bi % 3);
+        ib = uint32_t(cy - 1 + bj / 3) * uint32_t(a.lw) + uint32_t(cx - 1 + bj % 3);
+        const float ip[3] = {ip0, ip1, ip2};
+        const float a3[3] = {ci.x, ci.y, ci.z}, b3[3] = {cj.x, cj.y, cj.z};
+        w = float(weight_exact64(ip, a3, b3, a.eps));
+    } else {
+        const int wx0 = max(0, cx - 1), wy0 = max(0, cy - 1);
+        const int nwx = min(a.lw - 1, cx + 1) - wx0 + 1;
+        const int nwy = min(a.lh - 1, cy + 1) - wy0 + 1;
+        const float ip[3] = {ip0, ip1, ip2};
+        PackedWindow pwin{packed + size_t(wy0 + 1) * pw + (wx0 + 1), pw, nwx};
+        const Pick pk = pick_exact64(ip, pwin, nwx * nwy, a.eps);
+        const int ar = pk.ai / nwx, br = pk.bi / nwx;
+        ia = uint32_t(wy0 + ar) * uint32_t(a.lw) + uint32_t(wx0 + pk.ai - ar * nwx);
+        ib = uint32_t(wy0 + br) * uint32_t(a.lw) + uint32_t(wx0 + pk.bi - br * nwx);
+        w = float(pk.w);
+        if (a.fallbacks) atomicAdd(a.fallbacks, 1ull);
+    }
+    if (a.params) {
+        unsigned* o = reinterpret_cast<unsigned*>(a.params + p);
+        o[0] = ia;
+        o[1] = ib;
+        o[2] = __float_as_uint(w);
+    }
+    if (a.lowT) {
+        const int C = a.channels;
+        for (int k = 0; k < C; ++k)
+            a.out[C * p + k] = lerp_clamp(w, __ldg(a.lowT + size_t(C) * ia + k),
+                                          __ldg(a.lowT + size_t(C) * ib + k), a.clamp != 0);
+    }
+}
+
+}  // namespace
+
+bool solve32x_supported(int mode, int S, int s) {
+    return mode == GLU_MODE_EXACT && S == 3 && s >= 3;
+}
+
+cudaError_t launch_solve32x(glu_ctx* ctx, const SolveArgs& a, const float4* packed,
+                            int forceFallback) {
+    dim3 grid((a.W + kTX - 1) / kTX, (a.H + kTY - 1) / kTY);
+    k_solve32x<<<grid, kThreads, 0, ctx->stream>>>(a, packed, forceFallback);
+    ++ctx->launches;
+    return cudaGetLastError();
+}
+
+}  // namespace glu_cu

@@ -252,7 +252,7 @@ def _stress_images():
     yield "two_level", (rng.random((200, 320, 1)) < 0.5).repeat(3, 2).astype(np.float32)
 
 
-@pytest.mark.parametrize("mode", ["fast", "gnu"])
+@pytest.mark.parametrize("mode", ["fast", "gnu", "exact"])
 @pytest.mark.parametrize("S", [3, 5])
 def test_fp32_filter_matches_oracle_on_stress_images(glu, oracle, mode, S):
     ctx = glu.glu.context()
