@@ -128,7 +128,8 @@ int glu_abi_version(void) { return GLU_CUDA_ABI_VERSION; }
 const char* glu_last_error(void) { return g_last_error.c_str(); }
 
 const char* glu_build_info(void) {
-    return "glu_cuda sm_100a; fp64-exact selection; -fmad=false; built " __DATE__ " " __TIME__;
+    return "glu_cuda sm_100a; fp32 filter + fp64 verify selection (bit-exact); -fmad=false; "
+           "built " __DATE__ " " __TIME__;
 }
 
 int glu_grid_create(int highW, int highH, int scale, glu_grid* out) {
