@@ -38,7 +38,7 @@ extern "C" {
 
 #define GLU_CUDA_ABI_VERSION 1
 
-enum glu_status { GLU_OK = 0, GLU_EINVAL = 1, GLU_ECUDA = 2, GLU_ENOMEM = 3 };
+enum glu_status { GLU_OK = 0, GLU_EINVAL = 1, GLU_ECUDA = 2, GLU_ENOMEM = 3, GLU_EFORMAT = 4 };
 /* glu::Mode (params.hpp:11-15) */
 enum glu_mode { GLU_MODE_FAST = 0, GLU_MODE_EXACT = 1, GLU_MODE_GNU = 2 };
 
@@ -210,6 +210,25 @@ int glu_cu_optimize_pixel_batch(glu_ctx* ctx, const float* ip, const uint32_t* o
 int glu_cu_pair_eval(glu_ctx* ctx, const float* ip, const float* ia, const float* ib,
                      const double* w, size_t count, double eps, double* weightExact,
                      double* weightFast, double* objective);
+
+/* ---- GLUP parameter files (io_glup.cpp:48-139; proj/README.md:97-117) --- */
+
+/* Bytes of the GLUP encoding of a field on `grid`. */
+size_t glu_glup_size(const glu_grid* grid);
+/* encode_glup: header + the LR image + the records, streamed from device
+ * buffers straight into `out` (pinned host memory or device memory). */
+int glu_cu_glup_encode(glu_ctx* ctx, const glu_pixel_params* field, const float* low,
+                       const glu_grid* grid, int mode, int optimized, uint8_t* out,
+                       size_t capacity);
+/* decode_glup: validates the header (host), copies the payload into device
+ * buffers and validates it on the device.  With low or field NULL only the
+ * header is checked and the grid / mode / flag are returned ("peek").
+ * Format violations return GLU_EFORMAT; glu_last_error() holds the
+ * reference's message and glu_last_error_field() its field name (length,
+ * magic, version, dims, mode, flag, reserved, lowres, index, weight). */
+int glu_cu_glup_decode(glu_ctx* ctx, const uint8_t* bytes, size_t size, glu_grid* grid,
+                       int* mode, int* optimized, float* low, glu_pixel_params* field);
+const char* glu_last_error_field(void);
 
 /* ---- host-pointer entry points (the C++ API's calls) ------------------- */
 

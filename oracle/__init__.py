@@ -236,6 +236,37 @@ class Reference(_Common):
     def set_num_threads(self, n: int) -> None:
         self.lib.glu_r_set_num_threads(n)
 
+    def encode_glup(self, field, low, s, mode=0, optimized=False) -> bytes:
+        """encode_glup (io_glup.cpp:48-77) of the reference."""
+        L = self.lib
+        L.glu_r_encode_glup.restype = C.c_long
+        L.glu_r_encode_glup.argtypes = [_parp, _f32p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                        C.c_int, C.c_void_p, C.c_size_t]
+        field = np.ascontiguousarray(field)
+        H, W = field.shape
+        n = L.glu_r_encode_glup(field, _f32(low), W, H, s, int(mode), int(optimized), None, 0)
+        if n < 0:
+            raise ValueError("encode_glup: invalid input")
+        out = (C.c_uint8 * n)()
+        L.glu_r_encode_glup(field, _f32(low), W, H, s, int(mode), int(optimized), out, n)
+        return bytes(out)
+
+    def decode_glup(self, data: bytes):
+        """decode_glup (io_glup.cpp:79-139): (ok, field-or-error-field, dims)."""
+        L = self.lib
+        L.glu_r_decode_glup.restype = C.c_int
+        L.glu_r_decode_glup.argtypes = [C.c_void_p, C.c_size_t, _i32p, C.c_void_p, C.c_void_p,
+                                        C.c_char_p, C.c_size_t]
+        dims = np.zeros(5, np.int32)
+        buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data or b"\0")
+        fld = C.create_string_buffer(32)
+        rc = L.glu_r_decode_glup(buf, len(data), dims, None, None, fld, 32)
+        if rc == 1:
+            return False, fld.value.decode(), None
+        if rc != 0:
+            raise RuntimeError("decode_glup failed")
+        return True, None, dims.tolist()
+
     def synth(self, kind: str, w: int, h: int, seed: int) -> np.ndarray:
         out = np.zeros((h, w, 3), np.float32)
         if self.lib.glu_r_synth(kind.encode(), w, h, seed, out):

@@ -6,12 +6,14 @@
 // It is used (1) to generate the golden vectors in tests/golden/ that pin
 // oracle/glu_oracle.c, and (2) as the CPU baseline ("kind": "reference") timed
 // by bench.py.  Nothing in the product links it.
+#include <cstdio>
 #include <cstring>
 #include <span>
 #include <thread>
 #include <vector>
 
 #include "glu/grid.hpp"
+#include "glu/io.hpp"
 #include "glu/jointopt.hpp"
 #include "glu/parallel.hpp"
 #include "glu/simop.hpp"
@@ -218,6 +220,48 @@ int glu_r_joint_optimize(const float* high, int W, int H, int s, int S, float th
         counters[1] = r.trialsAccepted;
         counters[2] = r.trialsRejected;
     });
+}
+
+// encode_glup (io_glup.cpp:48-77): writes up to cap bytes, returns the size.
+long glu_r_encode_glup(const PixelParams* params, const float* low, int W, int H, int s,
+                       int mode, int optimized, uint8_t* out, size_t cap) {
+    long n = -1;
+    guarded([&] {
+        GlupFile f;
+        f.field.grid = GridSpec::create(W, H, s);
+        f.field.mode = static_cast<Mode>(mode);
+        f.field.params.assign(params, params + static_cast<size_t>(W) * H);
+        f.low = wrap(low, f.field.grid.lowW, f.field.grid.lowH);
+        f.optimized = optimized != 0;
+        const std::vector<uint8_t> b = encode_glup(f);
+        if (b.size() <= cap) std::memcpy(out, b.data(), b.size());
+        n = static_cast<long>(b.size());
+    });
+    return n;
+}
+
+// decode_glup (io_glup.cpp:79-139): 0 ok, 1 FormatError (field copied into
+// `field`), 2 other exception.  Outputs are written only on success.
+int glu_r_decode_glup(const uint8_t* bytes, size_t n, int* dims, float* low, PixelParams* params,
+                      char* field, size_t fieldCap) {
+    try {
+        const GlupFile f = decode_glup(std::vector<uint8_t>(bytes, bytes + n));
+        const GridSpec& g = f.field.grid;
+        dims[0] = g.highW;
+        dims[1] = g.highH;
+        dims[2] = g.scale;
+        dims[3] = static_cast<int>(f.field.mode);
+        dims[4] = f.optimized ? 1 : 0;
+        if (low) std::memcpy(low, f.low.data.data(), f.low.data.size() * sizeof(float));
+        if (params)
+            std::memcpy(params, f.field.params.data(), f.field.params.size() * sizeof(PixelParams));
+        return 0;
+    } catch (const FormatError& e) {
+        std::snprintf(field, fieldCap, "%s", e.field.c_str());
+        return 1;
+    } catch (const std::exception&) {
+        return 2;
+    }
 }
 
 }  // extern "C"

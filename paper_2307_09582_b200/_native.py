@@ -35,6 +35,14 @@ class GluError(RuntimeError):
     """A CUDA / runtime failure reported by the C-ABI (GLU_ECUDA / GLU_ENOMEM)."""
 
 
+class FormatError(RuntimeError):
+    """glu::FormatError (io.hpp:15-20): a structurally invalid GLUP file."""
+
+    def __init__(self, field: str, msg: str):
+        super().__init__(msg)
+        self.field = field
+
+
 # Every symbol include/glu_cuda.h declares, with its ctypes signature.
 P, I, SZ, D, F, U64 = C.c_void_p, C.c_int, C.c_size_t, C.c_double, C.c_float, C.c_ulonglong
 GP, CP, SP = C.POINTER(GluGrid), C.POINTER(GluConfigC), C.POINTER(GluJointStats)
@@ -69,6 +77,10 @@ SIGNATURES: dict[str, tuple] = {
     "glu_cu_upsample_frames": (I, [P, P, I, GP, CP, I, I, P, P]),
     "glu_h_upsample_frames": (I, [P, P, I, GP, CP, I, I, P, P]),
     "glu_cu_fp32_peak": (I, [P, C.POINTER(D), C.POINTER(D)]),
+    "glu_glup_size": (SZ, [GP]),
+    "glu_cu_glup_encode": (I, [P, P, P, GP, I, I, P, SZ]),
+    "glu_cu_glup_decode": (I, [P, P, SZ, GP, C.POINTER(I), C.POINTER(I), P, P]),
+    "glu_last_error_field": (C.c_char_p, []),
     "glu_cu_op_color": (I, [P, P, SZ, P, P, D, P]),
     "glu_cu_op_matte": (I, [P, P, SZ, P]),
     "glu_cu_optimize_pixel_batch": (I, [P, P, P, P, P, SZ, D, I, P]),
@@ -113,6 +125,8 @@ def check(rc: int) -> None:
         raise ValueError(msg)  # std::invalid_argument in the reference
     if rc == GLU_ENOMEM:
         raise MemoryError(msg)
+    if rc == 4:  # GLU_EFORMAT
+        raise FormatError(lib().glu_last_error_field().decode(), msg)
     raise GluError(msg)
 
 

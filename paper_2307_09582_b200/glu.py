@@ -562,3 +562,50 @@ def fp32_peak(device: int | None = None) -> tuple[float, float]:
     t, m = C.c_double(), C.c_double()
     N.check(N.lib().glu_cu_fp32_peak(ctx.handle, C.byref(t), C.byref(m)))
     return t.value, m.value
+
+
+# ---- GLUP parameter files (io_glup.cpp:48-139) ----------------------------------
+
+FormatError = N.FormatError
+
+
+def encode_glup(field: ParamField, low: torch.Tensor, optimized: bool = False,
+                out: torch.Tensor | None = None) -> torch.Tensor:
+    """encode_glup: device field + LR image -> GLUP bytes (uint8 tensor, pinned
+    host memory by default, or a device tensor passed as `out`)."""
+    g = field.grid
+    if low.shape[1] != g.lowW or low.shape[0] != g.lowH:
+        raise ValueError("encode_glup: low-res image does not match grid")
+    if field.params.numel() != 3 * g.highW * g.highH:
+        raise ValueError("encode_glup: param count does not match grid")
+    n = int(N.lib().glu_glup_size(C.byref(g.c())))
+    if out is None:
+        out = torch.empty(n, dtype=torch.uint8).pin_memory()
+    ctx = context(field.params.device.index)
+    N.check(N.lib().glu_cu_glup_encode(ctx.handle, _ptr(field.params), _ptr(low.contiguous()),
+                                       C.byref(g.c()), int(field.mode), int(bool(optimized)),
+                                       C.c_void_p(out.data_ptr()), out.numel()))
+    return out
+
+
+def decode_glup(data, device: int | None = None):
+    """decode_glup: GLUP bytes (bytes / numpy / uint8 tensor, host or device) ->
+    (ParamField, low, optimized) on the device; raises FormatError(field, msg)."""
+    if isinstance(data, (bytes, bytearray)):
+        data = torch.frombuffer(bytearray(data), dtype=torch.uint8) if len(data) else \
+            torch.empty(0, dtype=torch.uint8)
+    elif isinstance(data, np.ndarray):
+        data = torch.from_numpy(np.ascontiguousarray(data, np.uint8))
+    data = data.contiguous()
+    ctx = context(device)
+    g, mode, opt = N.GluGrid(), C.c_int(), C.c_int()
+    ptr = C.c_void_p(data.data_ptr() if data.numel() else 0)
+    N.check(N.lib().glu_cu_glup_decode(ctx.handle, ptr, data.numel(), C.byref(g), C.byref(mode),
+                                       C.byref(opt), None, None))
+    dev = torch.device("cuda", ctx.device)
+    low = torch.empty((g.lowH, g.lowW, 3), dtype=torch.float32, device=dev)
+    params = torch.empty((g.highH, g.highW, 3), dtype=torch.int32, device=dev)
+    N.check(N.lib().glu_cu_glup_decode(ctx.handle, ptr, data.numel(), C.byref(g), C.byref(mode),
+                                       C.byref(opt), _ptr(low), _ptr(params)))
+    grid = GridSpec(g.scale, g.highW, g.highH, g.lowW, g.lowH, g.sampleOffset)
+    return ParamField(grid, Mode(mode.value), params), low, bool(opt.value)
