@@ -228,6 +228,29 @@ struct JointResult {
 
 JointResult joint_optimize(const ImageF32& high, int scale, const GluConfig& cfg, Mode mode);
 
+// ---- io.hpp: GLUP parameter files (PNG/PPM image I/O is out of scope) --------
+
+struct IoError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+struct FormatError : std::runtime_error {
+    std::string field;
+    FormatError(std::string fieldName, const std::string& msg)
+        : std::runtime_error(msg), field(std::move(fieldName)) {}
+};
+
+struct GlupFile {
+    ParamField field;
+    ImageF32 low;
+    bool optimized = false;
+};
+
+void write_glup(const std::string& path, const GlupFile& f);
+GlupFile read_glup(const std::string& path);
+std::vector<uint8_t> encode_glup(const GlupFile& f);
+GlupFile decode_glup(const std::vector<uint8_t>& bytes);
+
 // ---- parallel.hpp (host utility kept for drop-in; the GPU path ignores it) ----
 
 void set_num_threads(int n);

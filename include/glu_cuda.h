@@ -118,6 +118,12 @@ unsigned long long glu_ctx_fallback_count(glu_ctx* ctx);
 /* Device-to-device copy on the context stream (e.g. out of the context-owned
  * component buffers of glu_cu_find_large_error). */
 int glu_cu_copy(glu_ctx* ctx, void* dst, const void* src, size_t bytes);
+/* Device memory for C/C++ callers without their own allocator; upload /
+ * download are synchronous host <-> device copies on the context stream. */
+int glu_cu_alloc(glu_ctx* ctx, void** ptr, size_t bytes);
+int glu_cu_free(glu_ctx* ctx, void* ptr);
+int glu_cu_upload(glu_ctx* ctx, void* dst, const void* hostSrc, size_t bytes);
+int glu_cu_download(glu_ctx* ctx, void* hostDst, const void* src, size_t bytes);
 
 /* grid_downsample (grid.cpp:41-52). low: lowW*lowH*3 floats. */
 int glu_cu_grid_downsample(glu_ctx* ctx, const float* high, const glu_grid* grid, float* low);

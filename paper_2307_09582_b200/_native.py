@@ -63,6 +63,10 @@ SIGNATURES: dict[str, tuple] = {
     "glu_ctx_launch_count": (U64, [P]),
     "glu_ctx_fallback_count": (U64, [P]),
     "glu_cu_copy": (I, [P, P, P, SZ]),
+    "glu_cu_alloc": (I, [P, C.POINTER(P), SZ]),
+    "glu_cu_free": (I, [P, P]),
+    "glu_cu_upload": (I, [P, P, P, SZ]),
+    "glu_cu_download": (I, [P, P, P, SZ]),
     "glu_cu_grid_downsample": (I, [P, P, GP, P]),
     "glu_cu_optimize_field": (I, [P, P, P, GP, CP, I, P]),
     "glu_cu_optimize_pixels": (I, [P, P, P, GP, CP, I, P, SZ, P]),

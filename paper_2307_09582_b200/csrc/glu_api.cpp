@@ -5,6 +5,7 @@
 // CPU implementation of the hot path here.
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
 #include <thread>
 
 #include "glu/glu_b200.hpp"
@@ -311,6 +312,87 @@ JointResult joint_optimize(const ImageF32& high, int scale, const GluConfig& cfg
     r.trialsAccepted = st.trialsAccepted;
     r.trialsRejected = st.trialsRejected;
     return r;
+}
+
+// ---- GLUP files (io_glup.cpp:48-159) -------------------------------------------
+
+namespace {
+
+// Device staging for the codec: field + LR image + raw bytes.
+struct DevBuf {
+    void* p = nullptr;
+    explicit DevBuf(size_t n) {
+        if (n && glu_cu_alloc(ctx(), &p, n) != GLU_OK) throw std::bad_alloc();
+    }
+    ~DevBuf() {
+        if (p) glu_cu_free(ctx(), p);
+    }
+};
+
+}  // namespace
+
+std::vector<uint8_t> encode_glup(const GlupFile& f) {
+    const GridSpec& g = f.field.grid;
+    if (g.highW <= 0 || g.highH <= 0 || g.scale < 2)
+        throw std::invalid_argument("encode_glup: field has no grid");
+    if (f.field.params.size() != size_t(g.highW) * g.highH)
+        throw std::invalid_argument("encode_glup: param count does not match grid");
+    if (f.low.width != g.lowW || f.low.height != g.lowH)
+        throw std::invalid_argument("encode_glup: low-res image does not match grid");
+    const glu_grid cg = cgrid(g);
+    std::vector<uint8_t> out(glu_glup_size(&cg));
+    DevBuf dp(f.field.params.size() * sizeof(PixelParams)), dl(f.low.data.size() * 4);
+    check(glu_cu_upload(ctx(), dp.p, f.field.params.data(), f.field.params.size() * 12));
+    check(glu_cu_upload(ctx(), dl.p, f.low.data.data(), f.low.data.size() * 4));
+    check(glu_cu_glup_encode(ctx(), static_cast<const glu_pixel_params*>(dp.p),
+                             static_cast<const float*>(dl.p), &cg, int(f.field.mode),
+                             f.optimized ? 1 : 0, out.data(), out.size()));
+    return out;
+}
+
+GlupFile decode_glup(const std::vector<uint8_t>& bytes) {
+    glu_grid g{};
+    int mode = 0, opt = 0;
+    auto rethrow = [](int rc) {
+        if (rc == GLU_EFORMAT) throw FormatError(glu_last_error_field(), glu_last_error());
+        check(rc);
+    };
+    rethrow(glu_cu_glup_decode(ctx(), bytes.data(), bytes.size(), &g, &mode, &opt, nullptr,
+                               nullptr));
+    GlupFile f;
+    f.field.grid = GridSpec::create(g.highW, g.highH, g.scale);
+    f.field.mode = static_cast<Mode>(mode);
+    f.optimized = opt == 1;
+    f.low = ImageF32(g.lowW, g.lowH);
+    f.field.params.resize(size_t(g.highW) * g.highH);
+    DevBuf dp(f.field.params.size() * 12), dl(f.low.data.size() * 4);
+    rethrow(glu_cu_glup_decode(ctx(), bytes.data(), bytes.size(), &g, &mode, &opt,
+                               static_cast<float*>(dl.p), static_cast<glu_pixel_params*>(dp.p)));
+    check(glu_cu_download(ctx(), f.field.params.data(), dp.p, f.field.params.size() * 12));
+    check(glu_cu_download(ctx(), f.low.data.data(), dl.p, f.low.data.size() * 4));
+    return f;
+}
+
+void write_glup(const std::string& path, const GlupFile& f) {
+    const std::vector<uint8_t> bytes = encode_glup(f);
+    std::FILE* fp = std::fopen(path.c_str(), "wb");
+    if (!fp) throw IoError("cannot open for writing: " + path);
+    const size_t n = std::fwrite(bytes.data(), 1, bytes.size(), fp);
+    const bool bad = n != bytes.size() || std::fclose(fp) != 0;
+    if (bad) throw IoError("write failed: " + path);
+}
+
+GlupFile read_glup(const std::string& path) {
+    std::FILE* fp = std::fopen(path.c_str(), "rb");
+    if (!fp) throw IoError("cannot open: " + path);
+    std::vector<uint8_t> bytes;
+    uint8_t buf[1 << 16];
+    size_t n;
+    while ((n = std::fread(buf, 1, sizeof(buf), fp)) > 0) bytes.insert(bytes.end(), buf, buf + n);
+    const bool bad = std::ferror(fp) != 0;
+    std::fclose(fp);
+    if (bad) throw IoError("read failed: " + path);
+    return decode_glup(bytes);
 }
 
 // ---- parallel (host utility) --------------------------------------------------

@@ -268,6 +268,33 @@ int glu_cu_copy(glu_ctx* ctx, void* dst, const void* src, size_t bytes) {
     return GLU_OK;
 }
 
+int glu_cu_alloc(glu_ctx* ctx, void** ptr, size_t bytes) {
+    if (!ctx || !ptr) return einval("ctx and ptr must not be null");
+    GLU_CUDA(cudaSetDevice(ctx->device), "cudaSetDevice");
+    GLU_CUDA(cudaMalloc(ptr, bytes ? bytes : 1), "cudaMalloc");
+    return GLU_OK;
+}
+
+int glu_cu_free(glu_ctx* ctx, void* ptr) {
+    if (!ctx) return einval("ctx must not be null");
+    GLU_CUDA(cudaStreamSynchronize(ctx->stream), "synchronize");
+    GLU_CUDA(cudaFree(ptr), "cudaFree");
+    return GLU_OK;
+}
+
+int glu_cu_upload(glu_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    if (!ctx) return einval("ctx must not be null");
+    if (bytes == 0) return GLU_OK;
+    GLU_TRY(h2d(ctx, dst, src, bytes));
+    GLU_CUDA(cudaStreamSynchronize(ctx->stream), "synchronize");
+    return GLU_OK;
+}
+
+int glu_cu_download(glu_ctx* ctx, void* dst, const void* src, size_t bytes) {
+    if (!ctx) return einval("ctx must not be null");
+    return d2h_sync(ctx, dst, src, bytes);
+}
+
 int glu_cu_grid_downsample(glu_ctx* ctx, const float* high, const glu_grid* g, float* low) {
     if (!ctx) return einval("ctx must not be null");
     GLU_TRY(check_grid(g));

@@ -78,3 +78,18 @@ def test_encode_validates_input(glu):
     field, low = _sample(glu)
     with pytest.raises(ValueError):
         glu.glu.encode_glup(field, torch.zeros((3, 3, 3), device="cuda"))
+
+
+def test_cpp_dropin_io_api(glu, tmp_path):
+    """include/glu/io.hpp through lib/libglu.so from a C++ program."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(root, "paper_2307_09582_b200", "lib")
+    exe = tmp_path / "dropin_io_test"
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I" + os.path.join(root, "include"),
+                    os.path.join(root, "tests", "cpp", "dropin_io_test.cpp"), "-L" + lib,
+                    "-lglu", "-lglu_cuda", "-Wl,-rpath," + lib, "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe), str(tmp_path / "x.glup")], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
