@@ -228,6 +228,19 @@ struct JointResult {
 
 JointResult joint_optimize(const ImageF32& high, int scale, const GluConfig& cfg, Mode mode);
 
+// ---- metrics.hpp -----------------------------------------------------------------
+
+struct QualityReport {
+    double mse = 0;
+    double psnrDb = 0;
+    double ssim = 0;
+};
+
+double mse(const ImageF32& a, const ImageF32& b);
+double psnr(const ImageF32& a, const ImageF32& b);
+double ssim(const ImageF32& a, const ImageF32& b);
+QualityReport quality_report(const ImageF32& reference, const ImageF32& test);
+
 // ---- io.hpp: GLUP parameter files (PNG/PPM image I/O is out of scope) --------
 
 struct IoError : std::runtime_error {

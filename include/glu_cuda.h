@@ -236,6 +236,14 @@ int glu_cu_glup_decode(glu_ctx* ctx, const uint8_t* bytes, size_t size, glu_grid
                        int* mode, int* optimized, float* low, glu_pixel_params* field);
 const char* glu_last_error_field(void);
 
+/* ---- quality metrics (metrics.cpp:62-107) -------------------------------- */
+
+/* mse: mean of squared differences over `count` floats (device pointers). */
+int glu_cu_mse(glu_ctx* ctx, const float* a, const float* b, size_t count, double* out);
+/* ssim: luma SSIM, 11x11 Gaussian sigma 1.5, valid windows, RGB images. */
+int glu_cu_ssim(glu_ctx* ctx, const float* a, const float* b, int width, int height,
+                double* out);
+
 /* ---- host-pointer entry points (the C++ API's calls) ------------------- */
 
 int glu_h_grid_downsample(glu_ctx* ctx, const float* high, const glu_grid* grid, float* low);

@@ -236,6 +236,17 @@ class Reference(_Common):
     def set_num_threads(self, n: int) -> None:
         self.lib.glu_r_set_num_threads(n)
 
+    def quality(self, a, b):
+        """(mse, psnr, ssim) of the reference (metrics.cpp:62-115)."""
+        L = self.lib
+        L.glu_r_quality.argtypes = [_f32p, _f32p, C.c_int, C.c_int,
+                                    np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")]
+        a = _f32(a)
+        out = np.zeros(3, np.float64)
+        if L.glu_r_quality(a, _f32(b), a.shape[1], a.shape[0], out):
+            raise ValueError("quality: invalid images")
+        return tuple(out.tolist())
+
     def encode_glup(self, field, low, s, mode=0, optimized=False) -> bytes:
         """encode_glup (io_glup.cpp:48-77) of the reference."""
         L = self.lib

@@ -15,6 +15,7 @@
 #include "glu/grid.hpp"
 #include "glu/io.hpp"
 #include "glu/jointopt.hpp"
+#include "glu/metrics.hpp"
 #include "glu/parallel.hpp"
 #include "glu/simop.hpp"
 #include "glu/synth.hpp"
@@ -219,6 +220,16 @@ int glu_r_joint_optimize(const float* high, int W, int H, int s, int S, float th
         counters[0] = r.iterations;
         counters[1] = r.trialsAccepted;
         counters[2] = r.trialsRejected;
+    });
+}
+
+// mse / psnr / ssim (metrics.cpp:62-107); out = {mse, psnr, ssim}.
+int glu_r_quality(const float* a, const float* b, int W, int H, double* out) {
+    return guarded([&] {
+        const QualityReport q = quality_report(wrap(a, W, H), wrap(b, W, H));
+        out[0] = q.mse;
+        out[1] = q.psnrDb;
+        out[2] = q.ssim;
     });
 }
 

@@ -395,6 +395,55 @@ GlupFile read_glup(const std::string& path) {
     return decode_glup(bytes);
 }
 
+// ---- metrics (metrics.cpp:62-115) ------------------------------------------------
+
+namespace {
+
+struct DevPair {
+    DevBuf a, b;
+    DevPair(const ImageF32& x, const ImageF32& y)
+        : a(x.data.size() * sizeof(float)), b(y.data.size() * sizeof(float)) {
+        check(glu_cu_upload(ctx(), a.p, x.data.data(), x.data.size() * sizeof(float)));
+        check(glu_cu_upload(ctx(), b.p, y.data.data(), y.data.size() * sizeof(float)));
+    }
+    const float* fa() const { return static_cast<const float*>(a.p); }
+    const float* fb() const { return static_cast<const float*>(b.p); }
+};
+
+}  // namespace
+
+double mse(const ImageF32& a, const ImageF32& b) {
+    requireSameShape(a, b, "mse");
+    DevPair d(a, b);
+    double m = 0;
+    check(glu_cu_mse(ctx(), d.fa(), d.fb(), a.data.size(), &m));
+    return m;
+}
+
+double psnr(const ImageF32& a, const ImageF32& b) {
+    const double m = mse(a, b);
+    if (m == 0) return 99.0;
+    return 10.0 * std::log10(1.0 / m);
+}
+
+double ssim(const ImageF32& a, const ImageF32& b) {
+    requireSameShape(a, b, "ssim");
+    if (a.width < 11 || a.height < 11)
+        throw std::invalid_argument("ssim: images smaller than the 11x11 window");
+    DevPair d(a, b);
+    double s = 0;
+    check(glu_cu_ssim(ctx(), d.fa(), d.fb(), a.width, a.height, &s));
+    return s;
+}
+
+QualityReport quality_report(const ImageF32& reference, const ImageF32& test) {
+    QualityReport q;
+    q.mse = mse(reference, test);
+    q.psnrDb = q.mse == 0 ? 99.0 : 10.0 * std::log10(1.0 / q.mse);
+    q.ssim = ssim(reference, test);
+    return q;
+}
+
 // ---- parallel (host utility) --------------------------------------------------
 
 void set_num_threads(int n) {

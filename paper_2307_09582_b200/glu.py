@@ -609,3 +609,43 @@ def decode_glup(data, device: int | None = None):
                                        C.byref(opt), _ptr(low), _ptr(params)))
     grid = GridSpec(g.scale, g.highW, g.highH, g.lowW, g.lowH, g.sampleOffset)
     return ParamField(grid, Mode(mode.value), params), low, bool(opt.value)
+
+
+# ---- quality metrics (metrics.cpp:62-117) ----------------------------------------
+
+def mse(a: torch.Tensor, b: torch.Tensor) -> float:
+    """mse (metrics.cpp:62-70)."""
+    if a.shape != b.shape:
+        raise ValueError("mse: image dimensions differ")
+    a, b = a.contiguous(), b.contiguous()
+    out = C.c_double()
+    ctx = context(a.device.index)
+    N.check(N.lib().glu_cu_mse(ctx.handle, _ptr(a), _ptr(b), a.numel(), C.byref(out)))
+    return out.value
+
+
+def psnr(a: torch.Tensor, b: torch.Tensor) -> float:
+    """psnr (metrics.cpp:72-76): 99 dB for identical images."""
+    import math
+    m = mse(a, b)
+    return 99.0 if m == 0 else 10.0 * math.log10(1.0 / m)
+
+
+def ssim(a: torch.Tensor, b: torch.Tensor) -> float:
+    """ssim (metrics.cpp:78-107) on the BT.601 luma channel."""
+    if a.shape != b.shape:
+        raise ValueError("ssim: image dimensions differ")
+    a, b = _image(a, "ssim"), _image(b, "ssim")
+    out = C.c_double()
+    ctx = context(a.device.index)
+    N.check(N.lib().glu_cu_ssim(ctx.handle, _ptr(a), _ptr(b), a.shape[1], a.shape[0],
+                                C.byref(out)))
+    return out.value
+
+
+def quality_report(reference: torch.Tensor, test: torch.Tensor) -> dict:
+    """quality_report (metrics.cpp:109-115)."""
+    m = mse(reference, test)
+    import math
+    return {"mse": m, "psnrDb": 99.0 if m == 0 else 10.0 * math.log10(1.0 / m),
+            "ssim": ssim(reference, test)}
