@@ -228,6 +228,26 @@ struct JointResult {
 
 JointResult joint_optimize(const ImageF32& high, int scale, const GluConfig& cfg, Mode mode);
 
+// ---- baseline.hpp: comparison upsamplers -----------------------------------------
+
+struct JbuParams {
+    int window = 5;
+    double sigmaD = 0.5;
+    double sigmaR = 0.1;
+
+    void validate() const {
+        if (window < 1 || window % 2 == 0)
+            throw std::invalid_argument("JbuParams: window must be odd and >= 1");
+        if (!(sigmaD > 0) || !(sigmaR > 0))
+            throw std::invalid_argument("JbuParams: sigmas must be > 0");
+    }
+};
+
+ImageF32 jbu_upsample(const ImageF32& guideHigh, const ImageF32& guideLow,
+                      const ImageF32& targetLow, const GridSpec& grid, const JbuParams& params);
+ImageF32 nearest_upsample(const ImageF32& targetLow, const GridSpec& grid);
+ImageF32 bilinear_upsample(const ImageF32& targetLow, const GridSpec& grid);
+
 // ---- metrics.hpp -----------------------------------------------------------------
 
 struct QualityReport {

@@ -244,6 +244,17 @@ int glu_cu_mse(glu_ctx* ctx, const float* a, const float* b, size_t count, doubl
 int glu_cu_ssim(glu_ctx* ctx, const float* a, const float* b, int width, int height,
                 double* out);
 
+/* ---- comparison upsamplers (baseline.cpp:30-129) ------------------------- */
+
+int glu_cu_nearest_upsample(glu_ctx* ctx, const float* lowTarget, const glu_grid* grid,
+                            float* out);
+int glu_cu_bilinear_upsample(glu_ctx* ctx, const float* lowTarget, const glu_grid* grid,
+                             float* out);
+/* JbuParams {window (odd >= 1), sigmaD, sigmaR} (baseline.hpp:8-14). */
+int glu_cu_jbu_upsample(glu_ctx* ctx, const float* guideHigh, const float* guideLow,
+                        const float* targetLow, const glu_grid* grid, int window,
+                        double sigmaD, double sigmaR, float* out);
+
 /* ---- host-pointer entry points (the C++ API's calls) ------------------- */
 
 int glu_h_grid_downsample(glu_ctx* ctx, const float* high, const glu_grid* grid, float* low);

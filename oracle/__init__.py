@@ -236,6 +236,29 @@ class Reference(_Common):
     def set_num_threads(self, n: int) -> None:
         self.lib.glu_r_set_num_threads(n)
 
+    def baseline(self, kind: str, target, s, guide_high=None, guide_low=None, window=5,
+                 sigma_d=0.5, sigma_r=0.1):
+        """nearest / bilinear / jbu upsampling of the reference (baseline.cpp:30-129)."""
+        L = self.lib
+        L.glu_r_baseline.argtypes = [C.c_int, C.c_void_p, C.c_void_p, _f32p, C.c_int, C.c_int,
+                                     C.c_int, C.c_int, C.c_double, C.c_double, _f32p]
+        t = _f32(target)
+        lh, lw = t.shape[:2]
+        if guide_high is not None:
+            gh = _f32(guide_high)
+            H, W = gh.shape[:2]
+        else:
+            H, W = lh * s, lw * s
+            gh = None
+        out = np.zeros((H, W, 3), np.float32)
+        k = {"nearest": 0, "bilinear": 1, "jbu": 2}[kind]
+        gl = _f32(guide_low) if guide_low is not None else None
+        if L.glu_r_baseline(k, gh.ctypes.data if gh is not None else None,
+                            gl.ctypes.data if gl is not None else None, t, W, H, s, window,
+                            sigma_d, sigma_r, out):
+            raise ValueError(kind + ": invalid arguments")
+        return out
+
     def quality(self, a, b):
         """(mse, psnr, ssim) of the reference (metrics.cpp:62-115)."""
         L = self.lib

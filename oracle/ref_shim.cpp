@@ -12,6 +12,7 @@
 #include <thread>
 #include <vector>
 
+#include "glu/baseline.hpp"
 #include "glu/grid.hpp"
 #include "glu/io.hpp"
 #include "glu/jointopt.hpp"
@@ -220,6 +221,28 @@ int glu_r_joint_optimize(const float* high, int W, int H, int s, int S, float th
         counters[0] = r.iterations;
         counters[1] = r.trialsAccepted;
         counters[2] = r.trialsRejected;
+    });
+}
+
+// jbu / nearest / bilinear (baseline.cpp:30-129); kind 0 nearest, 1 bilinear, 2 jbu.
+int glu_r_baseline(int kind, const float* guideHigh, const float* guideLow, const float* target,
+                   int W, int H, int s, int window, double sigmaD, double sigmaR, float* out) {
+    return guarded([&] {
+        const GridSpec g = GridSpec::create(W, H, s);
+        const ImageF32 t = wrap(target, g.lowW, g.lowH);
+        ImageF32 o;
+        if (kind == 0)
+            o = nearest_upsample(t, g);
+        else if (kind == 1)
+            o = bilinear_upsample(t, g);
+        else {
+            JbuParams p;
+            p.window = window;
+            p.sigmaD = sigmaD;
+            p.sigmaR = sigmaR;
+            o = jbu_upsample(wrap(guideHigh, W, H), wrap(guideLow, g.lowW, g.lowH), t, g, p);
+        }
+        std::memcpy(out, o.data.data(), o.data.size() * sizeof(float));
     });
 }
 

@@ -85,6 +85,9 @@ SIGNATURES: dict[str, tuple] = {
     "glu_cu_glup_encode": (I, [P, P, P, GP, I, I, P, SZ]),
     "glu_cu_glup_decode": (I, [P, P, SZ, GP, C.POINTER(I), C.POINTER(I), P, P]),
     "glu_last_error_field": (C.c_char_p, []),
+    "glu_cu_nearest_upsample": (I, [P, P, GP, P]),
+    "glu_cu_bilinear_upsample": (I, [P, P, GP, P]),
+    "glu_cu_jbu_upsample": (I, [P, P, P, P, GP, I, D, D, P]),
     "glu_cu_mse": (I, [P, P, P, SZ, C.POINTER(D)]),
     "glu_cu_ssim": (I, [P, P, P, I, I, C.POINTER(D)]),
     "glu_cu_op_color": (I, [P, P, SZ, P, P, D, P]),

@@ -25,7 +25,7 @@ NVFLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler",
                   "-diag-suppress", "177,550",
                   "-I" + INCLUDE]
 CUDA_SRCS = ["glu_kernels.cu", "glu_solve32.cu", "glu_solve32x.cu", "glu_joint.cu",
-             "glu_glup.cu", "glu_metrics.cu", "glu_capi.cu"]
+             "glu_glup.cu", "glu_metrics.cu", "glu_baselines.cu", "glu_capi.cu"]
 CUDA_SO = os.path.join(LIB, "libglu_cuda.so")
 CPP_SO = os.path.join(LIB, "libglu.so")
 SYNTH_SO = os.path.join(LIB, "libglu_synth.so")

@@ -324,6 +324,9 @@ struct DevBuf {
     explicit DevBuf(size_t n) {
         if (n && glu_cu_alloc(ctx(), &p, n) != GLU_OK) throw std::bad_alloc();
     }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p) { o.p = nullptr; }
     ~DevBuf() {
         if (p) glu_cu_free(ctx(), p);
     }
@@ -442,6 +445,67 @@ QualityReport quality_report(const ImageF32& reference, const ImageF32& test) {
     q.psnrDb = q.mse == 0 ? 99.0 : 10.0 * std::log10(1.0 / q.mse);
     q.ssim = ssim(reference, test);
     return q;
+}
+
+// ---- comparison upsamplers (baseline.cpp:30-129) -----------------------------------
+
+namespace {
+
+void checkLowGrid(const ImageF32& low, const GridSpec& grid, const char* what) {
+    if (low.width != grid.lowW || low.height != grid.lowH)
+        throw std::invalid_argument(std::string(what) + ": low-res image does not match grid");
+}
+
+ImageF32 downloadImage(const DevBuf& d, int w, int h) {
+    ImageF32 out(w, h);
+    check(glu_cu_download(ctx(), out.data.data(), d.p, out.data.size() * sizeof(float)));
+    return out;
+}
+
+DevBuf uploadImage(const ImageF32& img) {
+    DevBuf d(img.data.size() * sizeof(float));
+    check(glu_cu_upload(ctx(), d.p, img.data.data(), img.data.size() * sizeof(float)));
+    return d;
+}
+
+}  // namespace
+
+ImageF32 jbu_upsample(const ImageF32& guideHigh, const ImageF32& guideLow,
+                      const ImageF32& targetLow, const GridSpec& grid, const JbuParams& params) {
+    params.validate();
+    if (guideHigh.width != grid.highW || guideHigh.height != grid.highH)
+        throw std::invalid_argument("jbu_upsample: guide image does not match grid");
+    checkLowGrid(guideLow, grid, "jbu_upsample");
+    checkLowGrid(targetLow, grid, "jbu_upsample");
+    const DevBuf gh = uploadImage(guideHigh), gl = uploadImage(guideLow),
+                 tl = uploadImage(targetLow);
+    DevBuf out(size_t(grid.highW) * grid.highH * 3 * sizeof(float));
+    const glu_grid cg = cgrid(grid);
+    check(glu_cu_jbu_upsample(ctx(), static_cast<const float*>(gh.p),
+                              static_cast<const float*>(gl.p), static_cast<const float*>(tl.p),
+                              &cg, params.window, params.sigmaD, params.sigmaR,
+                              static_cast<float*>(out.p)));
+    return downloadImage(out, grid.highW, grid.highH);
+}
+
+ImageF32 nearest_upsample(const ImageF32& targetLow, const GridSpec& grid) {
+    checkLowGrid(targetLow, grid, "nearest_upsample");
+    const DevBuf tl = uploadImage(targetLow);
+    DevBuf out(size_t(grid.highW) * grid.highH * 3 * sizeof(float));
+    const glu_grid cg = cgrid(grid);
+    check(glu_cu_nearest_upsample(ctx(), static_cast<const float*>(tl.p), &cg,
+                                  static_cast<float*>(out.p)));
+    return downloadImage(out, grid.highW, grid.highH);
+}
+
+ImageF32 bilinear_upsample(const ImageF32& targetLow, const GridSpec& grid) {
+    checkLowGrid(targetLow, grid, "bilinear_upsample");
+    const DevBuf tl = uploadImage(targetLow);
+    DevBuf out(size_t(grid.highW) * grid.highH * 3 * sizeof(float));
+    const glu_grid cg = cgrid(grid);
+    check(glu_cu_bilinear_upsample(ctx(), static_cast<const float*>(tl.p), &cg,
+                                   static_cast<float*>(out.p)));
+    return downloadImage(out, grid.highW, grid.highH);
 }
 
 // ---- parallel (host utility) --------------------------------------------------

@@ -643,6 +643,58 @@ def ssim(a: torch.Tensor, b: torch.Tensor) -> float:
     return out.value
 
 
+@dataclass
+class JbuParams:
+    """glu::JbuParams (baseline.hpp:8-14)."""
+    window: int = 5
+    sigmaD: float = 0.5
+    sigmaR: float = 0.1
+
+
+def _baseline_out(g: GridSpec, ref: torch.Tensor) -> torch.Tensor:
+    return torch.empty((g.highH, g.highW, 3), dtype=torch.float32, device=ref.device)
+
+
+def nearest_upsample(targetLow: torch.Tensor, grid: GridSpec) -> torch.Tensor:
+    """nearest_upsample (baseline.cpp:87-98)."""
+    if targetLow.shape[1] != grid.lowW or targetLow.shape[0] != grid.lowH:
+        raise ValueError("nearest_upsample: low-res image does not match grid")
+    t = _image(targetLow, "nearest_upsample")
+    out = _baseline_out(grid, t)
+    ctx = context(t.device.index)
+    N.check(N.lib().glu_cu_nearest_upsample(ctx.handle, _ptr(t), C.byref(grid.c()), _ptr(out)))
+    return out
+
+
+def bilinear_upsample(targetLow: torch.Tensor, grid: GridSpec) -> torch.Tensor:
+    """bilinear_upsample (baseline.cpp:100-129)."""
+    if targetLow.shape[1] != grid.lowW or targetLow.shape[0] != grid.lowH:
+        raise ValueError("bilinear_upsample: low-res image does not match grid")
+    t = _image(targetLow, "bilinear_upsample")
+    out = _baseline_out(grid, t)
+    ctx = context(t.device.index)
+    N.check(N.lib().glu_cu_bilinear_upsample(ctx.handle, _ptr(t), C.byref(grid.c()), _ptr(out)))
+    return out
+
+
+def jbu_upsample(guideHigh: torch.Tensor, guideLow: torch.Tensor, targetLow: torch.Tensor,
+                 grid: GridSpec, params: JbuParams | None = None) -> torch.Tensor:
+    """jbu_upsample (baseline.cpp:30-85)."""
+    p = params or JbuParams()
+    gh, gl, t = (_image(x, "jbu_upsample") for x in (guideHigh, guideLow, targetLow))
+    if gh.shape[1] != grid.highW or gh.shape[0] != grid.highH:
+        raise ValueError("jbu_upsample: guide image does not match grid")
+    for x in (gl, t):
+        if x.shape[1] != grid.lowW or x.shape[0] != grid.lowH:
+            raise ValueError("jbu_upsample: low-res image does not match grid")
+    out = _baseline_out(grid, t)
+    ctx = context(t.device.index)
+    N.check(N.lib().glu_cu_jbu_upsample(ctx.handle, _ptr(gh), _ptr(gl), _ptr(t),
+                                        C.byref(grid.c()), int(p.window), float(p.sigmaD),
+                                        float(p.sigmaR), _ptr(out)))
+    return out
+
+
 def quality_report(reference: torch.Tensor, test: torch.Tensor) -> dict:
     """quality_report (metrics.cpp:109-115)."""
     m = mse(reference, test)
