@@ -217,6 +217,39 @@ int glu_cu_pair_eval(glu_ctx* ctx, const float* ip, const float* ia, const float
                      const double* w, size_t count, double eps, double* weightExact,
                      double* weightFast, double* objective);
 
+/* ---- distributed joint loop building blocks ---------- *
+ * Every rank keeps the full LR / params / errors state (replicas) and finds
+ * the same components (glu_cu_find_large_error).  glu_trial_levels groups
+ * the components of a sweep into levels of mutually independent trials
+ * (Chebyshev box distance > 2h to every earlier member of other levels it
+ * depends on); each rank runs its share of a level with a change log, the
+ * logs are exchanged (NCCL / gloo all-gather), and every rank applies the
+ * others' logs.  The result is bit-identical to the sequential loop. */
+typedef struct glu_trial_log {
+    uint32_t* counts; /* device: [0] cells, [1] pixels, [2] overflow flag */
+    uint32_t* cells;  /* device: 4 words per replaced cell {idx, r, g, b} (accepted trials) */
+    uint32_t* pixels; /* device: 5 words per affected pixel {idx, a, b, w, e} */
+    uint32_t cellCapacity, pixelCapacity;
+} glu_trial_log;
+
+/* Cell bounding boxes {x0, y0, x1, y1} of components (device, 4 int32 each). */
+int glu_cu_component_boxes(glu_ctx* ctx, const uint32_t* compOffsets,
+                           const uint32_t* compPixels, size_t count, const glu_grid* grid,
+                           int32_t* boxes);
+/* Host: level of each component (1-based) for Chebyshev reach `reach` (= 2h). */
+int glu_trial_levels(const int32_t* boxes, size_t count, int reach, int32_t* levels);
+/* Run the listed components (device ids, mutually independent or ordered by
+ * index) as trials; accepted trials are appended to `log` (may be NULL). */
+int glu_cu_run_trials(glu_ctx* ctx, const float* high, float* low, glu_pixel_params* field,
+                      float* errors, const glu_grid* grid, const glu_config* cfg, int mode,
+                      const uint32_t* compOffsets, const uint32_t* compPixels,
+                      const uint32_t* ids, size_t count, glu_trial_log* log, int* accepted,
+                      int* rejected);
+/* Apply another rank's change log. */
+int glu_cu_apply_trial_log(glu_ctx* ctx, float* low, glu_pixel_params* field, float* errors,
+                           const uint32_t* cells, size_t cellCount, const uint32_t* pixels,
+                           size_t pixelCount);
+
 /* ---- GLUP parameter files (io_glup.cpp:48-139; proj/README.md:97-117) --- */
 
 /* Bytes of the GLUP encoding of a field on `grid`. */

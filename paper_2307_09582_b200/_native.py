@@ -26,6 +26,11 @@ class GluConfigC(C.Structure):
                 ("literalComponentUpdate", C.c_int)]
 
 
+class GluTrialLog(C.Structure):
+    _fields_ = [("counts", C.c_void_p), ("cells", C.c_void_p), ("pixels", C.c_void_p),
+                ("cellCapacity", C.c_uint32), ("pixelCapacity", C.c_uint32)]
+
+
 class GluJointStats(C.Structure):
     _fields_ = [("iterations", C.c_int), ("trialsAccepted", C.c_int),
                 ("trialsRejected", C.c_int), ("components", C.c_int)]
@@ -81,6 +86,11 @@ SIGNATURES: dict[str, tuple] = {
     "glu_cu_upsample_frames": (I, [P, P, I, GP, CP, I, I, P, P]),
     "glu_h_upsample_frames": (I, [P, P, I, GP, CP, I, I, P, P]),
     "glu_cu_fp32_peak": (I, [P, C.POINTER(D), C.POINTER(D)]),
+    "glu_cu_component_boxes": (I, [P, P, P, SZ, GP, P]),
+    "glu_trial_levels": (I, [P, SZ, I, P]),
+    "glu_cu_run_trials": (I, [P, P, P, P, P, GP, CP, I, P, P, P, SZ, C.POINTER(GluTrialLog),
+                              C.POINTER(I), C.POINTER(I)]),
+    "glu_cu_apply_trial_log": (I, [P, P, P, P, P, SZ, P, SZ]),
     "glu_glup_size": (SZ, [GP]),
     "glu_cu_glup_encode": (I, [P, P, P, GP, I, I, P, SZ]),
     "glu_cu_glup_decode": (I, [P, P, SZ, GP, C.POINTER(I), C.POINTER(I), P, P]),

@@ -2,6 +2,7 @@
 // the reference's error texts, device-pointer and host-pointer entry points.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -582,6 +583,69 @@ int glu_cu_fp32_peak(glu_ctx* ctx, double* tflops, double* sm_mhz) {
     if (sm_mhz) *sm_mhz = flops / 2.0 / (best * 1e-3) / (128.0 * sms) / 1e6;
     (void)clk;
     return GLU_OK;
+}
+
+int glu_cu_component_boxes(glu_ctx* ctx, const uint32_t* off, const uint32_t* px, size_t n,
+                           const glu_grid* g, int32_t* boxes) {
+    if (!ctx) return einval("ctx must not be null");
+    GLU_TRY(check_grid(g));
+    return component_boxes(ctx, off, px, n, *g, boxes);
+}
+
+int glu_trial_levels(const int32_t* boxes, size_t n, int reach, int32_t* levels) {
+    if ((n && (!boxes || !levels)) || reach < 0) return einval("glu_trial_levels: bad arguments");
+    // Spatial bins of kBin x kBin cells; a component only has to be checked
+    // against earlier components registered in the bins its dilated box covers.
+    constexpr int kBin = 16;
+    int maxX = 0, maxY = 0;
+    for (size_t i = 0; i < n; ++i) {
+        maxX = std::max(maxX, boxes[4 * i + 2]);
+        maxY = std::max(maxY, boxes[4 * i + 3]);
+    }
+    const int bw = maxX / kBin + 1, bh = maxY / kBin + 1;
+    std::vector<std::vector<uint32_t>> bins(size_t(bw) * bh);
+    for (size_t i = 0; i < n; ++i) {
+        const int32_t* b = boxes + 4 * i;
+        const int x0 = std::max(0, b[0] - reach), y0 = std::max(0, b[1] - reach);
+        const int x1 = b[2] + reach, y1 = b[3] + reach;
+        int lvl = 1;
+        for (int by = y0 / kBin; by <= std::min(bh - 1, y1 / kBin); ++by)
+            for (int bx = x0 / kBin; bx <= std::min(bw - 1, x1 / kBin); ++bx)
+                for (uint32_t j : bins[size_t(by) * bw + bx]) {
+                    const int32_t* c = boxes + 4 * size_t(j);
+                    const int dx = std::max(0, std::max(c[0] - b[2], b[0] - c[2]));
+                    const int dy = std::max(0, std::max(c[1] - b[3], b[1] - c[3]));
+                    if (std::max(dx, dy) <= reach) lvl = std::max(lvl, levels[j] + 1);
+                }
+        levels[i] = lvl;
+        for (int by = b[1] / kBin; by <= b[3] / kBin; ++by)
+            for (int bx = b[0] / kBin; bx <= b[2] / kBin; ++bx)
+                bins[size_t(by) * bw + bx].push_back(uint32_t(i));
+    }
+    return GLU_OK;
+}
+
+int glu_cu_run_trials(glu_ctx* ctx, const float* high, float* low, glu_pixel_params* field,
+                      float* errors, const glu_grid* g, const glu_config* cfg, int mode,
+                      const uint32_t* off, const uint32_t* px, const uint32_t* ids, size_t n,
+                      glu_trial_log* log, int* accepted, int* rejected) {
+    if (!ctx) return einval("ctx must not be null");
+    GLU_TRY(glu_config_validate(cfg));
+    GLU_TRY(check_grid(g));
+    GLU_TRY(check_mode(mode));
+    int acc = 0, rej = 0;
+    GLU_TRY(run_trials(ctx, high, low, field, errors, *g, *cfg, mode, off, px, ids, n, log, &acc,
+                       &rej));
+    if (accepted) *accepted = acc;
+    if (rejected) *rejected = rej;
+    return GLU_OK;
+}
+
+int glu_cu_apply_trial_log(glu_ctx* ctx, float* low, glu_pixel_params* field, float* errors,
+                           const uint32_t* cells, size_t ncells, const uint32_t* pixels,
+                           size_t npixels) {
+    if (!ctx) return einval("ctx must not be null");
+    return apply_trial_log(ctx, low, field, errors, cells, ncells, pixels, npixels);
 }
 
 int glu_cu_op_color(glu_ctx* ctx, const float* in, size_t n, const double* M,

@@ -96,6 +96,15 @@ int ccl_find_large_error(glu_ctx* ctx, const float* errors, int W, int H, float 
 int trial_one(glu_ctx* ctx, const float* high, float* low, glu_pixel_params* field,
               float* errors, const glu_grid& g, const glu_config& cfg, int mode,
               const uint32_t* comp, size_t n, int* accepted);
+int component_boxes(glu_ctx* ctx, const uint32_t* off, const uint32_t* px, size_t n,
+                    const glu_grid& g, int32_t* boxes);
+int run_trials(glu_ctx* ctx, const float* high, float* low, glu_pixel_params* field,
+               float* errors, const glu_grid& g, const glu_config& cfg, int mode,
+               const uint32_t* off, const uint32_t* px, const uint32_t* ids, size_t n,
+               glu_trial_log* log, int* accepted, int* rejected);
+int apply_trial_log(glu_ctx* ctx, float* low, glu_pixel_params* field, float* errors,
+                    const uint32_t* cells, size_t ncells, const uint32_t* pixels,
+                    size_t npixels);
 int joint_sweep(glu_ctx* ctx, const float* high, float* low, glu_pixel_params* field,
                 float* errors, const glu_grid& g, const glu_config& cfg, int mode,
                 const uint32_t* off, const uint32_t* px, size_t ncomp, int* accepted,

@@ -141,6 +141,12 @@ struct TrialState {
     uint32_t* cellFlag;           // per LR cell, 0 between trials
     uint8_t* affMark;             // per LR cell, 0 between trials
     int* result;  // [0] accepted, [1] rejected, [2] sequential-sum fallbacks, [3] last verdict
+    // Optional change log of accepted trials (distributed joint loop): cells
+    // as {idx, r, g, b} words, pixels as {idx, a, b, w, e} words.
+    uint32_t* dCount;  // [0] cells, [1] pixels, [2] overflow flag
+    uint32_t* dCells;
+    uint32_t* dPixels;
+    uint32_t dCellCap, dPixelCap;
 };
 
 struct TrialBuffers {
@@ -172,6 +178,7 @@ struct TrialSmem {
     int box[4];
     double e0;
     int verdict;
+    uint32_t logCells, logPixels;  // change-log bases of this trial
 };
 
 // One trial (jointopt.cpp:114-180) executed by the whole CTA.  Returns the
@@ -334,6 +341,39 @@ __device__ int run_trial(const TrialState& t, const TrialBuffers& b, TrialSmem<N
     }
     __syncthreads();
     const int verdict = sm.verdict;
+    // change log of an accepted trial (distributed joint loop)
+    if (t.dCount && verdict) {
+        if (tid == 0) {
+            sm.logCells = atomicAdd(t.dCount, nt);
+            sm.logPixels = atomicAdd(t.dCount + 1, na);
+            if (sm.logCells + nt > t.dCellCap || sm.logPixels + na > t.dPixelCap) {
+                atomicExch(t.dCount + 2, 1u);
+                sm.logCells = sm.logPixels = 0xffffffffu;
+            }
+        }
+        __syncthreads();
+        if (sm.logCells != 0xffffffffu) {
+            for (uint32_t i = tid; i < nt; i += NT) {
+                const uint32_t cell = b.touched[i];
+                uint32_t* o = t.dCells + 4 * size_t(sm.logCells + i);
+                const float* lc = t.low + 3 * size_t(cell);
+                o[0] = cell;
+                o[1] = __float_as_uint(lc[0]);
+                o[2] = __float_as_uint(lc[1]);
+                o[3] = __float_as_uint(lc[2]);
+            }
+            for (uint32_t i = tid; i < na; i += NT) {
+                const uint32_t p = aff[i];
+                uint32_t* o = t.dPixels + 5 * size_t(sm.logPixels + i);
+                const glu_pixel_params pp = t.field[p];
+                o[0] = p;
+                o[1] = pp.a;
+                o[2] = pp.b;
+                o[3] = __float_as_uint(pp.w);
+                o[4] = __float_as_uint(t.errors[p]);
+            }
+        }
+    }
     // 6. rollback (jointopt.cpp:169-179) and reset per-cell state.
     if (!verdict) {
         for (uint32_t i = tid; i < na; i += NT) {
@@ -374,12 +414,15 @@ __global__ void __launch_bounds__(kSeqThreads) k_trial_sweep(TrialState t, Trial
 
 // Cell bounding box of every component; components whose worst-case
 // affected set exceeds a CTA's private buffers get the whole grid.
+// With raw != 0 the plain cell box is written (for level scheduling); `ids`
+// (optional) lists the components, box k belonging to component ids[k].
 __global__ void k_trial_boxes(const uint32_t* __restrict__ off, const uint32_t* __restrict__ px,
-                              int ncomp, int W, int s, int lw, int lh, int h, int literal,
-                              int4* __restrict__ boxes) {
+                              const uint32_t* __restrict__ ids, int ncomp, int W, int s, int lw,
+                              int lh, int h, int literal, int raw, int4* __restrict__ boxes) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= ncomp) return;
-    const uint32_t b0 = off[warp], b1 = off[warp + 1];
+    const uint32_t comp = ids ? ids[warp] : uint32_t(warp);
+    const uint32_t b0 = off[comp], b1 = off[comp + 1];
     int x0 = lw, y0 = lh, x1 = -1, y1 = -1;
     for (uint32_t i = b0 + lane; i < b1; i += 32) {
         const uint32_t p = px[i];
@@ -400,7 +443,7 @@ __global__ void k_trial_boxes(const uint32_t* __restrict__ off, const uint32_t* 
         const uint64_t dil = uint64_t(min(lw - 1, x1 + h) - max(0, x0 - h) + 1) *
                              uint64_t(min(lh - 1, y1 + h) - max(0, y0 - h) + 1);
         const uint64_t affPx = literal ? uint64_t(b1 - b0) : dil * uint64_t(s) * uint64_t(s);
-        const bool big = cells > kCtaCells || affPx > kCtaPixels;
+        const bool big = !raw && (cells > kCtaCells || affPx > kCtaPixels);
         boxes[warp] = big ? make_int4(-(1 << 28), -(1 << 28), 1 << 28, 1 << 28)
                           : make_int4(x0, y0, x1, y1);
     }
@@ -425,7 +468,7 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 // Persistent conflict-aware trial scheduler (see the file comment).
 __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
     TrialState t, TrialBuffers big, char* ctaBufs, const uint32_t* off, const uint32_t* px,
-    int ncomp, const int4* boxes, int* done, int* next, int reach) {
+    const uint32_t* ids, int ncomp, const int4* boxes, int* done, int* next, int reach) {
     __shared__ TrialSmem<kSchedThreads> sm;
     __shared__ int sIdx;
     // this CTA's private buffers
@@ -451,8 +494,9 @@ __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
         __syncthreads();
         __threadfence();
         const bool isBig = bi.x < 0;
-        const int v = run_trial<kSchedThreads>(t, isBig ? big : local, sm, px + off[i],
-                                               off[i + 1] - off[i]);
+        const uint32_t c = ids ? ids[i] : uint32_t(i);
+        const int v = run_trial<kSchedThreads>(t, isBig ? big : local, sm, px + off[c],
+                                               off[c + 1] - off[c]);
         if (threadIdx.x == 0) {
             atomicAdd(t.result + (v ? 0 : 1), 1);
             __threadfence();
@@ -518,6 +562,9 @@ TrialState trial_state(const float* high, float* low, glu_pixel_params* field, f
     t.cellFlag = js.cellFlag;
     t.affMark = js.affMark;
     t.result = js.result;
+    t.dCount = nullptr;
+    t.dCells = t.dPixels = nullptr;
+    t.dCellCap = t.dPixelCap = 0;
     return t;
 }
 
@@ -530,6 +577,37 @@ int sched_grid(glu_ctx* ctx) {
     cached = sms * std::max(1, std::min(per, 2));
     cachedDev = ctx->device;
     return cached;
+}
+
+// Parallel conflict-aware schedule of the listed components (all when
+// ids == NULL), k_trial_sched.  Asynchronous on ctx->stream.
+int run_sched(glu_ctx* ctx, const TrialState& t, const JointScratch& js, const glu_grid& g,
+              const glu_config& cfg, const uint32_t* off, const uint32_t* px,
+              const uint32_t* ids, size_t n) {
+    const int grid = sched_grid(ctx);
+    const size_t per = size_t(kCtaCells) * 16 + size_t(kCtaPixels) * 20;
+    char* ctaBufs = static_cast<char*>(scratch(ctx, S_SCHED, per * grid));
+    // boxes (int4 per trial) | done flags | next counter
+    char* meta = static_cast<char*>(scratch(ctx, S_SCHED_META, n * 20 + 64));
+    if (!ctaBufs || !meta) return GLU_ENOMEM;
+    int4* boxes = reinterpret_cast<int4*>(meta);
+    int* done = reinterpret_cast<int*>(meta + n * 16);
+    int* next = done + n;
+    cudaError_t e = cudaMemsetAsync(done, 0, (n + 1) * sizeof(int), ctx->stream);
+    if (e != cudaSuccess) return fail_cuda(e, "trial schedule");
+    k_trial_boxes<<<blocks_for(n * 32, 256), 256, 0, ctx->stream>>>(
+        off, px, ids, int(n), g.highW, g.scale, g.lowW, g.lowH, cfg.windowSide / 2,
+        cfg.literalComponentUpdate, 0, boxes);
+    ++ctx->launches;
+    TrialState ts = t;
+    TrialBuffers big = js.big;
+    int nc = int(n), reach = 2 * (cfg.windowSide / 2);
+    void* args[] = {&ts, &big, &ctaBufs, &off, &px, &ids, &nc, &boxes, &done, &next, &reach};
+    e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_trial_sched), grid, kSchedThreads,
+                                    args, 0, ctx->stream);
+    ++ctx->launches;
+    if (e != cudaSuccess) return fail_cuda(e, "trial schedule");
+    return GLU_OK;
 }
 
 }  // namespace
@@ -628,28 +706,9 @@ int joint_sweep(glu_ctx* ctx, const float* high, float* low, glu_pixel_params* f
         ++ctx->launches;
         e = cudaGetLastError();
     } else {
-        const int grid = sched_grid(ctx);
-        const size_t per = size_t(kCtaCells) * 16 + size_t(kCtaPixels) * 20;
-        char* ctaBufs = static_cast<char*>(scratch(ctx, S_SCHED, per * grid));
-        // boxes (int4 per component) | done flags | next counter
-        char* meta = static_cast<char*>(scratch(ctx, S_SCHED_META, ncomp * 20 + 64));
-        if (!ctaBufs || !meta) return GLU_ENOMEM;
-        int4* boxes = reinterpret_cast<int4*>(meta);
-        int* done = reinterpret_cast<int*>(meta + ncomp * 16);
-        int* next = done + ncomp;
-        e = cudaMemsetAsync(done, 0, (ncomp + 1) * sizeof(int), ctx->stream);
-        if (e != cudaSuccess) return fail_cuda(e, "trial sweep");
-        k_trial_boxes<<<blocks_for(ncomp * 32, 256), 256, 0, ctx->stream>>>(
-            off, px, int(ncomp), g.highW, g.scale, g.lowW, g.lowH, cfg.windowSide / 2,
-            cfg.literalComponentUpdate, boxes);
-        ++ctx->launches;
-        TrialState ts = t;
-        TrialBuffers big = js.big;
-        int nc = int(ncomp), reach = 2 * (cfg.windowSide / 2);
-        void* args[] = {&ts, &big, &ctaBufs, &off, &px, &nc, &boxes, &done, &next, &reach};
-        e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_trial_sched), grid,
-                                        kSchedThreads, args, 0, ctx->stream);
-        ++ctx->launches;
+        rc = run_sched(ctx, t, js, g, cfg, off, px, nullptr, ncomp);
+        if (rc) return rc;
+        e = cudaSuccess;
     }
     int res[4];
     if (e == cudaSuccess)
@@ -675,6 +734,107 @@ int trial_one(glu_ctx* ctx, const float* high, float* low, glu_pixel_params* fie
     if (rc) return rc;
     *accepted = acc;
     return GLU_OK;
+}
+
+// ---- building blocks of the distributed joint loop --------------------------------
+//
+// Every rank holds the full (replicated) LR / params / errors state and finds the
+// same components.  The components of a sweep are grouped into levels (level =
+// 1 + the highest level of an earlier conflicting component); components of one
+// level are mutually independent, so each rank runs its share of a level
+// (run_trials with a change log), the ranks exchange the logs of accepted trials
+// and apply each other's changes (apply_trial_log).  Any order of independent
+// trials gives the sequential result, so every rank ends each level with the
+// state the reference's sequential loop has after the same trials.
+
+namespace {
+
+__global__ void k_apply_log(float* __restrict__ low, glu_pixel_params* __restrict__ field,
+                            float* __restrict__ errors, const uint32_t* __restrict__ cells,
+                            size_t ncells, const uint32_t* __restrict__ pixels, size_t npixels) {
+    const size_t stride = size_t(gridDim.x) * blockDim.x;
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < ncells; i += stride) {
+        const uint32_t* c = cells + 4 * i;
+        float* lc = low + 3 * size_t(c[0]);
+        lc[0] = __uint_as_float(c[1]);
+        lc[1] = __uint_as_float(c[2]);
+        lc[2] = __uint_as_float(c[3]);
+    }
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < npixels; i += stride) {
+        const uint32_t* q = pixels + 5 * i;
+        glu_pixel_params pp;
+        pp.a = q[1];
+        pp.b = q[2];
+        pp.w = __uint_as_float(q[3]);
+        field[q[0]] = pp;
+        errors[q[0]] = __uint_as_float(q[4]);
+    }
+}
+
+}  // namespace
+
+int component_boxes(glu_ctx* ctx, const uint32_t* off, const uint32_t* px, size_t n,
+                    const glu_grid& g, int32_t* boxes) {
+    if (n == 0) return GLU_OK;
+    k_trial_boxes<<<blocks_for(n * 32, 256), 256, 0, ctx->stream>>>(
+        off, px, nullptr, int(n), g.highW, g.scale, g.lowW, g.lowH, 0, 0, 1,
+        reinterpret_cast<int4*>(boxes));
+    ++ctx->launches;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? GLU_OK : fail_cuda(e, "component boxes");
+}
+
+int run_trials(glu_ctx* ctx, const float* high, float* low, glu_pixel_params* field,
+               float* errors, const glu_grid& g, const glu_config& cfg, int mode,
+               const uint32_t* off, const uint32_t* px, const uint32_t* ids, size_t n,
+               glu_trial_log* log, int* accepted, int* rejected) {
+    JointScratch js;
+    int rc = joint_scratch(ctx, g, &js, true);
+    if (rc) return rc;
+    TrialState t = trial_state(high, low, field, errors, g, cfg, mode, js);
+    if (log) {
+        t.dCount = log->counts;
+        t.dCells = log->cells;
+        t.dPixels = log->pixels;
+        t.dCellCap = log->cellCapacity;
+        t.dPixelCap = log->pixelCapacity;
+        cudaError_t e = cudaMemsetAsync(log->counts, 0, 3 * sizeof(uint32_t), ctx->stream);
+        if (e != cudaSuccess) return fail_cuda(e, "run_trials");
+    }
+    if (n) {
+        rc = run_sched(ctx, t, js, g, cfg, off, px, ids, n);
+        if (rc) return rc;
+    }
+    int res[4];
+    cudaError_t e =
+        cudaMemcpyAsync(res, js.result, sizeof(res), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return fail_cuda(e, "run_trials");
+    if (log) {
+        uint32_t over = 0;
+        e = cudaMemcpy(&over, log->counts + 2, sizeof(over), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return fail_cuda(e, "run_trials");
+        if (over) {
+            set_error("run_trials: change log capacity exceeded");
+            return GLU_ENOMEM;
+        }
+    }
+    *accepted = res[0];
+    *rejected = res[1];
+    return GLU_OK;
+}
+
+int apply_trial_log(glu_ctx* ctx, float* low, glu_pixel_params* field, float* errors,
+                    const uint32_t* cells, size_t ncells, const uint32_t* pixels,
+                    size_t npixels) {
+    if (ncells == 0 && npixels == 0) return GLU_OK;
+    const size_t work = ncells > npixels ? ncells : npixels;
+    const unsigned blocks = unsigned(std::min<size_t>((work + 255) / 256, 148 * 16));
+    k_apply_log<<<blocks, 256, 0, ctx->stream>>>(low, field, errors, cells, ncells, pixels,
+                                                 npixels);
+    ++ctx->launches;
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? GLU_OK : fail_cuda(e, "apply_trial_log");
 }
 
 }  // namespace glu_cu

@@ -82,3 +82,37 @@ def test_row_bands_partition_c4(world):
     if world == 8:
         assert sizes == [34] * 6 + [33] * 2
         assert sharding.halo_bytes(bands[3], 480) == 2 * 480 * 12  # 5,760 B per side
+
+
+def _log_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2307_09582_b200.distributed import TorchComm
+        comm = TorchComm()
+        cells = torch.arange(4 * (rank + 1), dtype=torch.int32).reshape(-1, 4) + 100 * rank
+        pixels = torch.arange(5 * (2 - rank), dtype=torch.int32).reshape(-1, 5) + 1000 * rank
+        logs = comm.all_gather_logs(cells, pixels)
+        sums = comm.all_reduce_sum([rank + 1, 10 * rank])
+        q.put((rank, [(c.tolist(), p.tolist()) for c, p in logs], sums))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_change_log_exchange():
+    """The distributed joint loop's all-gather of variable-size change logs."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_log_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = dict((r, (logs, sums)) for r, logs, sums in (q.get(timeout=10) for _ in range(2)))
+    want = [([[0, 1, 2, 3]], [[0, 1, 2, 3, 4], [5, 6, 7, 8, 9]]),
+            ([[100, 101, 102, 103], [104, 105, 106, 107]], [[1000, 1001, 1002, 1003, 1004]])]
+    for r in (0, 1):
+        assert res[r][0] == want
+        assert res[r][1] == [3, 10]
