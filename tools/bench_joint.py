@@ -26,6 +26,38 @@ p.add_argument("--reps", type=int, default=3)
 p.add_argument("--cpu", action="store_true")
 a = p.parse_args()
 
+# Under torchrun (WORLD_SIZE > 1) the level-synchronous multi-rank loop runs
+# over NCCL, one rank per GPU, and rank 0 reports the max-over-ranks time.
+WORLD = int(os.environ.get("WORLD_SIZE", "1"))
+if WORLD > 1:
+    import torch.distributed as dist
+    from paper_2307_09582_b200 import distributed as D
+    LOCAL = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(LOCAL)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", LOCAL))
+    for c in a.config:
+        cfg = workloads.CONFIGS[c]
+        img = torch.from_numpy(workloads.scene(cfg["W"], cfg["H"], c, 0)).cuda()
+        D.joint_optimize_distributed(img, cfg["scale"])
+        times = []
+        for _ in range(a.reps):
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            r = D.joint_optimize_distributed(img, cfg["scale"])
+            e1.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            times.append(float(t.item()))
+        if dist.get_rank() == 0:
+            print(json.dumps({"config": cfg["name"], "ranks": WORLD, "gpu_ms": min(times),
+                              "accepted": r.trialsAccepted, "rejected": r.trialsRejected}),
+                  flush=True)
+    dist.destroy_process_group()
+    sys.exit(0)
+
 for c in a.config:
     cfg = workloads.CONFIGS[c]
     W, H, s = cfg["W"], cfg["H"], cfg["scale"]
