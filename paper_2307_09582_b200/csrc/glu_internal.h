@@ -69,7 +69,7 @@ bool solve32_supported(int mode, int S, int s);
 cudaError_t launch_solve32(glu_ctx* ctx, const SolveArgs& a, int forceFallback);
 bool solve32x_supported(int mode, int S, int s);
 cudaError_t launch_solve32x(glu_ctx* ctx, const SolveArgs& a, const float4* packed,
-                            int forceFallback);
+                            int forceFallback, const unsigned* nanFlag);
 cudaError_t launch_solve_list(glu_ctx* ctx, const SolveArgs& a, const uint32_t* pixels,
                               size_t count);
 cudaError_t launch_apply(glu_ctx* ctx, const glu_pixel_params* field, size_t npx,

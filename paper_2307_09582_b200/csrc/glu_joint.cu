@@ -30,6 +30,7 @@
 #include <cub/cub.cuh>
 
 #include "glu_internal.h"
+#include "glu_filter32.cuh"
 #include "glu_math.cuh"
 
 namespace glu_cu {
@@ -39,8 +40,11 @@ namespace {
 constexpr uint32_t kNone = 0xffffffffu;
 constexpr int kSchedThreads = 256;   // CTA size of the parallel trial scheduler
 constexpr int kSeqThreads = 1024;    // CTA size of the sequential (single-CTA) sweep
-constexpr uint32_t kCtaPixels = 16384;  // per-CTA affected-pixel capacity
-constexpr uint32_t kCtaCells = 4096;    // per-CTA replaced-cell capacity
+// Per-CTA private trial buffers (x 2 CTAs per SM): a diagonal 200-pixel line
+// at s = 8 has a 27 x 27-cell dilated box (46,656 pixels), so 64 Ki pixels
+// keeps the serialising whole-grid fallback for genuinely huge components.
+constexpr uint32_t kCtaPixels = 65536;  // per-CTA affected-pixel capacity
+constexpr uint32_t kCtaCells = 8192;    // per-CTA replaced-cell capacity
 
 // ---- connected components ---------------------------------------------------
 
@@ -302,13 +306,38 @@ __device__ int run_trial(const TrialState& t, const TrialBuffers& b, TrialSmem<N
         const int cx = x / t.s, cy = y / t.s;
         const int x0 = max(0, cx - h), y0 = max(0, cy - h);
         const int nwx = min(t.lw - 1, cx + h) - x0 + 1, nwy = min(t.lh - 1, cy + h) - y0 + 1;
-        const Pick pk = pick64(t.mode, ip, GlobalLowWindow{t.low, t.lw, x0, y0, nwx}, nwx * nwy,
-                               t.eps);
-        const int ar = pk.ai / nwx, br = pk.bi / nwx;
         glu_pixel_params np;
-        np.a = uint32_t(y0 + ar) * uint32_t(t.lw) + uint32_t(x0 + pk.ai - ar * nwx);
-        np.b = uint32_t(y0 + br) * uint32_t(t.lw) + uint32_t(x0 + pk.bi - br * nwx);
-        np.w = float(pk.w);
+        bool done = false;
+        if (t.S == 3 && t.mode != GLU_MODE_EXACT) {
+            // fp32 filter + fp64 verify (glu_filter32.cuh) on the live LR image
+            float4 c[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                const int gx = cx - 1 + k % 3, gy = cy - 1 + k / 3;
+                c[k] = make_float4(__int_as_float(0x7f800000), __int_as_float(0x7f800000),
+                                   __int_as_float(0x7f800000), 0.0f);
+                if (gx >= 0 && gy >= 0 && gx < t.lw && gy < t.lh) {
+                    const float* s = t.low + 3 * (size_t(gy) * t.lw + gx);
+                    c[k] = make_float4(s[0], s[1], s[2], 0.0f);
+                }
+            }
+            const Filter32Result fr =
+                filter32_pixel(c, ip, float(t.eps), t.eps, t.mode == GLU_MODE_GNU);
+            if (fr.ok) {
+                np.a = uint32_t(cy - 1 + fr.ja / 3) * uint32_t(t.lw) + uint32_t(cx - 1 + fr.ja % 3);
+                np.b = uint32_t(cy - 1 + fr.jb / 3) * uint32_t(t.lw) + uint32_t(cx - 1 + fr.jb % 3);
+                np.w = fr.w;
+                done = true;
+            }
+        }
+        if (!done) {
+            const Pick pk = pick64(t.mode, ip, GlobalLowWindow{t.low, t.lw, x0, y0, nwx},
+                                   nwx * nwy, t.eps);
+            const int ar = pk.ai / nwx, br = pk.bi / nwx;
+            np.a = uint32_t(y0 + ar) * uint32_t(t.lw) + uint32_t(x0 + pk.ai - ar * nwx);
+            np.b = uint32_t(y0 + br) * uint32_t(t.lw) + uint32_t(x0 + pk.bi - br * nwx);
+            np.w = float(pk.w);
+        }
         t.field[p] = np;
         float r[3];
         for (int k = 0; k < 3; ++k)

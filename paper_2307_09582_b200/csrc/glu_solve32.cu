@@ -96,8 +96,11 @@ struct PackedWindow {
     }
 };
 
+// Also raises *nanFlag when the LR image holds a NaN: the reference's scans
+// treat NaN candidates by index order (every comparison is false), which the
+// filter does not model, so such a solve runs entirely on the exact path.
 __global__ void k_pack_low(const float* __restrict__ low, int lw, int lh, int h,
-                           float4* __restrict__ packed) {
+                           float4* __restrict__ packed, unsigned* nanFlag) {
     const int pw = lw + 2 * h, ph = lh + 2 * h;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= pw * ph) return;
@@ -106,13 +109,15 @@ __global__ void k_pack_low(const float* __restrict__ low, int lw, int lh, int h,
     if (x >= 0 && y >= 0 && x < lw && y < lh) {
         const float* s = low + 3 * (size_t(y) * lw + x);
         v = make_float4(s[0], s[1], s[2], 0.0f);
+        if (v.x != v.x || v.y != v.y || v.z != v.z) atomicOr(nanFlag, 1u);
     }
     packed[i] = v;
 }
 
 template <int S, int MODE>
-__global__ void __launch_bounds__(kThreads, GLU_SOLVE_MIN_BLOCKS) k_solve32(SolveArgs a, const float4* packed,
-                                                          int forceFallback) {
+__global__ void __launch_bounds__(kThreads, GLU_SOLVE_MIN_BLOCKS)
+    k_solve32(SolveArgs a, const float4* packed, int forceFallback, const unsigned* nanFlag) {
+    forceFallback |= int(__ldg(nanFlag));
     constexpr int N = S * S;
     constexpr int h = S / 2;
     constexpr int NE = S == 3 ? N : 1;  // S = 3 keeps e_j in registers; S = 5 reloads
@@ -261,9 +266,10 @@ __global__ void __launch_bounds__(kThreads, GLU_SOLVE_MIN_BLOCKS) k_solve32(Solv
 }
 
 template <int S, int MODE>
-cudaError_t launch_t(glu_ctx* ctx, const SolveArgs& a, const float4* packed, int force) {
+cudaError_t launch_t(glu_ctx* ctx, const SolveArgs& a, const float4* packed, int force,
+                     const unsigned* nanFlag) {
     dim3 grid((a.W + 31) / 32, (a.H + kThreads / 32 - 1) / (kThreads / 32));
-    k_solve32<S, MODE><<<grid, kThreads, 0, ctx->stream>>>(a, packed, force);
+    k_solve32<S, MODE><<<grid, kThreads, 0, ctx->stream>>>(a, packed, force, nanFlag);
     ++ctx->launches;
     return cudaGetLastError();
 }
@@ -286,15 +292,18 @@ cudaError_t launch_solve32(glu_ctx* ctx, const SolveArgs& a0, int forceFallback)
     const size_t cells = size_t(a.lw + 2 * h) * (a.lh + 2 * h);
     float4* packed = static_cast<float4*>(scratch(ctx, S_PACKED, cells * sizeof(float4)));
     if (!packed) return cudaErrorMemoryAllocation;
+    unsigned* nanFlag = reinterpret_cast<unsigned*>(ctx->d_counters + 3);
+    cudaError_t e = cudaMemsetAsync(nanFlag, 0, sizeof(unsigned), ctx->stream);
+    if (e != cudaSuccess) return e;
     k_pack_low<<<unsigned((cells + 255) / 256), 256, 0, ctx->stream>>>(a.low, a.lw, a.lh, h,
-                                                                        packed);
+                                                                        packed, nanFlag);
     ++ctx->launches;
-    if (a.mode == GLU_MODE_EXACT) return launch_solve32x(ctx, a, packed, forceFallback);
+    if (a.mode == GLU_MODE_EXACT) return launch_solve32x(ctx, a, packed, forceFallback, nanFlag);
     if (a.mode == GLU_MODE_GNU)
-        return a.S == 3 ? launch_t<3, GLU_MODE_GNU>(ctx, a, packed, forceFallback)
-                        : launch_t<5, GLU_MODE_GNU>(ctx, a, packed, forceFallback);
-    return a.S == 3 ? launch_t<3, GLU_MODE_FAST>(ctx, a, packed, forceFallback)
-                    : launch_t<5, GLU_MODE_FAST>(ctx, a, packed, forceFallback);
+        return a.S == 3 ? launch_t<3, GLU_MODE_GNU>(ctx, a, packed, forceFallback, nanFlag)
+                        : launch_t<5, GLU_MODE_GNU>(ctx, a, packed, forceFallback, nanFlag);
+    return a.S == 3 ? launch_t<3, GLU_MODE_FAST>(ctx, a, packed, forceFallback, nanFlag)
+                    : launch_t<5, GLU_MODE_FAST>(ctx, a, packed, forceFallback, nanFlag);
 }
 
 }  // namespace glu_cu

@@ -69,7 +69,9 @@ __device__ __forceinline__ void pair_ij(int k, int& i, int& j) {
 }
 
 __global__ void __launch_bounds__(kThreads, 2) k_solve32x(SolveArgs a, const float4* packed,
-                                                          int forceFallback) {
+                                                          int forceFallback,
+                                                          const unsigned* nanFlag) {
+    forceFallback |= int(__ldg(nanFlag));
     __shared__ float4 table[kMaxCells * kCellStride];
     const int pw = a.lw + 2;  // h = 1
     const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
@@ -222,9 +224,9 @@ bool solve32x_supported(int mode, int S, int s) {
 }
 
 cudaError_t launch_solve32x(glu_ctx* ctx, const SolveArgs& a, const float4* packed,
-                            int forceFallback) {
+                            int forceFallback, const unsigned* nanFlag) {
     dim3 grid((a.W + kTX - 1) / kTX, (a.H + kTY - 1) / kTY);
-    k_solve32x<<<grid, kThreads, 0, ctx->stream>>>(a, packed, forceFallback);
+    k_solve32x<<<grid, kThreads, 0, ctx->stream>>>(a, packed, forceFallback, nanFlag);
     ++ctx->launches;
     return cudaGetLastError();
 }
