@@ -299,6 +299,7 @@ __device__ int run_trial(const TrialState& t, const TrialBuffers& b, TrialSmem<N
     __syncthreads();
     // 5. re-solve (optimize_pixels, 159) and re-score (160-165).
     part = 0;
+    bool changed = false;
     for (uint32_t i = tid; i < na; i += NT) {
         const uint32_t p = aff[i];
         const int x = int(p % W), y = int(p / W);
@@ -345,30 +346,50 @@ __device__ int run_trial(const TrialState& t, const TrialBuffers& b, TrialSmem<N
                               true);
         const float e = pixel_error(ip, r);
         t.errors[p] = e;
+        changed |= __float_as_uint(e) != __float_as_uint(b.bkE[i]);
         part += double(e);
     }
     const double e1 = BlockReduce(sm.tmp.reduce).Sum(part);
+    // Identical per-pixel errors give identical sequential sums: accept.
+    const bool anyChanged = __syncthreads_or(changed);
     if (tid == 0) {
         const double s0 = sm.e0;
         // |parallel - sequential| <= 2 * gamma_na * sum for non-negative terms.
         const double bound = 4.0 * (double(na) + 64.0) * 0x1.0p-53 * (s0 + e1);
-        int verdict;
-        if (e1 + bound < s0)
-            verdict = 1;
+        if (!anyChanged || e1 + bound < s0)
+            sm.verdict = 1;
         else if (e1 > s0 + bound)
-            verdict = 0;
-        else {  // exact reference order (jointopt.cpp:150-165)
-            double q0 = 0, q1 = 0;
-            for (uint32_t i = 0; i < na; ++i) {
-                q0 += double(b.bkE[i]);
-                q1 += double(t.errors[aff[i]]);
-            }
-            verdict = q1 <= q0;
-            atomicAdd(t.result + 2, 1);
-        }
-        sm.verdict = verdict;
+            sm.verdict = 0;
+        else
+            sm.verdict = -1;  // too close: redo both sums in the reference order
     }
     __syncthreads();
+    if (sm.verdict < 0) {
+        // exact reference order (jointopt.cpp:150-165); the block stages each
+        // chunk of old / new errors in shared memory for thread 0's chain
+        double q0 = 0, q1 = 0;
+        float* stage = reinterpret_cast<float*>(&sm.tmp);
+        constexpr uint32_t kChunk = sizeof(sm.tmp) / (2 * sizeof(float));
+        for (uint32_t c0 = 0; c0 < na; c0 += kChunk) {
+            const uint32_t m = min(kChunk, na - c0);
+            for (uint32_t k = tid; k < m; k += NT) {
+                stage[2 * k] = b.bkE[c0 + k];
+                stage[2 * k + 1] = t.errors[aff[c0 + k]];
+            }
+            __syncthreads();
+            if (tid == 0)
+                for (uint32_t k = 0; k < m; ++k) {
+                    q0 += double(stage[2 * k]);
+                    q1 += double(stage[2 * k + 1]);
+                }
+            __syncthreads();
+        }
+        if (tid == 0) {
+            sm.verdict = q1 <= q0;
+            atomicAdd(t.result + 2, 1);
+        }
+        __syncthreads();
+    }
     const int verdict = sm.verdict;
     // change log of an accepted trial (distributed joint loop)
     if (t.dCount && verdict) {
@@ -484,9 +505,12 @@ __device__ __forceinline__ bool boxes_conflict(int4 a, int4 b, int reach) {
     return max(dx, dy) <= reach;
 }
 
-__device__ __forceinline__ int ld_acquire(const int* p) {
+// Polling uses relaxed loads (served by L2, no L1 invalidation: an acquire load
+// would flush the SM's L1 on every poll and starve the co-resident CTA doing
+// real work); the waiting CTA issues one acquire fence after the flags are set.
+__device__ __forceinline__ int ld_relaxed(const int* p) {
     int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 
@@ -519,9 +543,9 @@ __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
         // wait for every earlier trial this one conflicts with
         for (int j = threadIdx.x; j < i; j += kSchedThreads)
             if (boxes_conflict(boxes[j], bi, reach))
-                while (ld_acquire(done + j) == 0) __nanosleep(64);
+                while (ld_relaxed(done + j) == 0) __nanosleep(200);
         __syncthreads();
-        __threadfence();
+        __threadfence();  // acquire: the published trials' writes are visible
         const bool isBig = bi.x < 0;
         const uint32_t c = ids ? ids[i] : uint32_t(i);
         const int v = run_trial<kSchedThreads>(t, isBig ? big : local, sm, px + off[c],
