@@ -14,11 +14,13 @@
 // dilate(Q_i, 2h) and errors in footprints of dilate(Q_i, h).  Two trials whose
 // cell bounding boxes are more than 2h apart (Chebyshev) therefore touch
 // disjoint state and commute.  k_trial_sched is a persistent, cooperatively
-// launched kernel: CTAs claim trials in sweep order from an atomic counter,
-// wait (acquire) until every earlier trial whose box is within 2h has
-// published its result (release), and run the trial with the whole CTA.
-// Claims are in order and every CTA is resident, so the smallest unfinished
-// trial never waits: no deadlock, and the final state is bit-identical to the
+// launched dataflow scheduler over that conflict graph: each trial counts its
+// earlier conflicting trials, CTAs pop trials whose count reached zero from a
+// FIFO, run them with the whole CTA and release their successors.  Claiming
+// in index order and blocking (round 1's first version) left every CTA parked
+// on a dependency chain while independent trials queued behind them; the
+// dataflow form runs at max(critical path, work / CTAs).  Conflicting trials
+// still run in index order, so the final state is bit-identical to the
 // sequential loop.  Trials too large for a CTA's private buffers get a
 // whole-grid box (they conflict with everything, so they run alone) and use
 // the global worst-case buffers.
@@ -29,6 +31,10 @@
 // otherwise one thread redoes both sums in the exact reference order.
 #include <cub/cub.cuh>
 
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 #include "glu_internal.h"
 #include "glu_filter32.cuh"
 #include "glu_math.cuh"
@@ -38,7 +44,10 @@ namespace glu_cu {
 namespace {
 
 constexpr uint32_t kNone = 0xffffffffu;
-constexpr int kSchedThreads = 256;   // CTA size of the parallel trial scheduler
+#ifndef GLU_SCHED_THREADS
+#define GLU_SCHED_THREADS 256
+#endif
+constexpr int kSchedThreads = GLU_SCHED_THREADS;  // CTA size of the parallel trial scheduler
 constexpr int kSeqThreads = 1024;    // CTA size of the sequential (single-CTA) sweep
 // Per-CTA private trial buffers (x 2 CTAs per SM): a diagonal 200-pixel line
 // at s = 8 has a 27 x 27-cell dilated box (46,656 pixels), so 64 Ki pixels
@@ -514,14 +523,89 @@ __device__ __forceinline__ int ld_relaxed(const int* p) {
     return v;
 }
 
+#ifdef GLU_SCHED_TRACE
+// Development builds only (-DGLU_SCHED_TRACE): per trial {claim, ready, end}
+// %globaltimer stamps, dumped by run_sched to $GLU_SCHED_TRACE_FILE.
+__device__ unsigned long long* g_trace;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    return v;
+}
+#endif
+
 __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Persistent conflict-aware trial scheduler (see the file comment).
+struct MinOp {
+    __device__ __forceinline__ int operator()(int a, int b) const { return min(a, b); }
+};
+
+// sufTop[j] = smallest box top row over trials j..n-1 (a whole-grid box counts
+// as -2^28).  No trial at or after j conflicts with a box whose bottom row +
+// reach lies above sufTop[j], so successor scans stop there.  Components are
+// in raster order of their first pixel, so box tops are non-decreasing and
+// scans cover only the trials starting within the box's rows (+ reach).
+__global__ void __launch_bounds__(1024) k_suffix_top(const int4* __restrict__ boxes, int n,
+                                                     int* __restrict__ sufTop) {
+    using Scan = cub::BlockScan<int, 1024>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ int carry;
+    if (threadIdx.x == 0) carry = 0x7fffffff;
+    __syncthreads();
+    for (int end = n; end > 0; end -= 1024) {
+        const int j = end - 1 - int(threadIdx.x);  // reversed: thread t holds end-1-t
+        const int v = j >= 0 ? boxes[j].y : 0x7fffffff;
+        int r;
+        Scan(tmp).InclusiveScan(v, r, MinOp{});
+        r = min(r, carry);
+        if (j >= 0) sufTop[j] = r;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry = r;
+        __syncthreads();
+    }
+}
+
+// pred[j] = number of earlier trials j conflicts with (one warp per trial i
+// walks its successors j > i).
+__global__ void k_trial_preds(const int4* __restrict__ boxes, const int* __restrict__ sufTop,
+                              int n, int reach, int* __restrict__ pred) {
+    const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (i >= n) return;
+    const int4 bi = boxes[i];
+    const int lim = bi.w + reach;
+    for (int base = i + 1; base < n; base += 32) {
+        if (sufTop[base] > lim) break;
+        const int j = base + lane;
+        if (j < n && boxes_conflict(bi, boxes[j], reach)) atomicAdd(pred + j, 1);
+    }
+}
+
+// Trials with no earlier conflict start ready, in index order within a warp.
+__global__ void k_trial_seed(const int* __restrict__ pred, int n, int* __restrict__ queue,
+                             int* __restrict__ qTail) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x, lane = threadIdx.x & 31;
+    const bool ready = j < n && pred[j] == 0;
+    const unsigned m = __ballot_sync(0xffffffffu, ready);
+    if (!m) return;
+    int base = 0;
+    if (lane == __ffs(m) - 1) base = atomicAdd(qTail, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+    if (ready) queue[base + __popc(m & ((1u << lane) - 1))] = j;
+}
+
+// Persistent conflict-aware trial scheduler (see the file comment): a
+// dependency-counting dataflow schedule.  CTAs pop ready trials from a FIFO
+// (slot k of `queue` is filled by the k-th trial to become ready); a finished
+// trial decrements the counters of its conflicting successors and pushes the
+// ones that reach zero.  Every CTA is resident, so whenever trials remain one
+// of them is ready or running: no deadlock, and conflicting trials still run
+// in index order, so the state is bit-identical to the sequential loop.
 __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
     TrialState t, TrialBuffers big, char* ctaBufs, const uint32_t* off, const uint32_t* px,
-    const uint32_t* ids, int ncomp, const int4* boxes, int* done, int* next, int reach) {
+    const uint32_t* ids, int ncomp, const int4* boxes, const int* sufTop, int* pred,
+    int* queue, int* qHead, int* qTail, int reach) {
     __shared__ TrialSmem<kSchedThreads> sm;
     __shared__ int sIdx;
     // this CTA's private buffers
@@ -535,25 +619,46 @@ __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
                                                          size_t(kCtaPixels) * 4);
     local.bkE = reinterpret_cast<float*>(mine + size_t(kCtaCells) * 16 + size_t(kCtaPixels) * 16);
     for (;;) {
-        if (threadIdx.x == 0) sIdx = atomicAdd(next, 1);
+        if (threadIdx.x == 0) {
+            const int k = atomicAdd(qHead, 1);
+            int i = -1;
+#ifdef GLU_SCHED_TRACE
+            const unsigned long long tc = gtimer();
+#endif
+            if (k < ncomp)
+                while ((i = ld_relaxed(queue + k)) < 0) __nanosleep(100);
+#ifdef GLU_SCHED_TRACE
+            if (i >= 0) {
+                g_trace[3 * i] = tc;
+                g_trace[3 * i + 1] = gtimer();
+            }
+#endif
+            sIdx = i;
+        }
         __syncthreads();
         const int i = sIdx;
-        if (i >= ncomp) break;
+        if (i < 0) break;
+        __threadfence();  // acquire: the predecessors' writes are visible
         const int4 bi = boxes[i];
-        // wait for every earlier trial this one conflicts with
-        for (int j = threadIdx.x; j < i; j += kSchedThreads)
-            if (boxes_conflict(boxes[j], bi, reach))
-                while (ld_relaxed(done + j) == 0) __nanosleep(200);
-        __syncthreads();
-        __threadfence();  // acquire: the published trials' writes are visible
         const bool isBig = bi.x < 0;
         const uint32_t c = ids ? ids[i] : uint32_t(i);
         const int v = run_trial<kSchedThreads>(t, isBig ? big : local, sm, px + off[c],
                                                off[c + 1] - off[c]);
         if (threadIdx.x == 0) {
             atomicAdd(t.result + (v ? 0 : 1), 1);
-            __threadfence();
-            st_release(done + i, 1);
+#ifdef GLU_SCHED_TRACE
+            g_trace[3 * i + 2] = gtimer();
+#endif
+        }
+        __threadfence();  // release this trial's writes (ordered after run_trial's barrier)
+        const int lim = bi.w + reach;
+        for (int base = i + 1; base < ncomp; base += kSchedThreads) {
+            if (sufTop[base] > lim) break;
+            const int j = base + int(threadIdx.x);
+            if (j < ncomp && boxes_conflict(bi, boxes[j], reach) && atomicSub(pred + j, 1) == 1) {
+                __threadfence();
+                st_release(queue + atomicAdd(qTail, 1), j);
+            }
         }
     }
 }
@@ -640,26 +745,61 @@ int run_sched(glu_ctx* ctx, const TrialState& t, const JointScratch& js, const g
     const int grid = sched_grid(ctx);
     const size_t per = size_t(kCtaCells) * 16 + size_t(kCtaPixels) * 20;
     char* ctaBufs = static_cast<char*>(scratch(ctx, S_SCHED, per * grid));
-    // boxes (int4 per trial) | done flags | next counter
-    char* meta = static_cast<char*>(scratch(ctx, S_SCHED_META, n * 20 + 64));
+    // boxes (int4) | sufTop | queue | pred | qHead, qTail (per trial, 4-byte words)
+    char* meta = static_cast<char*>(scratch(ctx, S_SCHED_META, n * 28 + 64));
     if (!ctaBufs || !meta) return GLU_ENOMEM;
     int4* boxes = reinterpret_cast<int4*>(meta);
-    int* done = reinterpret_cast<int*>(meta + n * 16);
-    int* next = done + n;
-    cudaError_t e = cudaMemsetAsync(done, 0, (n + 1) * sizeof(int), ctx->stream);
+    int* sufTop = reinterpret_cast<int*>(meta + n * 16);
+    int* queue = sufTop + n;
+    int* pred = queue + n;
+    int* qHead = pred + n;
+    int* qTail = qHead + 1;
+    cudaError_t e = cudaMemsetAsync(pred, 0, (n + 2) * sizeof(int), ctx->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(queue, 0xff, n * sizeof(int), ctx->stream);
     if (e != cudaSuccess) return fail_cuda(e, "trial schedule");
+    const int reach = 2 * (cfg.windowSide / 2);
     k_trial_boxes<<<blocks_for(n * 32, 256), 256, 0, ctx->stream>>>(
         off, px, ids, int(n), g.highW, g.scale, g.lowW, g.lowH, cfg.windowSide / 2,
         cfg.literalComponentUpdate, 0, boxes);
-    ++ctx->launches;
+    k_suffix_top<<<1, 1024, 0, ctx->stream>>>(boxes, int(n), sufTop);
+    k_trial_preds<<<blocks_for(n * 32, 256), 256, 0, ctx->stream>>>(boxes, sufTop, int(n), reach,
+                                                                    pred);
+    k_trial_seed<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(pred, int(n), queue, qTail);
+    ctx->launches += 4;
     TrialState ts = t;
     TrialBuffers big = js.big;
-    int nc = int(n), reach = 2 * (cfg.windowSide / 2);
-    void* args[] = {&ts, &big, &ctaBufs, &off, &px, &ids, &nc, &boxes, &done, &next, &reach};
+    int nc = int(n), rch = reach;
+    void* args[] = {&ts,    &big,   &ctaBufs, &off,  &px,    &ids,   &nc,
+                    &boxes, &sufTop, &pred,   &queue, &qHead, &qTail, &rch};
+#ifdef GLU_SCHED_TRACE
+    unsigned long long* trace = nullptr;
+    cudaMalloc(&trace, n * 24 + 8);
+    cudaMemcpyToSymbolAsync(g_trace, &trace, sizeof(trace), 0, cudaMemcpyHostToDevice,
+                            ctx->stream);
+#endif
     e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_trial_sched), grid, kSchedThreads,
                                     args, 0, ctx->stream);
     ++ctx->launches;
     if (e != cudaSuccess) return fail_cuda(e, "trial schedule");
+#ifdef GLU_SCHED_TRACE
+    {
+        std::vector<unsigned long long> h(3 * n);
+        std::vector<int4> hb(n);
+        cudaMemcpyAsync(h.data(), trace, n * 24, cudaMemcpyDeviceToHost, ctx->stream);
+        cudaMemcpyAsync(hb.data(), boxes, n * 16, cudaMemcpyDeviceToHost, ctx->stream);
+        cudaStreamSynchronize(ctx->stream);
+        cudaFree(trace);
+        if (const char* f = getenv("GLU_SCHED_TRACE_FILE")) {
+            if (FILE* fp = fopen(f, "ab")) {
+                const unsigned long long hdr[2] = {0x5452414345ull, n};
+                fwrite(hdr, 8, 2, fp);
+                fwrite(h.data(), 8, 3 * n, fp);
+                fwrite(hb.data(), 16, n, fp);
+                fclose(fp);
+            }
+        }
+    }
+#endif
     return GLU_OK;
 }
 

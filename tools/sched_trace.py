@@ -1,0 +1,81 @@
+"""Critical-path analysis of the parallel trial scheduler (k_trial_sched).
+
+    GPU box:  bash tools/ab_sched.sh -DGLU_SCHED_TRACE -- python tools/sched_trace.py run
+    here:     python tools/sched_trace.py show gpurun_out/sched_trace.bin
+
+`run` times one joint_optimize per config (after a warm-up) with the trace
+build, which appends per-trial {claim, ready, end} %globaltimer stamps and
+the trial boxes of every k_trial_sched launch to $GLU_SCHED_TRACE_FILE.
+`show` reports, per launch: span, mean wait / run time, and the critical
+path through the conflict graph (Chebyshev box distance <= 2h) weighted by
+the measured run times -- the lower bound of any in-order schedule.
+"""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def run(out):
+    import torch
+    import paper_2307_09582_b200 as glu
+    from paper_2307_09582_b200 import workloads
+    for c in (2, 4):
+        cfg = workloads.CONFIGS[c]
+        high = torch.from_numpy(workloads.scene(cfg["W"], cfg["H"], c, 0)).cuda()
+        glu.joint_optimize(high, cfg["scale"])
+        torch.cuda.synchronize()
+        os.environ["GLU_SCHED_TRACE_FILE"] = out + ".C%d" % c
+        glu.joint_optimize(high, cfg["scale"])
+        torch.cuda.synchronize()
+        del os.environ["GLU_SCHED_TRACE_FILE"]
+
+
+def launches(path):
+    raw = open(path, "rb").read()
+    o = 0
+    while o < len(raw):
+        magic, n = np.frombuffer(raw, np.uint64, 2, o)
+        assert magic == 0x5452414345
+        n = int(n)
+        o += 16
+        st = np.frombuffer(raw, np.uint64, 3 * n, o).reshape(n, 3).astype(np.int64)
+        o += 24 * n
+        bx = np.frombuffer(raw, np.int32, 4 * n, o).reshape(n, 4).astype(np.int64)
+        o += 16 * n
+        yield st, bx
+
+
+def show(path, reach=2):
+    for k, (st, bx) in enumerate(launches(path)):
+        n = len(st)
+        t0 = st[:, 0].min()
+        wait = (st[:, 1] - st[:, 0]) / 1e3
+        runt = (st[:, 2] - st[:, 1]) / 1e3
+        fin = np.zeros(n)
+        depth = np.zeros(n, np.int64)
+        for i in range(n):
+            dx = np.maximum(0, np.maximum(bx[:i, 0] - bx[i, 2], bx[i, 0] - bx[:i, 2]))
+            dy = np.maximum(0, np.maximum(bx[:i, 1] - bx[i, 3], bx[i, 1] - bx[:i, 3]))
+            dep = np.maximum(dx, dy) <= reach
+            fin[i] = runt[i] + (fin[:i][dep].max() if dep.any() else 0.0)
+            depth[i] = 1 + (depth[:i][dep].max() if dep.any() else 0)
+        span = (st[:, 2].max() - t0) / 1e3
+        print(f"launch {k}: {n} trials, span {span:.0f} us, run mean {runt.mean():.1f} "
+              f"p50 {np.median(runt):.1f} max {runt.max():.1f} us, wait mean {wait.mean():.1f} us, "
+              f"sum run {runt.sum():.0f} us, critical path {fin.max():.0f} us "
+              f"({depth.max()} trials deep)")
+        # claim timeline: when did the last trial get claimed / become ready
+        print(f"   last claim at {(st[:, 0].max() - t0) / 1e3:.0f} us, "
+              f"last ready at {(st[:, 1].max() - t0) / 1e3:.0f} us")
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "run":
+        run(sys.argv[2] if len(sys.argv) > 2 else "gpurun_out/sched_trace.bin")
+    else:
+        for f in sys.argv[2:]:
+            print("==", f)
+            show(f)
