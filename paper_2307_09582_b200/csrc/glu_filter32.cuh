@@ -11,6 +11,7 @@ namespace glu_cu {
 
 struct Filter32Result {
     bool ok;     // false: take the exact double-precision path
+    int why;     // which rule sent the pixel to the exact path (diagnostics)
     int ja, jb;  // slot (r * 3 + c) of a and b in the 3 x 3 window
     float w;
 };
@@ -51,7 +52,7 @@ __device__ inline Filter32Result filter32_pixel(const float4 (&c)[9], const floa
         m1 = lt ? qq : m1;
         ja = lt ? j : ja;
     }
-    Filter32Result r{false, ja, ja, 1.0f};
+    Filter32Result r{false, 1, ja, ja, 1.0f};
     // a NaN candidate must take the reference's exact scan (comparisons with
     // NaN keep the earlier index there, e.g. a NaN first candidate stays a)
 #pragma unroll
@@ -62,8 +63,10 @@ __device__ inline Filter32Result filter32_pixel(const float4 (&c)[9], const floa
     for (int j = 1; j < 9; ++j)
         if (j == ja) ca = c[j];
     const bool exactA = ca.x == ip0 && ca.y == ip1 && ca.z == ip2;
+    r.why = 2;
     if (!(m1 < kInf) || ip0 != ip0 || ip1 != ip1 || ip2 != ip2 || !(m1 >= 1e-27f || exactA))
         return r;
+    r.why = 3;
     const float lim = __fmaf_rn(m1, kCA * kU, m1) + 1e-36f;
     if (m2 <= lim) {
 #pragma unroll
@@ -100,9 +103,11 @@ __device__ inline Filter32Result filter32_pixel(const float4 (&c)[9], const floa
 #pragma unroll
     for (int j = 1; j < 9; ++j)
         if (j == jb) cb = c[j];
+    r.why = 4;
     if (b1 == 0.0f) {
         if (!(cb.x == ip0 && cb.y == ip1 && cb.z == ip2)) return r;
     } else {
+        r.why = 5;
         const float smax = da + dmax;
         const float bb = fmaxf(b1, 1e-30f);
         const float rt = f32_rsqrt_approx(bb), st = bb * rt;
@@ -110,11 +115,37 @@ __device__ inline Filter32Result filter32_pixel(const float4 (&c)[9], const floa
         const float alpha = 1.0f - kU * (0.5f * kC1 * smax * rt + kC2);
         const float rhs = b1 + mb + kU * (0.5f * kC1 * smax * st + kC3 * epsf);
         if (b2 * alpha <= rhs || alpha <= 0.0f) {
+            // Close call.  Every candidate outside the close set has a larger
+            // double objective than jb, so the reference's first argmin lies in
+            // the set: evaluate just those in double, in index order.
+            unsigned close = 0;
 #pragma unroll
             for (int j = 0; j < 9; ++j)
-                if (j != jb && (obj[j] * alpha <= rhs || alpha <= 0.0f) &&
-                    !(c[j].x == cb.x && c[j].y == cb.y && c[j].z == cb.z))
-                    return r;
+                if (j == jb || obj[j] * alpha <= rhs || alpha <= 0.0f) {
+                    if (!(q[j] < kInf)) return r;  // off-grid slot: exact path
+                    close |= 1u << j;
+                }
+            const float a3[3] = {ca.x, ca.y, ca.z};
+            const double dA = dist64(ip, a3);
+            double best = 0, bw = 0;
+            int bj = -1;
+            for (int j = 0; j < 9; ++j) {
+                if (!(close >> j & 1u)) continue;
+                const float cj[3] = {c[j].x, c[j].y, c[j].z};
+                const double dj = dist64(ip, cj);
+                const double w = dj / (dA + dj + eps);
+                const double o = objective64(ip, a3, cj, w, eps);
+                if (bj < 0 || o < best) {
+                    best = o;
+                    bw = w;
+                    bj = j;
+                }
+            }
+            r.ok = true;
+            r.jb = bj;
+            r.w = float(bw);
+            r.why = 6;
+            return r;
         }
     }
     const float a3[3] = {ca.x, ca.y, ca.z}, b3[3] = {cb.x, cb.y, cb.z};

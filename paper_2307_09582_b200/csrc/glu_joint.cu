@@ -33,6 +33,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "glu_internal.h"
@@ -45,11 +46,11 @@ namespace {
 
 constexpr uint32_t kNone = 0xffffffffu;
 #ifndef GLU_SCHED_THREADS
-#define GLU_SCHED_THREADS 256
+#define GLU_SCHED_THREADS 512
 #endif
 constexpr int kSchedThreads = GLU_SCHED_THREADS;  // CTA size of the parallel trial scheduler
 constexpr int kSeqThreads = 1024;    // CTA size of the sequential (single-CTA) sweep
-// Per-CTA private trial buffers (x 2 CTAs per SM): a diagonal 200-pixel line
+// Per-CTA private trial buffers (one 512-thread CTA per SM): a diagonal 200-pixel line
 // at s = 8 has a 27 x 27-cell dilated box (46,656 pixels), so 64 Ki pixels
 // keeps the serialising whole-grid fallback for genuinely huge components.
 constexpr uint32_t kCtaPixels = 65536;  // per-CTA affected-pixel capacity
@@ -142,6 +143,28 @@ __global__ void k_ccl_offsets(const uint32_t* __restrict__ keys, size_t n, uint3
 
 // ---- trials -------------------------------------------------------------------
 
+#ifdef GLU_SCHED_TRACE
+// Development builds only (-DGLU_SCHED_TRACE): per trial {claim, ready, end}
+// %globaltimer stamps, dumped by run_sched to $GLU_SCHED_TRACE_FILE, and SM
+// cycles per run_trial phase (thread 0, after the phase's barrier).
+__device__ unsigned long long* g_trace;
+__device__ unsigned long long g_phase[24];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    return v;
+}
+#define GLU_PHASE(k)                                            \
+    if (threadIdx.x == 0) {                                     \
+        const long long c_ = clock64();                         \
+        atomicAdd(&g_phase[k], (unsigned long long)(c_ - tph)); \
+        tph = c_;                                               \
+    }
+#else
+#define GLU_PHASE(k)
+#endif
+
+
 struct TrialState {
     const float* high;
     float* low;
@@ -204,6 +227,9 @@ __device__ int run_trial(const TrialState& t, const TrialBuffers& b, TrialSmem<N
     const int tid = threadIdx.x;
     const int h = t.S / 2;
     const uint32_t W = uint32_t(t.W), s = uint32_t(t.s);
+#ifdef GLU_SCHED_TRACE
+    long long tph = clock64();
+#endif
     if (tid == 0) {
         sm.touched = 0;
         sm.box[0] = t.lw;
@@ -231,6 +257,7 @@ __device__ int run_trial(const TrialState& t, const TrialBuffers& b, TrialSmem<N
         }
     }
     __syncthreads();
+    GLU_PHASE(0)
     const uint32_t nt = sm.touched;
     // 2. replace each cell by its worst pixel (jointopt.cpp:130-142) and mark
     //    the cells whose windows reach it (affectedPixels, 76-110).
@@ -253,6 +280,7 @@ __device__ int run_trial(const TrialState& t, const TrialBuffers& b, TrialSmem<N
         }
     }
     __syncthreads();
+    GLU_PHASE(1)
     // 3. affected pixels in the reference order: dilated bounding box in raster
     //    cell order, then each footprint in raster order.
     const uint32_t* aff = comp;
@@ -295,6 +323,7 @@ __device__ int run_trial(const TrialState& t, const TrialBuffers& b, TrialSmem<N
         aff = b.aff;
         na = sm.base;
     }
+    GLU_PHASE(2)
     // 4. backup and e0 (jointopt.cpp:150-157).
     double part = 0;
     for (uint32_t i = tid; i < na; i += NT) {
@@ -306,6 +335,7 @@ __device__ int run_trial(const TrialState& t, const TrialBuffers& b, TrialSmem<N
     const double e0 = BlockReduce(sm.tmp.reduce).Sum(part);
     if (tid == 0) sm.e0 = e0;
     __syncthreads();
+    GLU_PHASE(3)
     // 5. re-solve (optimize_pixels, 159) and re-score (160-165).
     part = 0;
     bool changed = false;
@@ -340,6 +370,10 @@ __device__ int run_trial(const TrialState& t, const TrialBuffers& b, TrialSmem<N
                 done = true;
             }
         }
+#ifdef GLU_SCHED_TRACE
+        atomicAdd(&g_phase[10], 1ull);
+        if (!done) atomicAdd(&g_phase[9], 1ull);
+#endif
         if (!done) {
             const Pick pk = pick64(t.mode, ip, GlobalLowWindow{t.low, t.lw, x0, y0, nwx},
                                    nwx * nwy, t.eps);
@@ -358,6 +392,7 @@ __device__ int run_trial(const TrialState& t, const TrialBuffers& b, TrialSmem<N
         changed |= __float_as_uint(e) != __float_as_uint(b.bkE[i]);
         part += double(e);
     }
+    GLU_PHASE(4)
     const double e1 = BlockReduce(sm.tmp.reduce).Sum(part);
     // Identical per-pixel errors give identical sequential sums: accept.
     const bool anyChanged = __syncthreads_or(changed);
@@ -399,6 +434,7 @@ __device__ int run_trial(const TrialState& t, const TrialBuffers& b, TrialSmem<N
         }
         __syncthreads();
     }
+    GLU_PHASE(5)
     const int verdict = sm.verdict;
     // change log of an accepted trial (distributed joint loop)
     if (t.dCount && verdict) {
@@ -433,6 +469,7 @@ __device__ int run_trial(const TrialState& t, const TrialBuffers& b, TrialSmem<N
             }
         }
     }
+    GLU_PHASE(6)
     // 6. rollback (jointopt.cpp:169-179) and reset per-cell state.
     if (!verdict) {
         for (uint32_t i = tid; i < na; i += NT) {
@@ -453,6 +490,366 @@ __device__ int run_trial(const TrialState& t, const TrialBuffers& b, TrialSmem<N
         t.cellFlag[cell] = 0;
     }
     __syncthreads();
+    GLU_PHASE(7)
+    return verdict;
+}
+
+// ---- shared-memory trial path ---------------------------------------------------
+//
+// run_trial keeps its per-trial state in global memory (per-cell keys / marks
+// and the affected-pixel list), so one trial is a dozen dependent L2 round
+// trips.  A trial on the scheduler's critical path is pure latency, so the
+// common case -- the component's cell box known up front (boxes[i]) and small
+// -- keeps everything on chip instead: the LR colours of the box dilated by 2h
+// (every candidate any re-solve reads), the worst-pixel key per box cell, the
+// previous colours of the replaced cells and the affected-pixel offsets of
+// the h-dilated box, from which thread-strided pixel indices are mapped in
+// reference order by binary search.  Backup, re-solve and both error sums run
+// in one pass (a pixel's re-solve writes only that pixel's params / error).
+// Same results as run_trial, state for state.
+constexpr int kSQ = 2048;  // cells of the component's box
+constexpr int kSW = 4096;  // cells of the box dilated by 2h
+constexpr size_t kTrialSmemBytes =
+    size_t(kSQ) * 8 + size_t(kSW) * 16 + size_t(kSW + 1) * 4 + size_t(kSQ) * 4 + size_t(kSQ) * 12;
+
+struct TrialShared {
+    unsigned long long* key;  // [kSQ] worst-pixel key per box cell, 0: untouched
+    float4* win;              // [kSW] LR colours of the 2h-dilated box
+    uint32_t* pre;            // [kSW + 1] affected-pixel offsets over the h-dilated box
+    uint32_t* touched;        // [kSQ] replaced cells (box-local index, raster order)
+    float* old;               // [3 kSQ] their previous colours
+    __device__ static TrialShared carve(char* base) {
+        TrialShared s;
+        s.key = reinterpret_cast<unsigned long long*>(base);
+        s.win = reinterpret_cast<float4*>(base + size_t(kSQ) * 8);
+        s.pre = reinterpret_cast<uint32_t*>(base + size_t(kSQ) * 8 + size_t(kSW) * 16);
+        s.touched = s.pre + kSW + 1;
+        s.old = reinterpret_cast<float*>(s.touched + kSQ);
+        return s;
+    }
+};
+
+// Box geometry of one trial (cells): Q = the component's cells, D = Q dilated
+// by h (owner cells of the affected pixels), V = Q dilated by 2h (candidates).
+struct TrialGeom {
+    int qx0, qy0, qw, qh;
+    int dx0, dy0, dw, dh;
+    int vx0, vy0, vw, vh;
+    __device__ TrialGeom(int4 b, int h, int lw, int lh) {
+        qx0 = b.x;
+        qy0 = b.y;
+        qw = b.z - b.x + 1;
+        qh = b.w - b.y + 1;
+        dx0 = max(0, b.x - h);
+        dy0 = max(0, b.y - h);
+        dw = min(lw - 1, b.z + h) - dx0 + 1;
+        dh = min(lh - 1, b.w + h) - dy0 + 1;
+        vx0 = max(0, b.x - 2 * h);
+        vy0 = max(0, b.y - 2 * h);
+        vw = min(lw - 1, b.z + 2 * h) - vx0 + 1;
+        vh = min(lh - 1, b.w + 2 * h) - vy0 + 1;
+    }
+    __device__ bool fits() const { return qw * qh <= kSQ && vw * vh <= kSW; }
+};
+
+struct SmemLowWindow {
+    const float4* win;
+    int vw, ox, oy, nwx;  // (ox, oy): window origin relative to V
+    __device__ __forceinline__ const float* operator[](int i) const {
+        const int r = i / nwx, q = i - r * nwx;
+        return reinterpret_cast<const float*>(win + (oy + r) * vw + ox + q);
+    }
+};
+
+// Affected pixel i (reference order) -> HR pixel index and its owner cell.
+__device__ __forceinline__ uint32_t affected_pixel(const TrialState& t, const TrialGeom& g,
+                                                   const uint32_t* pre, uint32_t i, int& cx,
+                                                   int& cy) {
+    int lo = 0, hi = g.dw * g.dh;  // pre[lo] <= i < pre[hi]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (pre[mid] <= i)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    cx = g.dx0 + lo % g.dw;
+    cy = g.dy0 + lo / g.dw;
+    const uint32_t k = i - pre[lo];
+    const int fx0 = cx * t.s, fy0 = cy * t.s;
+    const uint32_t fw = uint32_t(min(fx0 + t.s, t.W) - fx0);
+    return uint32_t(fy0 + int(k / fw)) * uint32_t(t.W) + uint32_t(fx0) + k % fw;
+}
+
+template <int NT>
+__device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialSmem<NT>& sm,
+                              const TrialShared& ss, const TrialGeom& g, const uint32_t* comp,
+                              uint32_t n) {
+    using BlockScan = typename TrialSmem<NT>::BlockScan;
+    __shared__ double red[2][NT / 32];
+    const int tid = threadIdx.x;
+    const int h = t.S / 2;
+    const uint32_t W = uint32_t(t.W), s = uint32_t(t.s);
+#ifdef GLU_SCHED_TRACE
+    long long tph = clock64();
+#endif
+    // A. stage the candidate colours, clear the keys
+    const int nv = g.vw * g.vh, nq = g.qw * g.qh, nd = g.dw * g.dh;
+    for (int k = tid; k < nv; k += NT) {
+        const int y = g.vy0 + k / g.vw, x = g.vx0 + k % g.vw;
+        const float* src = t.low + 3 * (size_t(y) * t.lw + x);
+        ss.win[k] = make_float4(src[0], src[1], src[2], 0.0f);
+    }
+    for (int k = tid; k < nq; k += NT) ss.key[k] = 0;
+    __syncthreads();
+    // B. groupByOwnerCell + worst pixel per cell (jointopt.cpp:56-72, 130-142)
+    for (uint32_t i = tid; i < n; i += NT) {
+        const uint32_t p = comp[i];
+        const int cx = int((p % W) / s), cy = int((p / W) / s);
+        const unsigned long long key =
+            (static_cast<unsigned long long>(__float_as_uint(t.errors[p])) << 32) |
+            (0xffffffffu - p);
+        atomicMax(ss.key + (cy - g.qy0) * g.qw + (cx - g.qx0), key);
+    }
+    __syncthreads();
+    GLU_PHASE(0)
+    // C. replace the touched cells; affected-pixel offsets over D (76-110)
+    uint32_t nt = 0;
+    for (int b0 = 0; b0 < nq; b0 += NT) {
+        const int k = b0 + tid;
+        const unsigned long long key = k < nq ? ss.key[k] : 0ull;
+        uint32_t pos, total;
+        BlockScan(sm.tmp.scan).ExclusiveSum(key ? 1u : 0u, pos, total);
+        if (key) {
+            const uint32_t slot = nt + pos;
+            const int qx = g.qx0 + k % g.qw, qy = g.qy0 + k / g.qw;
+            const uint32_t best = 0xffffffffu - uint32_t(key & 0xffffffffu);
+            float4& wc = ss.win[(qy - g.vy0) * g.vw + (qx - g.vx0)];
+            ss.touched[slot] = uint32_t(k);
+            ss.old[3 * slot] = wc.x;
+            ss.old[3 * slot + 1] = wc.y;
+            ss.old[3 * slot + 2] = wc.z;
+            const float* src = t.high + 3 * size_t(best);
+            const float c0 = src[0], c1 = src[1], c2 = src[2];
+            wc = make_float4(c0, c1, c2, 0.0f);
+            float* lc = t.low + 3 * (size_t(qy) * t.lw + qx);
+            lc[0] = c0;
+            lc[1] = c1;
+            lc[2] = c2;
+        }
+        nt += total;
+        __syncthreads();
+    }
+    uint32_t na = 0;
+    for (int b0 = 0; b0 < nd; b0 += NT) {
+        const int k = b0 + tid;
+        uint32_t fs = 0;
+        if (k < nd) {
+            const int x = g.dx0 + k % g.dw, y = g.dy0 + k / g.dw;
+            bool hit = false;
+            for (int yy = max(y - h, g.qy0); yy <= min(y + h, g.qy0 + g.qh - 1) && !hit; ++yy)
+                for (int xx = max(x - h, g.qx0); xx <= min(x + h, g.qx0 + g.qw - 1); ++xx)
+                    if (ss.key[(yy - g.qy0) * g.qw + (xx - g.qx0)]) {
+                        hit = true;
+                        break;
+                    }
+            if (hit)
+                fs = uint32_t(min(x * t.s + t.s, t.W) - x * t.s) *
+                     uint32_t(min(y * t.s + t.s, t.H) - y * t.s);
+        }
+        uint32_t pos, total;
+        BlockScan(sm.tmp.scan).ExclusiveSum(fs, pos, total);
+        if (k < nd) ss.pre[k] = na + pos;
+        na += total;
+        __syncthreads();
+    }
+    if (tid == 0) ss.pre[nd] = na;
+    __syncthreads();
+    GLU_PHASE(2)
+    // D. backup + e0, re-solve + e1 (jointopt.cpp:150-165, optimize_pixels 159)
+    double part0 = 0, part1 = 0;
+    bool changed = false;
+    for (uint32_t i = tid; i < na; i += NT) {
+        int cx, cy;
+        const uint32_t p = affected_pixel(t, g, ss.pre, i, cx, cy);
+        const glu_pixel_params op = t.field[p];
+        const float oe = t.errors[p];
+        b.bkParams[i] = op;
+        b.bkE[i] = oe;
+        part0 += double(oe);
+        const float ip[3] = {t.high[3 * size_t(p)], t.high[3 * size_t(p) + 1],
+                             t.high[3 * size_t(p) + 2]};
+        const int x0 = max(0, cx - h), y0 = max(0, cy - h);
+        const int nwx = min(t.lw - 1, cx + h) - x0 + 1, nwy = min(t.lh - 1, cy + h) - y0 + 1;
+        int ax, ay, bx, by;
+        float w;
+        bool done = false;
+#ifdef GLU_SCHED_TRACE
+        float4 c_dbg[9];
+#endif
+        if (t.S == 3 && t.mode != GLU_MODE_EXACT) {
+            float4 c[9];
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                const int gx = cx - 1 + k % 3, gy = cy - 1 + k / 3;
+                c[k] = make_float4(__int_as_float(0x7f800000), __int_as_float(0x7f800000),
+                                   __int_as_float(0x7f800000), 0.0f);
+                if (gx >= 0 && gy >= 0 && gx < t.lw && gy < t.lh)
+                    c[k] = ss.win[(gy - g.vy0) * g.vw + (gx - g.vx0)];
+            }
+            const Filter32Result fr =
+                filter32_pixel(c, ip, float(t.eps), t.eps, t.mode == GLU_MODE_GNU);
+#ifdef GLU_SCHED_TRACE
+            for (int k = 0; k < 9; ++k) c_dbg[k] = c[k];
+            if (fr.ok && fr.why == 6) atomicAdd(&g_phase[16], 1ull);
+#endif
+            if (fr.ok) {
+                ax = cx - 1 + fr.ja % 3;
+                ay = cy - 1 + fr.ja / 3;
+                bx = cx - 1 + fr.jb % 3;
+                by = cy - 1 + fr.jb / 3;
+                w = fr.w;
+                done = true;
+            }
+        }
+#ifdef GLU_SCHED_TRACE
+        atomicAdd(&g_phase[10], 1ull);
+        if (!done) atomicAdd(&g_phase[9], 1ull);
+        if (!done && t.S == 3 && t.mode != GLU_MODE_EXACT)
+            atomicAdd(&g_phase[10 + filter32_pixel(c_dbg, ip, float(t.eps), t.eps,
+                                                   t.mode == GLU_MODE_GNU).why], 1ull);
+#endif
+        if (!done) {
+            const Pick pk = pick64(t.mode, ip,
+                                   SmemLowWindow{ss.win, g.vw, x0 - g.vx0, y0 - g.vy0, nwx},
+                                   nwx * nwy, t.eps);
+            ay = y0 + pk.ai / nwx;
+            ax = x0 + pk.ai % nwx;
+            by = y0 + pk.bi / nwx;
+            bx = x0 + pk.bi % nwx;
+            w = float(pk.w);
+        }
+        glu_pixel_params np;
+        np.a = uint32_t(ay) * uint32_t(t.lw) + uint32_t(ax);
+        np.b = uint32_t(by) * uint32_t(t.lw) + uint32_t(bx);
+        np.w = w;
+        t.field[p] = np;
+        const float4 la = ss.win[(ay - g.vy0) * g.vw + (ax - g.vx0)];
+        const float4 lb = ss.win[(by - g.vy0) * g.vw + (bx - g.vx0)];
+        const float r[3] = {lerp_clamp(w, la.x, lb.x, true), lerp_clamp(w, la.y, lb.y, true),
+                            lerp_clamp(w, la.z, lb.z, true)};
+        const float e = pixel_error(ip, r);
+        t.errors[p] = e;
+        changed |= __float_as_uint(e) != __float_as_uint(oe);
+        part1 += double(e);
+    }
+    GLU_PHASE(4)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        part0 += __shfl_down_sync(0xffffffffu, part0, o);
+        part1 += __shfl_down_sync(0xffffffffu, part1, o);
+    }
+    if ((tid & 31) == 0) {
+        red[0][tid >> 5] = part0;
+        red[1][tid >> 5] = part1;
+    }
+    const bool anyChanged = __syncthreads_or(changed);
+    if (tid == 0) {
+        double s0 = 0, e1 = 0;
+        for (int k = 0; k < NT / 32; ++k) {
+            s0 += red[0][k];
+            e1 += red[1][k];
+        }
+        const double bound = 4.0 * (double(na) + 64.0) * 0x1.0p-53 * (s0 + e1);
+        if (!anyChanged || e1 + bound < s0)
+            sm.verdict = 1;
+        else if (e1 > s0 + bound)
+            sm.verdict = 0;
+        else
+            sm.verdict = -1;
+    }
+    __syncthreads();
+    if (sm.verdict < 0) {
+        // exact reference order, as in run_trial
+        double q0 = 0, q1 = 0;
+        float* stage = reinterpret_cast<float*>(&sm.tmp);
+        constexpr uint32_t kChunk = sizeof(sm.tmp) / (2 * sizeof(float));
+        for (uint32_t c0 = 0; c0 < na; c0 += kChunk) {
+            const uint32_t m = min(kChunk, na - c0);
+            for (uint32_t k = tid; k < m; k += NT) {
+                int cx, cy;
+                stage[2 * k] = b.bkE[c0 + k];
+                stage[2 * k + 1] = t.errors[affected_pixel(t, g, ss.pre, c0 + k, cx, cy)];
+            }
+            __syncthreads();
+            if (tid == 0)
+                for (uint32_t k = 0; k < m; ++k) {
+                    q0 += double(stage[2 * k]);
+                    q1 += double(stage[2 * k + 1]);
+                }
+            __syncthreads();
+        }
+        if (tid == 0) {
+            sm.verdict = q1 <= q0;
+            atomicAdd(t.result + 2, 1);
+        }
+        __syncthreads();
+    }
+    const int verdict = sm.verdict;
+    GLU_PHASE(5)
+    if (t.dCount && verdict) {
+        if (tid == 0) {
+            sm.logCells = atomicAdd(t.dCount, nt);
+            sm.logPixels = atomicAdd(t.dCount + 1, na);
+            if (sm.logCells + nt > t.dCellCap || sm.logPixels + na > t.dPixelCap) {
+                atomicExch(t.dCount + 2, 1u);
+                sm.logCells = sm.logPixels = 0xffffffffu;
+            }
+        }
+        __syncthreads();
+        if (sm.logCells != 0xffffffffu) {
+            for (uint32_t i = tid; i < nt; i += NT) {
+                const int k = int(ss.touched[i]);
+                const int qx = g.qx0 + k % g.qw, qy = g.qy0 + k / g.qw;
+                const float4 c = ss.win[(qy - g.vy0) * g.vw + (qx - g.vx0)];
+                uint32_t* o = t.dCells + 4 * size_t(sm.logCells + i);
+                o[0] = uint32_t(qy) * uint32_t(t.lw) + uint32_t(qx);
+                o[1] = __float_as_uint(c.x);
+                o[2] = __float_as_uint(c.y);
+                o[3] = __float_as_uint(c.z);
+            }
+            for (uint32_t i = tid; i < na; i += NT) {
+                int cx, cy;
+                const uint32_t p = affected_pixel(t, g, ss.pre, i, cx, cy);
+                uint32_t* o = t.dPixels + 5 * size_t(sm.logPixels + i);
+                const glu_pixel_params pp = t.field[p];
+                o[0] = p;
+                o[1] = pp.a;
+                o[2] = pp.b;
+                o[3] = __float_as_uint(pp.w);
+                o[4] = __float_as_uint(t.errors[p]);
+            }
+        }
+    }
+    GLU_PHASE(6)
+    // E. rollback (jointopt.cpp:169-179); nothing global to reset
+    if (!verdict) {
+        for (uint32_t i = tid; i < na; i += NT) {
+            int cx, cy;
+            const uint32_t p = affected_pixel(t, g, ss.pre, i, cx, cy);
+            t.field[p] = b.bkParams[i];
+            t.errors[p] = b.bkE[i];
+        }
+        for (uint32_t i = tid; i < nt; i += NT) {
+            const int k = int(ss.touched[i]);
+            float* lc = t.low + 3 * (size_t(g.qy0 + k / g.qw) * t.lw + g.qx0 + k % g.qw);
+            lc[0] = ss.old[3 * i];
+            lc[1] = ss.old[3 * i + 1];
+            lc[2] = ss.old[3 * i + 2];
+        }
+    }
+    __syncthreads();
+    GLU_PHASE(7)
     return verdict;
 }
 
@@ -522,17 +919,6 @@ __device__ __forceinline__ int ld_relaxed(const int* p) {
     asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-
-#ifdef GLU_SCHED_TRACE
-// Development builds only (-DGLU_SCHED_TRACE): per trial {claim, ready, end}
-// %globaltimer stamps, dumped by run_sched to $GLU_SCHED_TRACE_FILE.
-__device__ unsigned long long* g_trace;
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long v;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
-    return v;
-}
-#endif
 
 __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -608,6 +994,8 @@ __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
     int* queue, int* qHead, int* qTail, int reach) {
     __shared__ TrialSmem<kSchedThreads> sm;
     __shared__ int sIdx;
+    extern __shared__ __align__(16) char dyn[];
+    const TrialShared ss = TrialShared::carve(dyn);
     // this CTA's private buffers
     char* mine = ctaBufs + size_t(blockIdx.x) *
                                (size_t(kCtaCells) * 16 + size_t(kCtaPixels) * 20);
@@ -642,14 +1030,23 @@ __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
         const int4 bi = boxes[i];
         const bool isBig = bi.x < 0;
         const uint32_t c = ids ? ids[i] : uint32_t(i);
-        const int v = run_trial<kSchedThreads>(t, isBig ? big : local, sm, px + off[c],
-                                               off[c + 1] - off[c]);
+        int v;
+        const TrialGeom geo(bi, t.S / 2, t.lw, t.lh);
+        if (!isBig && !t.literal && geo.fits())
+            v = run_trial_smem<kSchedThreads>(t, local, sm, ss, geo, px + off[c],
+                                              off[c + 1] - off[c]);
+        else
+            v = run_trial<kSchedThreads>(t, isBig ? big : local, sm, px + off[c],
+                                         off[c + 1] - off[c]);
         if (threadIdx.x == 0) {
             atomicAdd(t.result + (v ? 0 : 1), 1);
 #ifdef GLU_SCHED_TRACE
             g_trace[3 * i + 2] = gtimer();
 #endif
         }
+#ifdef GLU_SCHED_TRACE
+        long long tph = clock64();
+#endif
         __threadfence();  // release this trial's writes (ordered after run_trial's barrier)
         const int lim = bi.w + reach;
         for (int base = i + 1; base < ncomp; base += kSchedThreads) {
@@ -660,6 +1057,8 @@ __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
                 st_release(queue + atomicAdd(qTail, 1), j);
             }
         }
+        __syncthreads();
+        GLU_PHASE(8)
     }
 }
 
@@ -731,7 +1130,10 @@ int sched_grid(glu_ctx* ctx) {
     if (cached > 0 && cachedDev == ctx->device) return cached;
     int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_trial_sched, kSchedThreads, 0);
+    cudaFuncSetAttribute(k_trial_sched, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(kTrialSmemBytes));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_trial_sched, kSchedThreads,
+                                                  kTrialSmemBytes);
     cached = sms * std::max(1, std::min(per, 2));
     cachedDev = ctx->device;
     return cached;
@@ -778,7 +1180,7 @@ int run_sched(glu_ctx* ctx, const TrialState& t, const JointScratch& js, const g
                             ctx->stream);
 #endif
     e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_trial_sched), grid, kSchedThreads,
-                                    args, 0, ctx->stream);
+                                    args, kTrialSmemBytes, ctx->stream);
     ++ctx->launches;
     if (e != cudaSuccess) return fail_cuda(e, "trial schedule");
 #ifdef GLU_SCHED_TRACE
@@ -795,6 +1197,17 @@ int run_sched(glu_ctx* ctx, const TrialState& t, const JointScratch& js, const g
                 fwrite(hdr, 8, 2, fp);
                 fwrite(h.data(), 8, 3 * n, fp);
                 fwrite(hb.data(), 16, n, fp);
+                fclose(fp);
+            }
+        }
+        unsigned long long ph[24];
+        cudaMemcpyFromSymbol(ph, g_phase, sizeof(ph));
+        const unsigned long long z[24] = {};
+        cudaMemcpyToSymbol(g_phase, z, sizeof(z));
+        if (const char* f = getenv("GLU_SCHED_TRACE_FILE")) {
+            if (FILE* fp = fopen((std::string(f) + ".phases").c_str(), "a")) {
+                for (int k = 0; k < 17; ++k) fprintf(fp, "%llu ", ph[k]);
+                fprintf(fp, "%zu\n", n);
                 fclose(fp);
             }
         }

@@ -72,6 +72,26 @@ def show(path, reach=2):
               f"last ready at {(st[:, 1].max() - t0) / 1e3:.0f} us")
 
 
+PHASES = ["group", "replace", "affected", "backup+e0", "re-solve", "verdict", "log",
+          "rollback+reset", "release"]
+
+
+def show_phases(path):
+    if not os.path.exists(path):
+        return
+    for k, line in enumerate(open(path)):
+        v = [int(x) for x in line.split()]
+        n = v[-1]
+        print(f"launch {k} phases (SM cycles / trial): " +
+              ", ".join(f"{nm} {c / n:.0f}" for nm, c in zip(PHASES, v[:9])))
+        if len(v) > 10:
+            print(f"   re-solved pixels / trial {v[10] / n:.0f}, fp64 fallbacks {v[9]} "
+                  f"({100.0 * v[9] / max(1, v[10]):.3f}%)")
+        if len(v) > 17:
+            print("   fallback rule: nan %d, no-a/tiny %d, a-tie %d, zero-b %d, b-tie %d; "
+                  "b close calls settled in double %d" % tuple(v[11:17]))
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "run":
         run(sys.argv[2] if len(sys.argv) > 2 else "gpurun_out/sched_trace.bin")
@@ -79,3 +99,4 @@ if __name__ == "__main__":
         for f in sys.argv[2:]:
             print("==", f)
             show(f)
+            show_phases(f + ".phases")
