@@ -509,12 +509,15 @@ __device__ int run_trial(const TrialState& t, const TrialBuffers& b, TrialSmem<N
 // Same results as run_trial, state for state.
 constexpr int kSQ = 2048;  // cells of the component's box
 constexpr int kSW = 4096;  // cells of the box dilated by 2h
-constexpr size_t kTrialSmemBytes =
-    size_t(kSQ) * 8 + size_t(kSW) * 16 + size_t(kSW + 1) * 4 + size_t(kSQ) * 4 + size_t(kSQ) * 12;
+constexpr int kSC = 2048;  // pixels of the component
+constexpr int kSS = 512;   // successors found by the early scan (= the CTA size)
+constexpr size_t kTrialSmemBytes = size_t(kSQ) * 8 + size_t(kSW) * 16 + size_t(kSC) * 16 +
+                                   size_t(kSW + 1) * 4 + size_t(kSQ) * 4 + size_t(kSQ) * 12;
 
 struct TrialShared {
     unsigned long long* key;  // [kSQ] worst-pixel key per box cell, 0: untouched
     float4* win;              // [kSW] LR colours of the 2h-dilated box
+    float4* compC;            // [kSC] HR colours of the component's pixels
     uint32_t* pre;            // [kSW + 1] affected-pixel offsets over the h-dilated box
     uint32_t* touched;        // [kSQ] replaced cells (box-local index, raster order)
     float* old;               // [3 kSQ] their previous colours
@@ -522,7 +525,8 @@ struct TrialShared {
         TrialShared s;
         s.key = reinterpret_cast<unsigned long long*>(base);
         s.win = reinterpret_cast<float4*>(base + size_t(kSQ) * 8);
-        s.pre = reinterpret_cast<uint32_t*>(base + size_t(kSQ) * 8 + size_t(kSW) * 16);
+        s.compC = s.win + kSW;
+        s.pre = reinterpret_cast<uint32_t*>(s.compC + kSC);
         s.touched = s.pre + kSW + 1;
         s.old = reinterpret_cast<float*>(s.touched + kSQ);
         return s;
@@ -549,7 +553,9 @@ struct TrialGeom {
         vw = min(lw - 1, b.z + 2 * h) - vx0 + 1;
         vh = min(lh - 1, b.w + 2 * h) - vy0 + 1;
     }
-    __device__ bool fits() const { return qw * qh <= kSQ && vw * vh <= kSW; }
+    __device__ bool fits(uint32_t n) const {
+        return qw * qh <= kSQ && vw * vh <= kSW && n <= uint32_t(kSC);
+    }
 };
 
 struct SmemLowWindow {
@@ -559,6 +565,24 @@ struct SmemLowWindow {
         const int r = i / nwx, q = i - r * nwx;
         return reinterpret_cast<const float*>(win + (oy + r) * vw + ox + q);
     }
+};
+
+__device__ __forceinline__ bool boxes_conflict(int4 a, int4 b, int reach) {
+    const int dx = max(0, max(a.x - b.z, b.x - a.z));
+    const int dy = max(0, max(a.y - b.w, b.y - a.w));
+    return max(dx, dy) <= reach;
+}
+
+// The scheduler's view of one trial: its index and box, and where its
+// conflicting successors found early (while pixel loads are in flight) go.
+struct SuccScan {
+    const int4* boxes;
+    const int* sufTop;
+    int ncomp, reach, self;
+    int4 box;
+    int* list;   // [kSS] shared
+    int* count;  // shared; the caller zeroes it
+    int* more;   // shared: successors may lie beyond the first kSS trials
 };
 
 // Affected pixel i (reference order) -> HR pixel index and its owner cell.
@@ -581,10 +605,17 @@ __device__ __forceinline__ uint32_t affected_pixel(const TrialState& t, const Tr
     return uint32_t(fy0 + int(k / fw)) * uint32_t(t.W) + uint32_t(fx0) + k % fw;
 }
 
+struct PixIn {
+    uint32_t p;
+    int cx, cy;
+    glu_pixel_params op;
+    float oe, i0, i1, i2;
+};
+
 template <int NT>
 __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialSmem<NT>& sm,
                               const TrialShared& ss, const TrialGeom& g, const uint32_t* comp,
-                              uint32_t n) {
+                              uint32_t n, const SuccScan& sc) {
     using BlockScan = typename TrialSmem<NT>::BlockScan;
     __shared__ double red[2][NT / 32];
     const int tid = threadIdx.x;
@@ -593,22 +624,24 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
 #ifdef GLU_SCHED_TRACE
     long long tph = clock64();
 #endif
-    // A. stage the candidate colours, clear the keys
+    // A. stage the candidate colours and the component's colours; group its
+    //    pixels by owner cell keeping the worst, i.e. the first strict argmax
+    //    over ascending pixels = max of (E, -index) (jointopt.cpp:56-72,
+    //    130-142).  Keys are zero on entry (the previous trial cleared them).
     const int nv = g.vw * g.vh, nq = g.qw * g.qh, nd = g.dw * g.dh;
     for (int k = tid; k < nv; k += NT) {
         const int y = g.vy0 + k / g.vw, x = g.vx0 + k % g.vw;
         const float* src = t.low + 3 * (size_t(y) * t.lw + x);
         ss.win[k] = make_float4(src[0], src[1], src[2], 0.0f);
     }
-    for (int k = tid; k < nq; k += NT) ss.key[k] = 0;
-    __syncthreads();
-    // B. groupByOwnerCell + worst pixel per cell (jointopt.cpp:56-72, 130-142)
     for (uint32_t i = tid; i < n; i += NT) {
         const uint32_t p = comp[i];
+        const float* src = t.high + 3 * size_t(p);
+        const float e = t.errors[p];
+        ss.compC[i] = make_float4(src[0], src[1], src[2], 0.0f);
         const int cx = int((p % W) / s), cy = int((p / W) / s);
         const unsigned long long key =
-            (static_cast<unsigned long long>(__float_as_uint(t.errors[p])) << 32) |
-            (0xffffffffu - p);
+            (static_cast<unsigned long long>(__float_as_uint(e)) << 32) | (0xffffffffu - i);
         atomicMax(ss.key + (cy - g.qy0) * g.qw + (cx - g.qx0), key);
     }
     __syncthreads();
@@ -623,15 +656,14 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
         if (key) {
             const uint32_t slot = nt + pos;
             const int qx = g.qx0 + k % g.qw, qy = g.qy0 + k / g.qw;
-            const uint32_t best = 0xffffffffu - uint32_t(key & 0xffffffffu);
+            const float4 bc = ss.compC[0xffffffffu - uint32_t(key & 0xffffffffu)];
             float4& wc = ss.win[(qy - g.vy0) * g.vw + (qx - g.vx0)];
             ss.touched[slot] = uint32_t(k);
             ss.old[3 * slot] = wc.x;
             ss.old[3 * slot + 1] = wc.y;
             ss.old[3 * slot + 2] = wc.z;
-            const float* src = t.high + 3 * size_t(best);
-            const float c0 = src[0], c1 = src[1], c2 = src[2];
-            wc = make_float4(c0, c1, c2, 0.0f);
+            const float c0 = bc.x, c1 = bc.y, c2 = bc.z;
+            wc = bc;
             float* lc = t.low + 3 * (size_t(qy) * t.lw + qx);
             lc[0] = c0;
             lc[1] = c1;
@@ -666,19 +698,42 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
     if (tid == 0) ss.pre[nd] = na;
     __syncthreads();
     GLU_PHASE(2)
-    // D. backup + e0, re-solve + e1 (jointopt.cpp:150-165, optimize_pixels 159)
+    // D. backup + e0, re-solve + e1 (jointopt.cpp:150-165, optimize_pixels 159).
+    //    Each thread's next pixel is loaded while the current one is solved.
+    for (int k = tid; k < nq; k += NT) ss.key[k] = 0;
+    auto load = [&](uint32_t i) {
+        PixIn q;
+        q.p = affected_pixel(t, g, ss.pre, i, q.cx, q.cy);
+        q.op = t.field[q.p];
+        q.oe = t.errors[q.p];
+        q.i0 = t.high[3 * size_t(q.p)];
+        q.i1 = t.high[3 * size_t(q.p) + 1];
+        q.i2 = t.high[3 * size_t(q.p) + 2];
+        return q;
+    };
+    PixIn cur{};
+    if (uint32_t(tid) < na) cur = load(tid);
+    {
+        // conflicting successors among the next NT trials, while loads fly
+        const int j = sc.self + 1 + tid;
+        if (j < sc.ncomp && boxes_conflict(sc.box, sc.boxes[j], sc.reach))
+            sc.list[atomicAdd(sc.count, 1)] = j;
+        if (tid == 0)
+            *sc.more = sc.self + 1 + NT < sc.ncomp && sc.sufTop[sc.self + 1 + NT] <= sc.box.w + sc.reach;
+    }
     double part0 = 0, part1 = 0;
     bool changed = false;
     for (uint32_t i = tid; i < na; i += NT) {
-        int cx, cy;
-        const uint32_t p = affected_pixel(t, g, ss.pre, i, cx, cy);
-        const glu_pixel_params op = t.field[p];
-        const float oe = t.errors[p];
+        PixIn nxt{};
+        if (i + NT < na) nxt = load(i + NT);
+        const uint32_t p = cur.p;
+        const int cx = cur.cx, cy = cur.cy;
+        const glu_pixel_params op = cur.op;
+        const float oe = cur.oe;
         b.bkParams[i] = op;
         b.bkE[i] = oe;
         part0 += double(oe);
-        const float ip[3] = {t.high[3 * size_t(p)], t.high[3 * size_t(p) + 1],
-                             t.high[3 * size_t(p) + 2]};
+        const float ip[3] = {cur.i0, cur.i1, cur.i2};
         const int x0 = max(0, cx - h), y0 = max(0, cy - h);
         const int nwx = min(t.lw - 1, cx + h) - x0 + 1, nwy = min(t.lh - 1, cy + h) - y0 + 1;
         int ax, ay, bx, by;
@@ -742,6 +797,7 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
         t.errors[p] = e;
         changed |= __float_as_uint(e) != __float_as_uint(oe);
         part1 += double(e);
+        cur = nxt;
     }
     GLU_PHASE(4)
 #pragma unroll
@@ -905,11 +961,6 @@ __global__ void k_trial_boxes(const uint32_t* __restrict__ off, const uint32_t* 
     }
 }
 
-__device__ __forceinline__ bool boxes_conflict(int4 a, int4 b, int reach) {
-    const int dx = max(0, max(a.x - b.z, b.x - a.z));
-    const int dy = max(0, max(a.y - b.w, b.y - a.w));
-    return max(dx, dy) <= reach;
-}
 
 // Polling uses relaxed loads (served by L2, no L1 invalidation: an acquire load
 // would flush the SM's L1 on every poll and starve the co-resident CTA doing
@@ -991,7 +1042,7 @@ __global__ void k_trial_seed(const int* __restrict__ pred, int n, int* __restric
 __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
     TrialState t, TrialBuffers big, char* ctaBufs, const uint32_t* off, const uint32_t* px,
     const uint32_t* ids, int ncomp, const int4* boxes, const int* sufTop, int* pred,
-    int* queue, int* qHead, int* qTail, int reach) {
+    int* queue, int* qHead, int* qTail, int* finished, int reach) {
     __shared__ TrialSmem<kSchedThreads> sm;
     __shared__ int sIdx;
     extern __shared__ __align__(16) char dyn[];
@@ -1006,15 +1057,25 @@ __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
     local.bkParams = reinterpret_cast<glu_pixel_params*>(mine + size_t(kCtaCells) * 16 +
                                                          size_t(kCtaPixels) * 4);
     local.bkE = reinterpret_cast<float*>(mine + size_t(kCtaCells) * 16 + size_t(kCtaPixels) * 16);
+    static_assert(kSS >= kSchedThreads, "early successor scan covers one CTA width");
+    __shared__ int sNext, sCount, sMore;
+    __shared__ int sList[kSS];
+    for (int k = threadIdx.x; k < kSQ; k += kSchedThreads) ss.key[k] = 0;
+    if (threadIdx.x == 0) sNext = -1;
     for (;;) {
         if (threadIdx.x == 0) {
-            const int k = atomicAdd(qHead, 1);
-            int i = -1;
+            int i = sNext;
 #ifdef GLU_SCHED_TRACE
             const unsigned long long tc = gtimer();
 #endif
-            if (k < ncomp)
-                while ((i = ld_relaxed(queue + k)) < 0) __nanosleep(100);
+            if (i < 0) {
+                const int k = atomicAdd(qHead, 1);
+                // (continuations bypass the FIFO, so not every slot fills:
+                // stop waiting once every trial has finished)
+                if (k < ncomp)
+                    while ((i = ld_relaxed(queue + k)) < 0 && ld_relaxed(finished) < ncomp)
+                        __nanosleep(100);
+            }
 #ifdef GLU_SCHED_TRACE
             if (i >= 0) {
                 g_trace[3 * i] = tc;
@@ -1022,6 +1083,9 @@ __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
             }
 #endif
             sIdx = i;
+            sNext = -1;
+            sCount = 0;
+            sMore = 1;
         }
         __syncthreads();
         const int i = sIdx;
@@ -1030,14 +1094,16 @@ __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
         const int4 bi = boxes[i];
         const bool isBig = bi.x < 0;
         const uint32_t c = ids ? ids[i] : uint32_t(i);
+        const uint32_t n = off[c + 1] - off[c];
         int v;
         const TrialGeom geo(bi, t.S / 2, t.lw, t.lh);
-        if (!isBig && !t.literal && geo.fits())
-            v = run_trial_smem<kSchedThreads>(t, local, sm, ss, geo, px + off[c],
-                                              off[c + 1] - off[c]);
-        else
-            v = run_trial<kSchedThreads>(t, isBig ? big : local, sm, px + off[c],
-                                         off[c + 1] - off[c]);
+        const bool onChip = !isBig && !t.literal && geo.fits(n);
+        if (onChip) {
+            const SuccScan sc{boxes, sufTop, ncomp, reach, i, bi, sList, &sCount, &sMore};
+            v = run_trial_smem<kSchedThreads>(t, local, sm, ss, geo, px + off[c], n, sc);
+        } else {
+            v = run_trial<kSchedThreads>(t, isBig ? big : local, sm, px + off[c], n);
+        }
         if (threadIdx.x == 0) {
             atomicAdd(t.result + (v ? 0 : 1), 1);
 #ifdef GLU_SCHED_TRACE
@@ -1047,17 +1113,27 @@ __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
 #ifdef GLU_SCHED_TRACE
         long long tph = clock64();
 #endif
+        // Release the conflicting successors (those found early, then the
+        // rest).  One successor whose count reaches zero runs next on this CTA
+        // (a dependency chain stays put); the others go to the FIFO.
         __threadfence();  // release this trial's writes (ordered after run_trial's barrier)
-        const int lim = bi.w + reach;
-        for (int base = i + 1; base < ncomp; base += kSchedThreads) {
-            if (sufTop[base] > lim) break;
-            const int j = base + int(threadIdx.x);
-            if (j < ncomp && boxes_conflict(bi, boxes[j], reach) && atomicSub(pred + j, 1) == 1) {
+        auto release = [&](int j) {
+            if (atomicSub(pred + j, 1) == 1 && atomicCAS(&sNext, -1, j) != -1) {
                 __threadfence();
                 st_release(queue + atomicAdd(qTail, 1), j);
             }
+        };
+        if (threadIdx.x < sCount) release(sList[threadIdx.x]);
+        if (sMore) {
+            const int lim = bi.w + reach;
+            for (int base = onChip ? i + 1 + kSchedThreads : i + 1; base < ncomp; base += kSchedThreads) {
+                if (sufTop[base] > lim) break;
+                const int j = base + int(threadIdx.x);
+                if (j < ncomp && boxes_conflict(bi, boxes[j], reach)) release(j);
+            }
         }
         __syncthreads();
+        if (threadIdx.x == 0) atomicAdd(finished, 1);  // after this trial's pushes
         GLU_PHASE(8)
     }
 }
@@ -1147,7 +1223,7 @@ int run_sched(glu_ctx* ctx, const TrialState& t, const JointScratch& js, const g
     const int grid = sched_grid(ctx);
     const size_t per = size_t(kCtaCells) * 16 + size_t(kCtaPixels) * 20;
     char* ctaBufs = static_cast<char*>(scratch(ctx, S_SCHED, per * grid));
-    // boxes (int4) | sufTop | queue | pred | qHead, qTail (per trial, 4-byte words)
+    // boxes (int4) | sufTop | queue | pred | qHead, qTail, finished (4-byte words)
     char* meta = static_cast<char*>(scratch(ctx, S_SCHED_META, n * 28 + 64));
     if (!ctaBufs || !meta) return GLU_ENOMEM;
     int4* boxes = reinterpret_cast<int4*>(meta);
@@ -1156,7 +1232,8 @@ int run_sched(glu_ctx* ctx, const TrialState& t, const JointScratch& js, const g
     int* pred = queue + n;
     int* qHead = pred + n;
     int* qTail = qHead + 1;
-    cudaError_t e = cudaMemsetAsync(pred, 0, (n + 2) * sizeof(int), ctx->stream);
+    int* finished = qHead + 2;
+    cudaError_t e = cudaMemsetAsync(pred, 0, (n + 3) * sizeof(int), ctx->stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(queue, 0xff, n * sizeof(int), ctx->stream);
     if (e != cudaSuccess) return fail_cuda(e, "trial schedule");
     const int reach = 2 * (cfg.windowSide / 2);
@@ -1172,7 +1249,7 @@ int run_sched(glu_ctx* ctx, const TrialState& t, const JointScratch& js, const g
     TrialBuffers big = js.big;
     int nc = int(n), rch = reach;
     void* args[] = {&ts,    &big,   &ctaBufs, &off,  &px,    &ids,   &nc,
-                    &boxes, &sufTop, &pred,   &queue, &qHead, &qTail, &rch};
+                    &boxes, &sufTop, &pred,   &queue, &qHead, &qTail, &finished, &rch};
 #ifdef GLU_SCHED_TRACE
     unsigned long long* trace = nullptr;
     cudaMalloc(&trace, n * 24 + 8);
