@@ -512,13 +512,15 @@ constexpr int kSW = 4096;  // cells of the box dilated by 2h
 constexpr int kSC = 2048;  // pixels of the component
 constexpr int kSS = 512;   // successors found by the early scan (= the CTA size)
 constexpr size_t kTrialSmemBytes = size_t(kSQ) * 8 + size_t(kSW) * 16 + size_t(kSC) * 16 +
-                                   size_t(kSW + 1) * 4 + size_t(kSQ) * 4 + size_t(kSQ) * 12;
+                                   size_t(kSW + 1) * 4 + size_t(kSW) * 4 + size_t(kSQ) * 4 +
+                                   size_t(kSQ) * 12;
 
 struct TrialShared {
     unsigned long long* key;  // [kSQ] worst-pixel key per box cell, 0: untouched
     float4* win;              // [kSW] LR colours of the 2h-dilated box
     float4* compC;            // [kSC] HR colours of the component's pixels
     uint32_t* pre;            // [kSW + 1] affected-pixel offsets over the h-dilated box
+    uint32_t* cellOf;         // [kSW] affected cells in order, (y << 16) | x
     uint32_t* touched;        // [kSQ] replaced cells (box-local index, raster order)
     float* old;               // [3 kSQ] their previous colours
     __device__ static TrialShared carve(char* base) {
@@ -527,7 +529,8 @@ struct TrialShared {
         s.win = reinterpret_cast<float4*>(base + size_t(kSQ) * 8);
         s.compC = s.win + kSW;
         s.pre = reinterpret_cast<uint32_t*>(s.compC + kSC);
-        s.touched = s.pre + kSW + 1;
+        s.cellOf = s.pre + kSW + 1;
+        s.touched = s.cellOf + kSW;
         s.old = reinterpret_cast<float*>(s.touched + kSQ);
         return s;
     }
@@ -539,7 +542,9 @@ struct TrialGeom {
     int qx0, qy0, qw, qh;
     int dx0, dy0, dw, dh;
     int vx0, vy0, vw, vh;
-    __device__ TrialGeom(int4 b, int h, int lw, int lh) {
+    bool full;  // every footprint in D is a full s x s block
+    int sh;     // log2(s) when s is a power of two, else -1
+    __device__ TrialGeom(int4 b, int h, int lw, int lh, int s, int W, int H) {
         qx0 = b.x;
         qy0 = b.y;
         qw = b.z - b.x + 1;
@@ -552,6 +557,8 @@ struct TrialGeom {
         vy0 = max(0, b.y - 2 * h);
         vw = min(lw - 1, b.z + 2 * h) - vx0 + 1;
         vh = min(lh - 1, b.w + 2 * h) - vy0 + 1;
+        full = (dx0 + dw) * s <= W && (dy0 + dh) * s <= H && lw < 65536 && lh < 65536;
+        sh = (s & (s - 1)) == 0 ? __ffs(s) - 1 : -1;
     }
     __device__ bool fits(uint32_t n) const {
         return qw * qh <= kSQ && vw * vh <= kSW && n <= uint32_t(kSC);
@@ -586,9 +593,31 @@ struct SuccScan {
 };
 
 // Affected pixel i (reference order) -> HR pixel index and its owner cell.
+// When every affected footprint is a full s x s block (g.full), pixel i is
+// pixel i % s^2 of the (i / s^2)-th affected cell; otherwise binary search.
 __device__ __forceinline__ uint32_t affected_pixel(const TrialState& t, const TrialGeom& g,
-                                                   const uint32_t* pre, uint32_t i, int& cx,
+                                                   const TrialShared& ss, uint32_t i, int& cx,
                                                    int& cy) {
+    if (g.full) {
+        uint32_t q, k, kx, ky;
+        if (g.sh >= 0) {
+            q = i >> (2 * g.sh);
+            k = i & ((1u << (2 * g.sh)) - 1);
+            ky = k >> g.sh;
+            kx = k & ((1u << g.sh) - 1);
+        } else {
+            const uint32_t s = uint32_t(t.s);
+            q = i / (s * s);
+            k = i - q * s * s;
+            ky = k / s;
+            kx = k - ky * s;
+        }
+        const uint32_t cc = ss.cellOf[q];
+        cx = int(cc & 0xffffu);
+        cy = int(cc >> 16);
+        return (uint32_t(cy * t.s) + ky) * uint32_t(t.W) + uint32_t(cx * t.s) + kx;
+    }
+    const uint32_t* pre = ss.pre;
     int lo = 0, hi = g.dw * g.dh;  // pre[lo] <= i < pre[hi]
     while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
@@ -692,6 +721,9 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
         uint32_t pos, total;
         BlockScan(sm.tmp.scan).ExclusiveSum(fs, pos, total);
         if (k < nd) ss.pre[k] = na + pos;
+        if (fs && g.full)
+            ss.cellOf[(na + pos) / uint32_t(t.s * t.s)] =
+                (uint32_t(g.dy0 + k / g.dw) << 16) | uint32_t(g.dx0 + k % g.dw);
         na += total;
         __syncthreads();
     }
@@ -703,7 +735,7 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
     for (int k = tid; k < nq; k += NT) ss.key[k] = 0;
     auto load = [&](uint32_t i) {
         PixIn q;
-        q.p = affected_pixel(t, g, ss.pre, i, q.cx, q.cy);
+        q.p = affected_pixel(t, g, ss, i, q.cx, q.cy);
         q.op = t.field[q.p];
         q.oe = t.errors[q.p];
         q.i0 = t.high[3 * size_t(q.p)];
@@ -835,7 +867,7 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
             for (uint32_t k = tid; k < m; k += NT) {
                 int cx, cy;
                 stage[2 * k] = b.bkE[c0 + k];
-                stage[2 * k + 1] = t.errors[affected_pixel(t, g, ss.pre, c0 + k, cx, cy)];
+                stage[2 * k + 1] = t.errors[affected_pixel(t, g, ss, c0 + k, cx, cy)];
             }
             __syncthreads();
             if (tid == 0)
@@ -876,7 +908,7 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
             }
             for (uint32_t i = tid; i < na; i += NT) {
                 int cx, cy;
-                const uint32_t p = affected_pixel(t, g, ss.pre, i, cx, cy);
+                const uint32_t p = affected_pixel(t, g, ss, i, cx, cy);
                 uint32_t* o = t.dPixels + 5 * size_t(sm.logPixels + i);
                 const glu_pixel_params pp = t.field[p];
                 o[0] = p;
@@ -892,7 +924,7 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
     if (!verdict) {
         for (uint32_t i = tid; i < na; i += NT) {
             int cx, cy;
-            const uint32_t p = affected_pixel(t, g, ss.pre, i, cx, cy);
+            const uint32_t p = affected_pixel(t, g, ss, i, cx, cy);
             t.field[p] = b.bkParams[i];
             t.errors[p] = b.bkE[i];
         }
@@ -1096,7 +1128,7 @@ __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
         const uint32_t c = ids ? ids[i] : uint32_t(i);
         const uint32_t n = off[c + 1] - off[c];
         int v;
-        const TrialGeom geo(bi, t.S / 2, t.lw, t.lh);
+        const TrialGeom geo(bi, t.S / 2, t.lw, t.lh, t.s, t.W, t.H);
         const bool onChip = !isBig && !t.literal && geo.fits(n);
         if (onChip) {
             const SuccScan sc{boxes, sufTop, ncomp, reach, i, bi, sList, &sCount, &sMore};

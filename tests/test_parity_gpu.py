@@ -290,19 +290,24 @@ def test_reference_unit_tests_pass_against_dropin_api(glu):
     assert m and int(m.group(1)) >= 55 and m.group(1) == m.group(2), r.stdout
 
 
-@pytest.mark.parametrize("W,H,s,S,literal", [(512, 384, 8, 3, False), (640, 360, 4, 3, False),
-                                             (480, 320, 6, 5, False), (400, 300, 8, 3, True)])
-def test_parallel_trial_schedule_matches_sequential(glu, W, H, s, S, literal):
-    """The conflict-aware parallel trial schedule is bit-identical to the
+@pytest.mark.parametrize("W,H,s,S,literal,mode", [
+    (512, 384, 8, 3, False, "fast"), (640, 360, 4, 3, False, "fast"),
+    (480, 320, 6, 5, False, "fast"), (400, 300, 8, 3, True, "fast"),
+    (480, 360, 6, 3, False, "fast"), (512, 384, 8, 3, False, "gnu"),
+    (384, 256, 8, 3, False, "exact"), (250, 190, 5, 5, False, "exact")])
+def test_parallel_trial_schedule_matches_sequential(glu, W, H, s, S, literal, mode):
+    """The conflict-aware parallel trial schedule (on-chip trial path, full and
+    clipped footprints, power-of-two and other scales) is bit-identical to the
     reference's sequential component loop (jointopt.cpp:195-202)."""
     from paper_2307_09582_b200 import workloads
     high = dev(workloads.scene(W, H, 40 + s))
     cfg = glu.GluConfig(windowSide=S, literalComponentUpdate=literal)
+    md = {"fast": glu.Mode.Fast, "gnu": glu.Mode.Gnu, "exact": glu.Mode.Exact}[mode]
     ctx = glu.glu.context()
     out = []
     for trials in (1, 0):
         ctx.set_trials(trials)
-        out.append(glu.joint_optimize(high, s, cfg))
+        out.append(glu.joint_optimize(high, s, cfg, md))
     ctx.set_trials(0)
     a, b = out
     assert a.trialsAccepted + a.trialsRejected > 10
