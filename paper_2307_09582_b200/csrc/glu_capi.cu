@@ -417,9 +417,9 @@ int glu_cu_joint_optimize(glu_ctx* ctx, const float* high, const glu_grid* g,
              "joint_optimize");
     SolveArgs a = solve_args(high, low, g, cfg, mode);
     a.params = field;
+    a.errOut = errors;  // self error map fused into the solve
     a.fallbacks = ctx->d_counters;
     GLU_CUDA(launch_solve(ctx, a), "joint_optimize");
-    GLU_CUDA(launch_self_error(ctx, high, field, npx_of(g), low, errors), "joint_optimize");
     glu_joint_stats st{0, 0, 0, 0};
     for (int it = 0; it < cfg->maxIterations; ++it) {
         size_t ncomp = 0;

@@ -57,6 +57,7 @@ struct SolveArgs {
     unsigned long long* fallbacks;
     unsigned sdiv;  // ceil(2^32 / s) when W, H < 2^16 (x / s = umulhi(x, sdiv)), else 0
     float epsf;     // (float)eps for the fp32 filter
+    float* errOut;  // optional: self reconstruction error per pixel (k_self_error fused)
 };
 
 // Launchers (return cudaError_t of the launch).

@@ -107,6 +107,12 @@ __global__ void __launch_bounds__(kSolveThreads) k_solve_tile(SolveArgs a) {
             a.out[C * p + c] = lerp_clamp(w, a.lowT[size_t(C) * ia + c], a.lowT[size_t(C) * ib + c],
                                           a.clamp != 0);
     }
+    if (a.errOut) {
+        float r[3];
+        for (int c = 0; c < 3; ++c)
+            r[c] = lerp_clamp(w, a.low[3 * size_t(ia) + c], a.low[3 * size_t(ib) + c], true);
+        a.errOut[p] = pixel_error(ip, r);
+    }
 }
 
 // optimize_pixels (upsample.cpp:218-233): one thread per listed pixel, window

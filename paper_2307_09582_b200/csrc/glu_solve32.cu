@@ -262,6 +262,14 @@ __global__ void __launch_bounds__(kThreads, GLU_SOLVE_MIN_BLOCKS)
         for (int k = 0; k < C; ++k)
             a.out[C * p + k] = lerp_clamp(w, __ldg(a.lowT + size_t(C) * ia + k),
                                           __ldg(a.lowT + size_t(C) * ib + k), a.clamp != 0);
+    }    if (a.errOut) {  // pixel_error of the clamped self reconstruction (jointopt.cpp:190)
+        float r[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            r[k] = lerp_clamp(w, __ldg(a.low + 3 * size_t(ia) + k), __ldg(a.low + 3 * size_t(ib) + k),
+                              true);
+        const float ipx[3] = {ip0, ip1, ip2};
+        a.errOut[p] = pixel_error(ipx, r);
     }
 }
 
