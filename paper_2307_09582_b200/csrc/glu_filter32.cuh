@@ -149,10 +149,14 @@ __device__ inline Filter32Result filter32_pixel(const float4 (&c)[9], const floa
         }
     }
     const float a3[3] = {ca.x, ca.y, ca.z}, b3[3] = {cb.x, cb.y, cb.z};
-    const double dA = dist64(ip, a3), dB = dist64(ip, b3);
+    bool wok = false;
+    r.w = weight_fast_verified(ip, a3, b3, eps, &wok);
+    if (!wok) {
+        const double dA = dist64(ip, a3), dB = dist64(ip, b3);
+        r.w = float(dB / (dA + dB + eps));
+    }
     r.ok = true;
     r.jb = jb;
-    r.w = float(dB / (dA + dB + eps));
     return r;
 }
 

@@ -70,6 +70,55 @@ GLU_HD double weight_fast64(const float* ip, const float* ia, const float* ib, d
     return db / (dist64(ip, ia) + db + eps);
 }
 
+#if defined(__CUDACC__)
+// float(weight_fast64(ip, ia, ib, eps)) without the IEEE sqrt / division
+// sequences (their special-case branches and slow paths are ~15 % of the
+// fp32 solve kernel's instructions).  The squared distances are the
+// reference's exact double sums; sqrt and the quotient come from the MUFU
+// double approximations refined by Newton / FMA residual steps, each within
+// 2 ulp of the correctly rounded value, so the double weight is within
+// 12 ulp of the reference's (da, db <= da + db, three more roundings).  The
+// float rounding of the reference's weight is therefore known unless the
+// estimate lies within 32 ulp of a float rounding midpoint: then *ok = false
+// and the caller evaluates weight_fast64 (probability ~2^-24 per pixel).
+__device__ __forceinline__ double sqrt_refined(double s) {
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(s));
+    const double hs = 0.5 * s;
+    r = r * __fma_rn(-(hs * r), r, 1.5);
+    r = r * __fma_rn(-(hs * r), r, 1.5);
+    const double y = s * r;
+    const double z = __fma_rn(__fma_rn(-y, y, s), 0.5 * r, y);
+    return s > 0.0 ? z : 0.0;
+}
+
+__device__ __forceinline__ float weight_fast_verified(const float* ip, const float* ia,
+                                                      const float* ib, double eps, bool* ok) {
+    const double da = sqrt_refined(dist2_64(ip, ia));
+    const double db = sqrt_refined(dist2_64(ip, ib));
+    const double den = (da + db) + eps;
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(den));
+    r = __fma_rn(r, __fma_rn(-den, r, 1.0), r);
+    r = __fma_rn(r, __fma_rn(-den, r, 1.0), r);
+    const double q0 = db * r;
+    const double wt = __fma_rn(__fma_rn(-den, q0, db), r, q0);
+    const float f = __double2float_rn(wt);
+    if (db == 0.0) {  // 0 / den: exactly 0 on both sides
+        *ok = true;
+        return f;
+    }
+    const unsigned fb = __float_as_uint(f);
+    const int E = int((fb >> 23) & 0xffu) - 127;
+    const double g = wt - double(f);  // exact: same binade up to a factor 2
+    // distance from f to the rounding midpoint on g's side
+    const int he = (g < 0.0 && (fb & 0x7fffffu) == 0u) ? E - 25 : E - 24;
+    const double half = __longlong_as_double((long long)(he + 1023) << 52);
+    *ok = E > -100 && fabs(g) + 0x1.0p-48 * wt < half;
+    return f;
+}
+#endif
+
 // Candidate access: any type whose operator[](i) returns candidate i's colour
 // (3 floats); candidates are indexed in the reference's raster list order.
 struct StridedCands {

@@ -72,6 +72,9 @@ __device__ __forceinline__ float fast_sqrt(float q) {
 // Exact reference weight for the chosen pair (upsample.cpp:28-33, 61).
 __device__ __forceinline__ float weight64(const float* ip, float4 ca, float4 cb, double eps) {
     const float a3[3] = {ca.x, ca.y, ca.z}, b3[3] = {cb.x, cb.y, cb.z};
+    bool ok = false;
+    const float w = weight_fast_verified(ip, a3, b3, eps, &ok);
+    if (ok) return w;
     const double da = dist64(ip, a3), db = dist64(ip, b3);
     return float(db / (da + db + eps));
 }
@@ -262,7 +265,8 @@ __global__ void __launch_bounds__(kThreads, GLU_SOLVE_MIN_BLOCKS)
         for (int k = 0; k < C; ++k)
             a.out[C * p + k] = lerp_clamp(w, __ldg(a.lowT + size_t(C) * ia + k),
                                           __ldg(a.lowT + size_t(C) * ib + k), a.clamp != 0);
-    }    if (a.errOut) {  // pixel_error of the clamped self reconstruction (jointopt.cpp:190)
+    }
+    if (a.errOut) {  // pixel_error of the clamped self reconstruction (jointopt.cpp:190)
         float r[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k)
