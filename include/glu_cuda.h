@@ -144,6 +144,13 @@ int glu_cu_optimize_pixels(glu_ctx* ctx, const float* high, const float* low,
 int glu_cu_apply_field(glu_ctx* ctx, const glu_pixel_params* field, const glu_grid* grid,
                        const float* lowTarget, int channels, int clampOutput, float* out);
 
+/* apply_field over a contiguous range of HR pixels (a row band of the field;
+ * multi-GPU C5): `bandField` / `out` hold `bandPixels`
+ * consecutive raster pixels whose params index the whole grid's LR target. */
+int glu_cu_apply_field_band(glu_ctx* ctx, const glu_pixel_params* bandField, size_t bandPixels,
+                            const glu_grid* grid, const float* lowTarget, int channels,
+                            int clampOutput, float* out);
+
 /* error_map + pixel_error (upsample.cpp:254-267, upsample.hpp:67-74). */
 int glu_cu_error_map(glu_ctx* ctx, const float* high, const float* recon, size_t pixelCount,
                      float* errors);

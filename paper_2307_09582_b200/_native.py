@@ -76,6 +76,7 @@ SIGNATURES: dict[str, tuple] = {
     "glu_cu_optimize_field": (I, [P, P, P, GP, CP, I, P]),
     "glu_cu_optimize_pixels": (I, [P, P, P, GP, CP, I, P, SZ, P]),
     "glu_cu_apply_field": (I, [P, P, GP, P, I, I, P]),
+    "glu_cu_apply_field_band": (I, [P, P, SZ, GP, P, I, I, P]),
     "glu_cu_error_map": (I, [P, P, P, SZ, P]),
     "glu_cu_self_error_map": (I, [P, P, P, GP, P, P]),
     "glu_cu_solve_apply": (I, [P, P, P, GP, CP, I, P, I, I, P, P]),

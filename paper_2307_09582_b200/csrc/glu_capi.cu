@@ -341,6 +341,20 @@ int glu_cu_apply_field(glu_ctx* ctx, const glu_pixel_params* field, const glu_gr
     return GLU_OK;
 }
 
+int glu_cu_apply_field_band(glu_ctx* ctx, const glu_pixel_params* bandField, size_t bandPixels,
+                            const glu_grid* g, const float* lowTarget, int channels,
+                            int clampOutput, float* out) {
+    if (!ctx) return einval("ctx must not be null");
+    GLU_TRY(check_grid(g));
+    if (channels != 1 && channels != 3) return einval("apply_field: channels must be 1 or 3");
+    if (bandPixels > npx_of(g)) return einval("apply_field: band exceeds the grid");
+    if (bandPixels == 0) return GLU_OK;
+    GLU_CUDA(launch_apply(ctx, bandField, bandPixels, lowTarget, lown_of(g), channels,
+                          clampOutput, out),
+             "apply_field");
+    return GLU_OK;
+}
+
 int glu_cu_error_map(glu_ctx* ctx, const float* high, const float* recon, size_t n,
                      float* errors) {
     if (!ctx) return einval("ctx must not be null");

@@ -123,7 +123,11 @@ __global__ void __launch_bounds__(kThreads, GLU_SOLVE_MIN_BLOCKS)
     forceFallback |= int(__ldg(nanFlag));
     constexpr int N = S * S;
     constexpr int h = S / 2;
+#ifdef GLU_S3_RELOAD
+    constexpr int NE = 1;
+#else
     constexpr int NE = S == 3 ? N : 1;  // S = 3 keeps e_j in registers; S = 5 reloads
+#endif
     const int pw = a.lw + 2 * h;
     // 32 x 4 pixel tiles: a warp covers 32 consecutive pixels of one row
     const int x = blockIdx.x * 32 + (threadIdx.x & 31);
@@ -144,7 +148,7 @@ __global__ void __launch_bounds__(kThreads, GLU_SOLVE_MIN_BLOCKS)
     for (int j = 0; j < N; ++j) {
         const float4 v = cand<S>(win, pw, j);
         const float d0 = v.x - ip0, d1 = v.y - ip1, d2 = v.z - ip2;
-        if (S == 3) {
+        if (NE == N) {
             e0[j % NE] = d0;
             e1[j % NE] = d1;
             e2[j % NE] = d2;
@@ -177,7 +181,7 @@ __global__ void __launch_bounds__(kThreads, GLU_SOLVE_MIN_BLOCKS)
 #pragma unroll
         for (int j = 0; j < N; ++j) {
             float d0, d1, d2;
-            if (S == 3) {
+            if (NE == N) {
                 d0 = e0[j % NE];
                 d1 = e1[j % NE];
                 d2 = e2[j % NE];

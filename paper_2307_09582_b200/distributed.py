@@ -17,8 +17,10 @@ Level-synchronous, replicated-state decomposition of joint_optimize
 * the sweep's accept / reject counts are summed across ranks; the loop stops
   exactly where the reference stops.
 
-On the C4 scene a sweep has 15 levels (C2: 8), so a sweep costs ~45 small
-all-gathers.  `joint_optimize_local` runs W ranks inside one process on one
+The first sweep of the C4 scene has 122 levels (C2: 159: chains of nearby
+components), so a sweep costs a few hundred small all-gathers; on one GPU the
+dataflow scheduler (glu_joint.cu k_trial_sched) is faster than any level
+schedule, and this module is the multi-rank decomposition.  `joint_optimize_local` runs W ranks inside one process on one
 device (what the tests use: one GPU is available); `joint_optimize_distributed`
 uses torch.distributed (NCCL for CUDA tensors, gloo via host staging).
 """

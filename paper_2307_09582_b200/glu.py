@@ -303,6 +303,28 @@ def apply_field(field: ParamField, lowTarget: torch.Tensor, clampOutput: bool = 
     return out
 
 
+def apply_field_band(bandParams: torch.Tensor, grid: GridSpec, lowTarget: torch.Tensor,
+                     clampOutput: bool = True, out: torch.Tensor | None = None) -> torch.Tensor:
+    """apply_field over a row band (multi-GPU C5): `bandParams` is a
+    (rows, W, 3) int32 slice of a field of `grid`, indexing the whole LR
+    target; returns (rows, W[, 3])."""
+    ch = 1 if lowTarget.dim() == 2 else lowTarget.shape[2]
+    if lowTarget.shape[1] != grid.lowW or lowTarget.shape[0] != grid.lowH or ch not in (1, 3):
+        raise ValueError("apply_field: low-res image does not match grid")
+    if bandParams.dim() != 3 or bandParams.shape[1] != grid.highW or bandParams.shape[2] != 3:
+        raise ValueError("apply_field: band does not match grid")
+    bandParams, lowTarget = bandParams.contiguous(), lowTarget.contiguous()
+    rows = bandParams.shape[0]
+    shape = (rows, grid.highW, 3) if ch == 3 else (rows, grid.highW)
+    if out is None:
+        out = torch.empty(shape, dtype=torch.float32, device=lowTarget.device)
+    ctx = context(lowTarget.device.index)
+    N.check(N.lib().glu_cu_apply_field_band(ctx.handle, _ptr(bandParams), rows * grid.highW,
+                                            C.byref(grid.c()), _ptr(lowTarget), ch,
+                                            int(bool(clampOutput)), _ptr(out)))
+    return out
+
+
 def error_map(high: torch.Tensor, reconstructed: torch.Tensor) -> torch.Tensor:
     """error_map (upsample.cpp:254-267)."""
     if high.shape != reconstructed.shape:

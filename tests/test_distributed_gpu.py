@@ -53,3 +53,23 @@ def test_levels_are_independent_sets(glu):
                     bx[i, 1] - bx[j, 3])
             if d <= 2:
                 assert lv[i] > lv[j]
+
+
+@pytest.mark.parametrize("world,channels", [(2, 3), (8, 3), (3, 1)])
+def test_banded_apply_tiles_full_apply(glu, world, channels):
+    """C5 row bands: per-band applies of a field through
+    glu_cu_apply_field_band concatenate to the single-GPU apply, bit for bit."""
+    from paper_2307_09582_b200 import banded, workloads
+    W, H, s = 640, 480, 16
+    high = torch.from_numpy(workloads.scene(W, H, 5)).cuda()
+    low, grid = glu.grid_downsample(high, s)
+    field = glu.optimize_field(high, low, grid)
+    target = glu.op_color(low, workloads.mix_op(1005).M)
+    if channels == 1:
+        target = glu.op_matte(target)
+    full = glu.apply_field(field, target)
+    parts = []
+    for r in range(world):
+        y0, y1 = banded.band_rows(grid, 3, world, r)
+        parts.append(glu.glu.apply_field_band(field.params[y0:y1], grid, target))
+    assert torch.equal(torch.cat(parts), full)

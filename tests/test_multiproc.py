@@ -116,3 +116,62 @@ def test_two_rank_change_log_exchange():
     for r in (0, 1):
         assert res[r][0] == want
         assert res[r][1] == [3, 10]
+
+
+def _banded_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import numpy as np
+
+        import oracle
+        from paper_2307_09582_b200 import banded
+        from paper_2307_09582_b200.glu import GridSpec
+        g = GridSpec.create(40, 48, 8)
+        rng = np.random.default_rng(7)
+        lown = g.lowW * g.lowH
+        full = np.zeros((g.highH, g.highW, 3), np.int32)
+        full[..., 0] = rng.integers(0, lown, (g.highH, g.highW))
+        full[..., 1] = rng.integers(0, lown, (g.highH, g.highW))
+        full[..., 2] = rng.uniform(-0.2, 1.2, (g.highH, g.highW)).astype(np.float32).view(np.int32)
+        targets = [torch.from_numpy(rng.uniform(-0.1, 1.1, (g.lowH, g.lowW, 3)).astype(np.float32))
+                   for _ in range(3)]
+        y0, y1 = banded.band_rows(g, 3, world, rank)
+        ora = oracle.Oracle()
+
+        def ora_apply(p, grid, t, clamp):
+            P = np.ascontiguousarray(p.numpy()).view(oracle.PARAMS_DTYPE).reshape(p.shape[0], -1)
+            return torch.from_numpy(ora.apply_field(P, t.numpy().copy(), clamp))
+
+        outs = {}
+        banded.run_banded_apply(torch.from_numpy(full[y0:y1].copy()), g,
+                                targets if rank == 0 else None, 3, apply=ora_apply,
+                                sink=lambda k, o: outs.__setitem__(k, o.clone()))
+        got = [None] * world
+        dist.all_gather_object(got, (y0, y1, [outs[k].numpy() for k in range(3)]))
+        ok = True
+        if rank == 0:
+            P = full.view(oracle.PARAMS_DTYPE).reshape(g.highH, g.highW)
+            for k in range(3):
+                want = ora.apply_field(P, targets[k].numpy())
+                cat = np.concatenate([o[2][k] for o in sorted(got, key=lambda o: o[0])])
+                ok &= cat.tobytes() == want.tobytes()
+            ok &= [o[0] for o in sorted(got)] == [0] + [o[1] for o in sorted(got)][:-1]
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_banded_apply_matches_full_apply():
+    """C5 over row bands: broadcast targets, per-band apply, outputs tile the frame."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_banded_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = dict(q.get(timeout=10) for _ in range(2))
+    assert res == {0: True, 1: True}
