@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(kThreads, GLU_SOLVE_MIN_BLOCKS)
     }
     int jb = ja;
     float w = 1.0f;
+    bool wExact = false;  // w already settled in double (close-set path)
     if (MODE == GLU_MODE_FAST && ok) {
         // ---- stage B: b = first argmin of the objective at w_j --------------
         const float da = fast_sqrt(m1);
@@ -218,7 +219,12 @@ __global__ void __launch_bounds__(kThreads, GLU_SOLVE_MIN_BLOCKS)
             const float alpha = 1.0f - kU * (0.5f * kC1 * smax * rt + kC2);
             const float rhs = b1 + mb + kU * (0.5f * kC1 * smax * st + kC3 * eps);
             if (b2 * alpha <= rhs || alpha <= 0.0f) {
-                // rare: recompute the objectives and compare colours
+                // rare: recompute the objectives; the close set (candidates
+                // within the bound of the best) holds the reference's first
+                // argmin.  All of the winner's colour: done; else settle the
+                // set in double, in index order (off-grid members: exact path).
+                unsigned close = 1u << jb;
+                bool mixed = false;
                 for (int j = 0; j < N; ++j) {
                     if (j == jb) continue;
                     const float4 v = cand<S>(win, pw, j);
@@ -230,11 +236,38 @@ __global__ void __launch_bounds__(kThreads, GLU_SOLVE_MIN_BLOCKS)
                     const float v2 = __fmaf_rn(wj, ea2 - d2, d2);
                     const float o = __fmaf_rn(eps * wj, wj,
                                               __fmaf_rn(v2, v2, __fmaf_rn(v1, v1, v0 * v0)));
-                    if ((o * alpha <= rhs || alpha <= 0.0f) && !same_rgb(v, cb)) ok = false;
+                    if (o * alpha <= rhs || alpha <= 0.0f) {
+                        if (!(q[j] < kInf)) ok = false;
+                        close |= 1u << j;
+                        mixed |= !same_rgb(v, cb);
+                    }
+                }
+                if (ok && mixed) {
+                    const float ip[3] = {ip0, ip1, ip2};
+                    const float a3[3] = {ca.x, ca.y, ca.z};
+                    const double dA = dist64(ip, a3);
+                    double best = 0, bw = 0;
+                    int bj = -1;
+                    for (int j = 0; j < N; ++j) {
+                        if (!(close >> j & 1u)) continue;
+                        const float4 v = cand<S>(win, pw, j);
+                        const float cj[3] = {v.x, v.y, v.z};
+                        const double dj = dist64(ip, cj);
+                        const double wj = dj / (dA + dj + a.eps);
+                        const double o = objective64(ip, a3, cj, wj, a.eps);
+                        if (bj < 0 || o < best) {
+                            best = o;
+                            bw = wj;
+                            bj = j;
+                        }
+                    }
+                    jb = bj;
+                    w = float(bw);
+                    wExact = true;
                 }
             }
         }
-        if (ok) {
+        if (ok && !wExact) {
             const float ip[3] = {ip0, ip1, ip2};
             w = weight64(ip, ca, cb, a.eps);
         }
