@@ -110,8 +110,12 @@ enum glu_option { GLU_OPT_SOLVER = 1, GLU_OPT_TRIALS = 2 };
 int glu_ctx_set_option(glu_ctx* ctx, int option, int value);
 /* Number of kernels this context has launched (bench.py's gpu_launches). */
 unsigned long long glu_ctx_launch_count(glu_ctx* ctx);
-/* Pixels the last solve/joint call re-evaluated on the exact fp64 path. */
+/* Pixels this context's solves re-evaluated on the exact fp64 path
+ * (cumulative). */
 unsigned long long glu_ctx_fallback_count(glu_ctx* ctx);
+/* Pixels whose fp32 near-tie was settled in double over the close set only
+ * (cumulative; diagnostics for the fp32 filter). */
+unsigned long long glu_ctx_close_set_count(glu_ctx* ctx);
 
 /* ---- device-pointer entry points (async on the context stream) ---------- */
 

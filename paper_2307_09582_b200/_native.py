@@ -67,6 +67,7 @@ SIGNATURES: dict[str, tuple] = {
     "glu_ctx_synchronize": (I, [P]),
     "glu_ctx_launch_count": (U64, [P]),
     "glu_ctx_fallback_count": (U64, [P]),
+    "glu_ctx_close_set_count": (U64, [P]),
     "glu_cu_copy": (I, [P, P, P, SZ]),
     "glu_cu_alloc": (I, [P, C.POINTER(P), SZ]),
     "glu_cu_free": (I, [P, P]),

@@ -260,6 +260,13 @@ unsigned long long glu_ctx_fallback_count(glu_ctx* ctx) {
     return v;
 }
 
+unsigned long long glu_ctx_close_set_count(glu_ctx* ctx) {
+    if (!ctx) return 0;
+    unsigned long long v = 0;
+    cudaMemcpy(&v, ctx->d_counters + 1, sizeof(v), cudaMemcpyDeviceToHost);
+    return v;
+}
+
 // ---- device entry points ------------------------------------------------------
 
 int glu_cu_copy(glu_ctx* ctx, void* dst, const void* src, size_t bytes) {

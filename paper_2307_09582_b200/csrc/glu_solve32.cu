@@ -264,6 +264,7 @@ __global__ void __launch_bounds__(kThreads, GLU_SOLVE_MIN_BLOCKS)
                     jb = bj;
                     w = float(bw);
                     wExact = true;
+                    if (a.fallbacks) atomicAdd(a.fallbacks + 1, 1ull);
                 }
             }
         }

@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_solve32x(SolveArgs a, const flo
                 ip2 = __ldg(a.high + 3 * p + 2);
 
     float e0[9], e1[9], e2[9], q[9];
-    float qmax = 0.0f, qmin = kInf;
+    float qmin = kInf;
 #pragma unroll
     for (int k = 0; k < 9; ++k) {
         const float4 v = __ldg(win + (k / 3) * pw + k % 3);
@@ -110,11 +110,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_solve32x(SolveArgs a, const flo
         e1[k] = v.y - ip1;
         e2[k] = v.z - ip2;
         q[k] = __fmaf_rn(e2[k], e2[k], __fmaf_rn(e1[k], e1[k], __fmul_rn(e0[k], e0[k])));
-        qmax = fmaxf(qmax, q[k] < kInf ? q[k] : 0.0f);
         qmin = fminf(qmin, q[k]);
     }
-    // lexicographic scan over (i <= j), first strict argmin + second best
-    float b1 = kInf, b2 = kInf;
+    // lexicographic scan over (i <= j), first strict argmin.  Alongside, m2
+    // = min over the other pairs of (o - E), E = the pair's error bound
+    // (kCE u q_j), and eb = the best pair's bound: a close call exists only
+    // if m2 <= b1 + eb, so the per-pair re-check below runs just for those.
+    float qe[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) qe[k] = __fmaf_rn(kCE * kU, q[k], 1e-36f);
+    float b1 = kInf, m2 = kInf, eb = 0.0f;
     int bi = 0, bj = 0;
     {
         int pr = 0;
@@ -123,7 +128,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_solve32x(SolveArgs a, const flo
             {
                 const float o = q[i];  // (i, i): w = 0
                 const bool lt = o < b1;
-                b2 = lt ? b1 : fminf(b2, o);
+                m2 = lt ? fminf(m2, b1 - eb) : fminf(m2, o - qe[i]);
+                eb = lt ? qe[i] : eb;
                 b1 = lt ? o : b1;
                 bi = lt ? i : bi;
                 bj = lt ? i : bj;
@@ -134,7 +140,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_solve32x(SolveArgs a, const flo
                 const float num = -__fmaf_rn(e0[j], t.x, __fmaf_rn(e1[j], t.y, e2[j] * t.z));
                 const float o = __fmaf_rn(-num * num, t.w, q[j]);
                 const bool lt = o < b1;
-                b2 = lt ? b1 : fminf(b2, o);
+                m2 = lt ? fminf(m2, b1 - eb) : fminf(m2, o - qe[j]);
+                eb = lt ? qe[j] : eb;
                 b1 = lt ? o : b1;
                 bi = lt ? i : bi;
                 bj = lt ? j : bj;
@@ -144,20 +151,25 @@ __global__ void __launch_bounds__(kThreads, 2) k_solve32x(SolveArgs a, const flo
     const float4 ci = __ldg(win + (bi / 3) * pw + bi % 3), cj = __ldg(win + (bj / 3) * pw + bj % 3);
     bool ok = !forceFallback && b1 < kInf && ip0 == ip0 && ip1 == ip1 && ip2 == ip2 &&
               (qmin >= 1e-27f || qmin == 0.0f);
-    const float M = kCE * kU * qmax + 1e-36f;
     // An exact zero with I_bj == I_p is exact in double too (w = 0, v = 0);
     // every other true zero also has e_j = 0 and evaluates to exactly 0 in
     // fp32, so the first zero in lexicographic order is the reference's pick.
     // (Every LR sample pixel lands here: all pairs (i, k) with I_k = I_p tie.)
     const bool exactZero = b1 == 0.0f && cj.x == ip0 && cj.y == ip1 && cj.z == ip2;
-    if (ok && !exactZero && b2 <= b1 + 2.0f * M) {
-        // rare: per-pair bounds; a close pair must have the winner's colours
-        const float mb = kCE * kU * q[bj] + 1e-36f;
-        int pr = 0;
+    bool wSet = false;  // w settled in double over the close set
+    float wClose = 0.0f;
+    if (ok && !exactZero && m2 <= b1 + eb) {
+        // rare: per-pair bounds.  The close pairs (bit k = lexicographic pair
+        // k, the winner included) hold the reference's first argmin: if they
+        // all carry the winner's colours the fp32 pick stands; otherwise they
+        // are evaluated in double, in lexicographic order.
+        unsigned long long close = 0;
+        bool mixed = false;
+        int pr = 0, k = 0;
 #pragma unroll
         for (int i = 0; i < 9; ++i) {
 #pragma unroll
-            for (int j = i; j < 9; ++j) {
+            for (int j = i; j < 9; ++j, ++k) {
                 float o;
                 if (j == i) {
                     o = q[i];
@@ -166,14 +178,47 @@ __global__ void __launch_bounds__(kThreads, 2) k_solve32x(SolveArgs a, const flo
                     const float num = -__fmaf_rn(e0[j], t.x, __fmaf_rn(e1[j], t.y, e2[j] * t.z));
                     o = __fmaf_rn(-num * num, t.w, q[j]);
                 }
-                if (i == bi && j == bj) continue;
+                if (i == bi && j == bj) {
+                    close |= 1ull << k;
+                    continue;
+                }
                 if (!(o <= kInf)) continue;  // NaN: outside the grid
-                if (o - (kCE * kU * q[j] + 1e-36f) <= b1 + mb) {
+                if (o - qe[j] <= b1 + eb) {
                     const float4 vi = __ldg(win + (i / 3) * pw + i % 3);
                     const float4 vj = __ldg(win + (j / 3) * pw + j % 3);
-                    if (!(same_rgb(vi, ci) && same_rgb(vj, cj))) ok = false;
+                    if (!(q[i] < kInf && q[j] < kInf)) ok = false;  // off-grid member
+                    close |= 1ull << k;
+                    mixed |= !(same_rgb(vi, ci) && same_rgb(vj, cj));
                 }
             }
+        }
+        if (ok && mixed) {
+            const float ip[3] = {ip0, ip1, ip2};
+            double best = 0, bw = 0;
+            int ni = -1, nj = -1;
+            int i = 0, j = 0;
+#pragma unroll 1
+            for (int kk = 0; kk < 45; ++kk) {
+                if (close >> kk & 1ull) {
+                    const float4 vi = __ldg(win + (i / 3) * pw + i % 3);
+                    const float4 vj = __ldg(win + (j / 3) * pw + j % 3);
+                    const float a3[3] = {vi.x, vi.y, vi.z}, b3[3] = {vj.x, vj.y, vj.z};
+                    const double wv = weight_exact64(ip, a3, b3, a.eps);
+                    const double o = objective64(ip, a3, b3, wv, a.eps);
+                    if (ni < 0 || o < best) {
+                        best = o;
+                        bw = wv;
+                        ni = i;
+                        nj = j;
+                    }
+                }
+                if (++j == 9) j = ++i;
+            }
+            bi = ni;
+            bj = nj;
+            wClose = float(bw);
+            wSet = true;
+            if (a.fallbacks) atomicAdd(a.fallbacks + 1, 1ull);
         }
     }
     // stage-A style guard: an exact-zero distance must be a true colour match
@@ -189,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_solve32x(SolveArgs a, const flo
         ib = uint32_t(cy - 1 + bj / 3) * uint32_t(a.lw) + uint32_t(cx - 1 + bj % 3);
         const float ip[3] = {ip0, ip1, ip2};
         const float a3[3] = {ci.x, ci.y, ci.z}, b3[3] = {cj.x, cj.y, cj.z};
-        w = float(weight_exact64(ip, a3, b3, a.eps));
+        w = wSet ? wClose : float(weight_exact64(ip, a3, b3, a.eps));
     } else {
         const int wx0 = max(0, cx - 1), wy0 = max(0, cy - 1);
         const int nwx = min(a.lw - 1, cx + 1) - wx0 + 1;

@@ -184,6 +184,11 @@ class Context:
     def fallbacks(self) -> int:
         return int(N.lib().glu_ctx_fallback_count(self.handle))
 
+    @property
+    def close_sets(self) -> int:
+        """Pixels whose near-tie was settled in double over the close set."""
+        return int(N.lib().glu_ctx_close_set_count(self.handle))
+
     def __del__(self):
         try:
             if getattr(self, "handle", None):

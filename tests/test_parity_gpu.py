@@ -256,6 +256,7 @@ def _stress_images():
 @pytest.mark.parametrize("S", [3, 5])
 def test_fp32_filter_matches_oracle_on_stress_images(glu, oracle, mode, S):
     ctx = glu.glu.context()
+    close0 = ctx.close_sets
     for name, img in _stress_images():
         for s in (4, 8):
             high = dev(img)
@@ -268,6 +269,9 @@ def test_fp32_filter_matches_oracle_on_stress_images(glu, oracle, mode, S):
                 got = host_params(f.params)
                 ctx.set_solver(0)
                 assert same(got, want), (name, s, solver, int((got != want).sum()))
+    if mode in ("fast", "exact") and S == 3:
+        # the near-tie close-set path (settled in double) ran and stayed exact
+        assert ctx.close_sets > close0
 
 
 def test_reference_unit_tests_pass_against_dropin_api(glu):
