@@ -683,7 +683,6 @@ __device__ __forceinline__ uint32_t affected_pixel(const TrialState& t, const Tr
 struct PixIn {
     uint32_t p;
     int cx, cy;
-    glu_pixel_params op;
     float oe, i0, i1, i2;
 };
 
@@ -737,12 +736,7 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
             ss.old[3 * slot] = wc.x;
             ss.old[3 * slot + 1] = wc.y;
             ss.old[3 * slot + 2] = wc.z;
-            const float c0 = bc.x, c1 = bc.y, c2 = bc.z;
-            wc = bc;
-            float* lc = t.low + 3 * (size_t(qy) * t.lw + qx);
-            lc[0] = c0;
-            lc[1] = c1;
-            lc[2] = c2;
+            wc = bc;  // global LR written at commit
         }
         nt += total;
         __syncthreads();
@@ -782,7 +776,6 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
     auto load = [&](uint32_t i) {
         PixIn q;
         q.p = affected_pixel(t, g, ss, i, q.cx, q.cy);
-        q.op = t.field[q.p];
         q.oe = t.errors[q.p];
         q.i0 = t.high[3 * size_t(q.p)];
         q.i1 = t.high[3 * size_t(q.p) + 1];
@@ -791,7 +784,7 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
     };
     PixIn cur{};
     if (uint32_t(tid) < na) cur = load(tid);
-    {
+    if (sc.list) {
         // conflicting successors among the next NT trials, while loads fly
         const int j = sc.self + 1 + tid;
         if (j < sc.ncomp && boxes_conflict(sc.box, sc.boxes[j], sc.reach))
@@ -806,10 +799,7 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
         if (i + NT < na) nxt = load(i + NT);
         const uint32_t p = cur.p;
         const int cx = cur.cx, cy = cur.cy;
-        const glu_pixel_params op = cur.op;
         const float oe = cur.oe;
-        b.bkParams[i] = op;
-        b.bkE[i] = oe;
         part0 += double(oe);
         const float ip[3] = {cur.i0, cur.i1, cur.i2};
         const int x0 = max(0, cx - h), y0 = max(0, cy - h);
@@ -866,13 +856,14 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
         np.a = uint32_t(ay) * uint32_t(t.lw) + uint32_t(ax);
         np.b = uint32_t(by) * uint32_t(t.lw) + uint32_t(bx);
         np.w = w;
-        t.field[p] = np;
+        b.bkParams[i] = np;  // the trial's new state, written back at commit
         const float4 la = ss.win[(ay - g.vy0) * g.vw + (ax - g.vx0)];
         const float4 lb = ss.win[(by - g.vy0) * g.vw + (bx - g.vx0)];
         const float r[3] = {lerp_clamp(w, la.x, lb.x, true), lerp_clamp(w, la.y, lb.y, true),
                             lerp_clamp(w, la.z, lb.z, true)};
         const float e = pixel_error(ip, r);
-        t.errors[p] = e;
+        b.bkE[i] = e;
+        (void)p;
         changed |= __float_as_uint(e) != __float_as_uint(oe);
         part1 += double(e);
         cur = nxt;
@@ -912,8 +903,8 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
             const uint32_t m = min(kChunk, na - c0);
             for (uint32_t k = tid; k < m; k += NT) {
                 int cx, cy;
-                stage[2 * k] = b.bkE[c0 + k];
-                stage[2 * k + 1] = t.errors[affected_pixel(t, g, ss, c0 + k, cx, cy)];
+                stage[2 * k] = t.errors[affected_pixel(t, g, ss, c0 + k, cx, cy)];
+                stage[2 * k + 1] = b.bkE[c0 + k];
             }
             __syncthreads();
             if (tid == 0)
@@ -930,8 +921,42 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
         __syncthreads();
     }
     const int verdict = sm.verdict;
+    if (tid == 0) {
+        sm.touched = nt;
+        sm.base = na;
+    }
+    __syncthreads();
     GLU_PHASE(5)
-    if (t.dCount && verdict) {
+    return verdict;
+}
+
+// Commit an accepted on-chip trial: the replaced LR cells, then the new params
+// and errors of the affected pixels (a rejected trial wrote nothing: no
+// rollback, jointopt.cpp:169-179 is implicit), plus the change log.
+template <int NT>
+__device__ void commit_trial_smem(const TrialState& t, const TrialBuffers& b, TrialSmem<NT>& sm,
+                                  const TrialShared& ss, const TrialGeom& g) {
+    const int tid = threadIdx.x;
+    const uint32_t nt = sm.touched, na = sm.base;
+#ifdef GLU_SCHED_TRACE
+    long long tph = clock64();
+#endif
+    for (uint32_t i = tid; i < nt; i += NT) {
+        const int k = int(ss.touched[i]);
+        const int qx = g.qx0 + k % g.qw, qy = g.qy0 + k / g.qw;
+        const float4 c = ss.win[(qy - g.vy0) * g.vw + (qx - g.vx0)];
+        float* lc = t.low + 3 * (size_t(qy) * t.lw + qx);
+        lc[0] = c.x;
+        lc[1] = c.y;
+        lc[2] = c.z;
+    }
+    for (uint32_t i = tid; i < na; i += NT) {
+        int cx, cy;
+        const uint32_t p = affected_pixel(t, g, ss, i, cx, cy);
+        t.field[p] = b.bkParams[i];
+        t.errors[p] = b.bkE[i];
+    }
+    if (t.dCount) {
         if (tid == 0) {
             sm.logCells = atomicAdd(t.dCount, nt);
             sm.logPixels = atomicAdd(t.dCount + 1, na);
@@ -956,35 +981,17 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
                 int cx, cy;
                 const uint32_t p = affected_pixel(t, g, ss, i, cx, cy);
                 uint32_t* o = t.dPixels + 5 * size_t(sm.logPixels + i);
-                const glu_pixel_params pp = t.field[p];
+                const glu_pixel_params pp = b.bkParams[i];
                 o[0] = p;
                 o[1] = pp.a;
                 o[2] = pp.b;
                 o[3] = __float_as_uint(pp.w);
-                o[4] = __float_as_uint(t.errors[p]);
+                o[4] = __float_as_uint(b.bkE[i]);
             }
-        }
-    }
-    GLU_PHASE(6)
-    // E. rollback (jointopt.cpp:169-179); nothing global to reset
-    if (!verdict) {
-        for (uint32_t i = tid; i < na; i += NT) {
-            int cx, cy;
-            const uint32_t p = affected_pixel(t, g, ss, i, cx, cy);
-            t.field[p] = b.bkParams[i];
-            t.errors[p] = b.bkE[i];
-        }
-        for (uint32_t i = tid; i < nt; i += NT) {
-            const int k = int(ss.touched[i]);
-            float* lc = t.low + 3 * (size_t(g.qy0 + k / g.qw) * t.lw + g.qx0 + k % g.qw);
-            lc[0] = ss.old[3 * i];
-            lc[1] = ss.old[3 * i + 1];
-            lc[2] = ss.old[3 * i + 2];
         }
     }
     __syncthreads();
     GLU_PHASE(7)
-    return verdict;
 }
 
 // Sequential sweep: one CTA runs the components in order (used for single
@@ -1179,13 +1186,14 @@ __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
         if (onChip) {
             const SuccScan sc{boxes, sufTop, ncomp, reach, i, bi, sList, &sCount, &sMore};
             v = run_trial_smem<kSchedThreads>(t, local, sm, ss, geo, px + off[c], n, sc);
+            if (v) commit_trial_smem<kSchedThreads>(t, local, sm, ss, geo);
         } else {
             v = run_trial<kSchedThreads>(t, isBig ? big : local, sm, px + off[c], n);
         }
         if (threadIdx.x == 0) {
             atomicAdd(t.result + (v ? 0 : 1), 1);
 #ifdef GLU_SCHED_TRACE
-            g_trace[3 * i + 2] = gtimer();
+            g_trace[3 * i + 2] = (gtimer() & ~1ull) | unsigned(v != 0);  // LSB: verdict
 #endif
         }
 #ifdef GLU_SCHED_TRACE

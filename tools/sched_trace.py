@@ -62,11 +62,20 @@ def show(path, reach=2):
             dep = np.maximum(dx, dy) <= reach
             fin[i] = runt[i] + (fin[:i][dep].max() if dep.any() else 0.0)
             depth[i] = 1 + (depth[:i][dep].max() if dep.any() else 0)
+        # speculation bound: only accepted predecessors order a trial
+        acc = (st[:, 2] & 1).astype(bool)
+        fin2 = np.zeros(n)
+        for i in range(n):
+            dx = np.maximum(0, np.maximum(bx[:i, 0] - bx[i, 2], bx[i, 0] - bx[:i, 2]))
+            dy = np.maximum(0, np.maximum(bx[:i, 1] - bx[i, 3], bx[i, 1] - bx[:i, 3]))
+            dep = (np.maximum(dx, dy) <= reach) & acc[:i]
+            fin2[i] = runt[i] + (fin2[:i][dep].max() if dep.any() else 0.0)
         span = (st[:, 2].max() - t0) / 1e3
         print(f"launch {k}: {n} trials, span {span:.0f} us, run mean {runt.mean():.1f} "
               f"p50 {np.median(runt):.1f} max {runt.max():.1f} us, wait mean {wait.mean():.1f} us, "
               f"sum run {runt.sum():.0f} us, critical path {fin.max():.0f} us "
-              f"({depth.max()} trials deep)")
+              f"({depth.max()} trials deep); accepted {acc.sum()}, critical path through "
+              f"accepted predecessors only {fin2.max():.0f} us")
         # claim timeline: when did the last trial get claimed / become ready
         print(f"   last claim at {(st[:, 0].max() - t0) / 1e3:.0f} us, "
               f"last ready at {(st[:, 1].max() - t0) / 1e3:.0f} us")
