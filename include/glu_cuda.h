@@ -103,8 +103,11 @@ int glu_ctx_synchronize(glu_ctx* ctx);
  *   1 the fp64 reference-order kernel everywhere;
  *   2 fp32 filter with every pixel forced through the fp64 verify (testing).
  * GLU_OPT_TRIALS selects the joint-loop trial schedule:
- *   0 (default) conflict-aware parallel schedule over all SMs;
- *   1 one CTA runs the trials in sweep order.
+ *   0 (default) speculative parallel schedule over all SMs (trials start at
+ *     once, commit in conflict order, re-run if an overlapping earlier trial
+ *     was accepted meanwhile);
+ *   1 one CTA runs the trials in sweep order;
+ *   2 dependency-counting dataflow schedule over all SMs.
  * All settings produce bit-identical results. */
 enum glu_option { GLU_OPT_SOLVER = 1, GLU_OPT_TRIALS = 2 };
 int glu_ctx_set_option(glu_ctx* ctx, int option, int value);

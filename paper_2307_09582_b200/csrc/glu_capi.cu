@@ -238,7 +238,7 @@ int glu_ctx_set_option(glu_ctx* ctx, int option, int value) {
         return GLU_OK;
     }
     if (option == GLU_OPT_TRIALS) {
-        if (value < 0 || value > 1) return einval("GLU_OPT_TRIALS: value must be 0 or 1");
+        if (value < 0 || value > 2) return einval("GLU_OPT_TRIALS: value must be 0, 1 or 2");
         ctx->trials = value;
         return GLU_OK;
     }

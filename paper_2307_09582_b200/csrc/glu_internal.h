@@ -14,7 +14,7 @@ struct glu_ctx {
     unsigned long long launches = 0;
     unsigned long long* d_counters = nullptr;  // [0] = fp64 fallback pixels
     // Grow-only scratch slots (device memory).
-    static constexpr int kSlots = 20;
+    static constexpr int kSlots = 24;
     void* buf[kSlots] = {};
     size_t cap[kSlots] = {};
     // Grow-only pinned host slots.
@@ -23,7 +23,8 @@ struct glu_ctx {
     // GLU_OPT_SOLVER: 0 auto, 1 fp64 reference-order kernel only, 2 fp32
     // filter with every pixel forced through the fp64 verify path (testing).
     int solver = 0;
-    // GLU_OPT_TRIALS: 0 conflict-aware parallel schedule, 1 one CTA in order.
+    // GLU_OPT_TRIALS: 0 speculative parallel schedule, 1 one CTA in order,
+    // 2 dependency-counting dataflow schedule (literal scope always uses 2).
     int trials = 0;
     // Copy streams + events of the host frame pipeline (created lazily).
     cudaStream_t h2d = nullptr, d2h = nullptr;
@@ -36,7 +37,7 @@ namespace glu_cu {
 enum Slot {
     S_HIGH = 0, S_LOW, S_PARAMS, S_OUT, S_ERR, S_AUX, S_PIX,
     S_CCL_LABEL, S_CCL_LIST, S_CCL_OFF, S_CCL_MISC, S_TRIAL, S_TRIAL2, S_TRIAL3,
-    S_SPARE1, S_SPARE2, S_PACKED, S_SCHED, S_SCHED_META
+    S_SPARE1, S_SPARE2, S_PACKED, S_SCHED, S_SCHED_META, S_PARK, S_PARK_TMP
 };
 
 void set_error(const std::string& msg);

@@ -557,6 +557,7 @@ constexpr int kSQ = 2048;  // cells of the component's box
 constexpr int kSW = 4096;  // cells of the box dilated by 2h
 constexpr int kSC = 2048;  // pixels of the component
 constexpr int kSS = 512;   // successors found by the early scan (= the CTA size)
+constexpr uint32_t kParkWords = 128u << 20;  // speculative-record arena (512 MB)
 constexpr size_t kTrialSmemBytes = size_t(kSQ) * 8 + size_t(kSW) * 16 + size_t(kSC) * 16 +
                                    size_t(kSW + 1) * 4 + size_t(kSW) * 4 + size_t(kSQ) * 4 +
                                    size_t(kSQ) * 12;
@@ -626,6 +627,25 @@ __device__ __forceinline__ bool boxes_conflict(int4 a, int4 b, int reach) {
     return max(dx, dy) <= reach;
 }
 
+// Polling uses relaxed loads (served by L2, no L1 invalidation: an acquire load
+// would flush the SM's L1 on every poll and starve the co-resident CTA doing
+// real work); the waiting CTA issues one acquire fence after the flags are set.
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // The scheduler's view of one trial: its index and box, and where its
 // conflicting successors found early (while pixel loads are in flight) go.
 struct SuccScan {
@@ -636,6 +656,12 @@ struct SuccScan {
     int* list;   // [kSS] shared
     int* count;  // shared; the caller zeroes it
     int* more;   // shared: successors may lie beyond the first kSS trials
+    // speculation (nullptr: off): successors left waiting on this trial alone
+    // are queued for an idle CTA to run speculatively (k_trial_sched)
+    const unsigned long long* pred;
+    int* specState;
+    int* specQ;
+    int* specTail;
 };
 
 // Affected pixel i (reference order) -> HR pixel index and its owner cell.
@@ -689,9 +715,13 @@ struct PixIn {
 template <int NT>
 __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialSmem<NT>& sm,
                               const TrialShared& ss, const TrialGeom& g, const uint32_t* comp,
-                              uint32_t n, const SuccScan& sc) {
+                              uint32_t n, const SuccScan& sc, uint32_t* park = nullptr) {
     using BlockScan = typename TrialSmem<NT>::BlockScan;
     __shared__ double red[2][NT / 32];
+    // park != nullptr (speculative run): the result goes to the trial's parked
+    // record {verdict, nt, na, na x {p, a, b, w, e}, nt x {cell, r, g, b}}
+    // instead of this CTA's buffers; see k_trial_sched.
+    uint32_t* parkPix = park ? park + 3 : nullptr;
     const int tid = threadIdx.x;
     const int h = t.S / 2;
     const uint32_t W = uint32_t(t.W), s = uint32_t(t.s);
@@ -717,6 +747,23 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
         const unsigned long long key =
             (static_cast<unsigned long long>(__float_as_uint(e)) << 32) | (0xffffffffu - i);
         atomicMax(ss.key + (cy - g.qy0) * g.qw + (cx - g.qx0), key);
+    }
+    if (sc.list) {
+        // conflicting successors among the next NT trials (loads overlap the
+        // staging above); one waiting on this trial alone is worth speculating
+        const int j = sc.self + 1 + tid;
+        if (j < sc.ncomp && boxes_conflict(sc.box, sc.boxes[j], sc.reach)) {
+            sc.list[atomicAdd(sc.count, 1)] = j;
+            if (sc.specQ && uint32_t(ld_relaxed64(sc.pred + j)) == 1 &&
+                atomicCAS(sc.specState + j, 0, 7) == 0) {
+                st_release(sc.specQ + atomicAdd(sc.specTail, 1), j);
+#ifdef GLU_SCHED_TRACE
+                atomicAdd(&g_phase[19], 1ull);
+#endif
+            }
+        }
+        if (tid == 0)
+            *sc.more = sc.self + 1 + NT < sc.ncomp && sc.sufTop[sc.self + 1 + NT] <= sc.box.w + sc.reach;
     }
     __syncthreads();
     GLU_PHASE(0)
@@ -784,14 +831,6 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
     };
     PixIn cur{};
     if (uint32_t(tid) < na) cur = load(tid);
-    if (sc.list) {
-        // conflicting successors among the next NT trials, while loads fly
-        const int j = sc.self + 1 + tid;
-        if (j < sc.ncomp && boxes_conflict(sc.box, sc.boxes[j], sc.reach))
-            sc.list[atomicAdd(sc.count, 1)] = j;
-        if (tid == 0)
-            *sc.more = sc.self + 1 + NT < sc.ncomp && sc.sufTop[sc.self + 1 + NT] <= sc.box.w + sc.reach;
-    }
     double part0 = 0, part1 = 0;
     bool changed = false;
     for (uint32_t i = tid; i < na; i += NT) {
@@ -856,14 +895,24 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
         np.a = uint32_t(ay) * uint32_t(t.lw) + uint32_t(ax);
         np.b = uint32_t(by) * uint32_t(t.lw) + uint32_t(bx);
         np.w = w;
-        b.bkParams[i] = np;  // the trial's new state, written back at commit
+        if (parkPix) {
+            uint32_t* o = parkPix + 5 * size_t(i);
+            o[0] = p;
+            o[1] = np.a;
+            o[2] = np.b;
+            o[3] = __float_as_uint(np.w);
+        } else {
+            b.bkParams[i] = np;  // the trial's new state, written back at commit
+        }
         const float4 la = ss.win[(ay - g.vy0) * g.vw + (ax - g.vx0)];
         const float4 lb = ss.win[(by - g.vy0) * g.vw + (bx - g.vx0)];
         const float r[3] = {lerp_clamp(w, la.x, lb.x, true), lerp_clamp(w, la.y, lb.y, true),
                             lerp_clamp(w, la.z, lb.z, true)};
         const float e = pixel_error(ip, r);
-        b.bkE[i] = e;
-        (void)p;
+        if (parkPix)
+            parkPix[5 * size_t(i) + 4] = __float_as_uint(e);
+        else
+            b.bkE[i] = e;
         changed |= __float_as_uint(e) != __float_as_uint(oe);
         part1 += double(e);
         cur = nxt;
@@ -904,7 +953,8 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
             for (uint32_t k = tid; k < m; k += NT) {
                 int cx, cy;
                 stage[2 * k] = t.errors[affected_pixel(t, g, ss, c0 + k, cx, cy)];
-                stage[2 * k + 1] = b.bkE[c0 + k];
+                stage[2 * k + 1] = parkPix ? __uint_as_float(parkPix[5 * size_t(c0 + k) + 4])
+                                           : b.bkE[c0 + k];
             }
             __syncthreads();
             if (tid == 0)
@@ -924,6 +974,24 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
     if (tid == 0) {
         sm.touched = nt;
         sm.base = na;
+    }
+    if (park) {
+        if (tid == 0) {
+            park[0] = uint32_t(verdict);
+            park[1] = nt;
+            park[2] = na;
+        }
+        uint32_t* cells = parkPix + 5 * size_t(na);
+        for (uint32_t i = tid; i < nt; i += NT) {
+            const int k = int(ss.touched[i]);
+            const int qx = g.qx0 + k % g.qw, qy = g.qy0 + k / g.qw;
+            const float4 c = ss.win[(qy - g.vy0) * g.vw + (qx - g.vx0)];
+            uint32_t* o = cells + 4 * size_t(i);
+            o[0] = uint32_t(qy) * uint32_t(t.lw) + uint32_t(qx);
+            o[1] = __float_as_uint(c.x);
+            o[2] = __float_as_uint(c.y);
+            o[3] = __float_as_uint(c.z);
+        }
     }
     __syncthreads();
     GLU_PHASE(5)
@@ -994,6 +1062,72 @@ __device__ void commit_trial_smem(const TrialState& t, const TrialBuffers& b, Tr
     GLU_PHASE(7)
 }
 
+// Commit a parked speculative record (see run_trial_smem); returns its verdict.
+template <int NT>
+__device__ int commit_parked(const TrialState& t, TrialSmem<NT>& sm, const uint32_t* park) {
+    const int tid = threadIdx.x;
+    const int verdict = int(park[0]);
+    const uint32_t nt = park[1], na = park[2];
+    const uint32_t* pix = park + 3;
+    const uint32_t* cells = pix + 5 * size_t(na);
+    if (verdict) {
+        for (uint32_t i = tid; i < nt; i += NT) {
+            const uint32_t* c = cells + 4 * size_t(i);
+            float* lc = t.low + 3 * size_t(c[0]);
+            lc[0] = __uint_as_float(c[1]);
+            lc[1] = __uint_as_float(c[2]);
+            lc[2] = __uint_as_float(c[3]);
+        }
+        for (uint32_t i = tid; i < na; i += NT) {
+            const uint32_t* q = pix + 5 * size_t(i);
+            glu_pixel_params pp;
+            pp.a = q[1];
+            pp.b = q[2];
+            pp.w = __uint_as_float(q[3]);
+            t.field[q[0]] = pp;
+            t.errors[q[0]] = __uint_as_float(q[4]);
+        }
+        if (t.dCount) {
+            if (tid == 0) {
+                sm.logCells = atomicAdd(t.dCount, nt);
+                sm.logPixels = atomicAdd(t.dCount + 1, na);
+                if (sm.logCells + nt > t.dCellCap || sm.logPixels + na > t.dPixelCap) {
+                    atomicExch(t.dCount + 2, 1u);
+                    sm.logCells = sm.logPixels = 0xffffffffu;
+                }
+            }
+            __syncthreads();
+            if (sm.logCells != 0xffffffffu) {
+                for (uint32_t i = tid; i < 4 * nt; i += NT)
+                    t.dCells[4 * size_t(sm.logCells) + i] = cells[i];
+                for (uint32_t i = tid; i < 5 * na; i += NT)
+                    t.dPixels[5 * size_t(sm.logPixels) + i] = pix[i];
+            }
+        }
+    }
+    __syncthreads();
+    return verdict;
+}
+
+// Parked-record size (32-bit words) of every trial that may run on chip.
+__global__ void k_park_words(const int4* __restrict__ boxes, int n, int h, int s, int lw, int lh,
+                             int W, int H, int literal, uint32_t* __restrict__ words) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > n) return;
+    if (i == n) {
+        words[n] = 0;
+        return;
+    }
+    const int4 b = boxes[i];
+    uint32_t w = 0;
+    if (b.x >= 0 && !literal) {
+        const TrialGeom g(b, h, lw, lh, s, W, H);
+        if (g.qw * g.qh <= kSQ && g.vw * g.vh <= kSW)
+            w = 3 + 5 * uint32_t(g.dw * g.dh) * uint32_t(s * s) + 4 * uint32_t(g.qw * g.qh);
+    }
+    words[i] = w;
+}
+
 // Sequential sweep: one CTA runs the components in order (used for single
 // trials and as the reference schedule in tests, GLU_OPT_TRIALS = 1).
 __global__ void __launch_bounds__(kSeqThreads) k_trial_sweep(TrialState t, TrialBuffers b,
@@ -1047,18 +1181,6 @@ __global__ void k_trial_boxes(const uint32_t* __restrict__ off, const uint32_t* 
 }
 
 
-// Polling uses relaxed loads (served by L2, no L1 invalidation: an acquire load
-// would flush the SM's L1 on every poll and starve the co-resident CTA doing
-// real work); the waiting CTA issues one acquire fence after the flags are set.
-__device__ __forceinline__ int ld_relaxed(const int* p) {
-    int v;
-    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ void st_release(int* p, int v) {
-    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 struct MinOp {
     __device__ __forceinline__ int operator()(int a, int b) const { return min(a, b); }
@@ -1092,7 +1214,7 @@ __global__ void __launch_bounds__(1024) k_suffix_top(const int4* __restrict__ bo
 // pred[j] = number of earlier trials j conflicts with (one warp per trial i
 // walks its successors j > i).
 __global__ void k_trial_preds(const int4* __restrict__ boxes, const int* __restrict__ sufTop,
-                              int n, int reach, int* __restrict__ pred) {
+                              int n, int reach, unsigned long long* __restrict__ pred) {
     const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (i >= n) return;
     const int4 bi = boxes[i];
@@ -1100,15 +1222,15 @@ __global__ void k_trial_preds(const int4* __restrict__ boxes, const int* __restr
     for (int base = i + 1; base < n; base += 32) {
         if (sufTop[base] > lim) break;
         const int j = base + lane;
-        if (j < n && boxes_conflict(bi, boxes[j], reach)) atomicAdd(pred + j, 1);
+        if (j < n && boxes_conflict(bi, boxes[j], reach)) atomicAdd(pred + j, 1ull);
     }
 }
 
 // Trials with no earlier conflict start ready, in index order within a warp.
-__global__ void k_trial_seed(const int* __restrict__ pred, int n, int* __restrict__ queue,
-                             int* __restrict__ qTail) {
+__global__ void k_trial_seed(const unsigned long long* __restrict__ pred, int n,
+                             int* __restrict__ queue, int* __restrict__ qTail) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x, lane = threadIdx.x & 31;
-    const bool ready = j < n && pred[j] == 0;
+    const bool ready = j < n && uint32_t(pred[j]) == 0;
     const unsigned m = __ballot_sync(0xffffffffu, ready);
     if (!m) return;
     int base = 0;
@@ -1118,18 +1240,34 @@ __global__ void k_trial_seed(const int* __restrict__ pred, int n, int* __restric
 }
 
 // Persistent conflict-aware trial scheduler (see the file comment): a
-// dependency-counting dataflow schedule.  CTAs pop ready trials from a FIFO
-// (slot k of `queue` is filled by the k-th trial to become ready); a finished
-// trial decrements the counters of its conflicting successors and pushes the
-// ones that reach zero.  Every CTA is resident, so whenever trials remain one
-// of them is ready or running: no deadlock, and conflicting trials still run
-// in index order, so the state is bit-identical to the sequential loop.
+// dependency-counting dataflow schedule with speculation.
+//
+// Dataflow: CTAs pop ready trials from a FIFO (slot k of `queue` is filled by
+// the k-th trial to become ready); a finished trial decrements the counters of
+// its conflicting successors and pushes the ones that reach zero, except one
+// that runs next on the same CTA (a dependency chain stays put).
+//
+// Speculation (spec != 0): a trial left waiting on one running predecessor is
+// queued for speculation; a CTA with no ready trial takes the newest queued
+// one and runs it on chip against the current state, parking the result (its
+// new LR cells, params and errors) instead of writing it.  Each trial's 64-bit
+// counter holds {accepted predecessors (high), unfinished predecessors (low)};
+// a finishing trial updates it with one atomic add.  The speculation snapshots
+// the high word before reading any state; when the trial becomes ready its
+// record is valid iff the high word is unchanged -- no conflicting predecessor
+// was accepted (or wrote in place) meanwhile, and a rejected trial leaves the
+// state bit for bit as it found it.  A valid record is committed (a copy
+// instead of a re-solve); otherwise the trial runs normally.  Chains of mostly
+// rejected trials thus overlap (C2: 57 % rejected, C4: 70 %).  Conflicting
+// trials still take effect in index order: the state is bit-identical to the
+// sequential loop.
 __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
     TrialState t, TrialBuffers big, char* ctaBufs, const uint32_t* off, const uint32_t* px,
-    const uint32_t* ids, int ncomp, const int4* boxes, const int* sufTop, int* pred,
-    int* queue, int* qHead, int* qTail, int* finished, int reach) {
+    const uint32_t* ids, int ncomp, const int4* boxes, const int* sufTop, unsigned long long* pred,
+    int* queue, int* qHead, int* qTail, int* finished, int reach, int spec, int* specState,
+    uint32_t* specSnap, int* specQ, int* specTail, const uint32_t* parkOff, uint32_t* parkBuf) {
     __shared__ TrialSmem<kSchedThreads> sm;
-    __shared__ int sIdx;
+    __shared__ int sIdx, sMode, sUse;
     extern __shared__ __align__(16) char dyn[];
     const TrialShared ss = TrialShared::carve(dyn);
     // this CTA's private buffers
@@ -1147,72 +1285,176 @@ __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
     __shared__ int sList[kSS];
     for (int k = threadIdx.x; k < kSQ; k += kSchedThreads) ss.key[k] = 0;
     if (threadIdx.x == 0) sNext = -1;
+    enum { kExit = 0, kRun = 1, kSpec = 2 };
     for (;;) {
         if (threadIdx.x == 0) {
-            int i = sNext;
+            int i = sNext, mode = kRun;
 #ifdef GLU_SCHED_TRACE
             const unsigned long long tc = gtimer();
 #endif
-            if (i < 0) {
-                const int k = atomicAdd(qHead, 1);
-                // (continuations bypass the FIFO, so not every slot fills:
-                // stop waiting once every trial has finished)
-                if (k < ncomp)
-                    while ((i = ld_relaxed(queue + k)) < 0 && ld_relaxed(finished) < ncomp)
-                        __nanosleep(100);
+            while (i < 0) {
+                const int h = ld_relaxed(qHead);
+                if (h < ld_relaxed(qTail)) {
+                    // slot h is reserved by a pusher: it fills shortly
+                    if (atomicCAS(qHead, h, h + 1) == h)
+                        while ((i = ld_relaxed(queue + h)) < 0) __nanosleep(64);
+                    continue;
+                }
+                if (ld_relaxed(finished) >= ncomp) {
+                    mode = kExit;
+                    break;
+                }
+                if (spec) {
+                    // newest queued speculation first (older entries are mostly
+                    // stale: their trials became ready meanwhile)
+                    constexpr int kWin = 16;
+                    const int tl = ld_relaxed(specTail);
+                    int cand[kWin];
+#pragma unroll
+                    for (int k = 0; k < kWin; ++k)
+                        cand[k] = tl - 1 - k >= 0 ? ld_relaxed(specQ + tl - 1 - k) : -1;
+                    int got = -1;
+#pragma unroll
+                    for (int k = 0; k < kWin; ++k) {
+                        const int j = cand[k];
+                        if (got < 0 && j >= 0 && ld_relaxed(specState + j) == 7 &&
+                            parkOff[j + 1] > parkOff[j] && parkOff[j + 1] <= kParkWords &&
+                            atomicCAS(specState + j, 7, 1) == 7)
+                            got = j;
+                    }
+                    if (got >= 0) {
+#ifdef GLU_SCHED_TRACE
+                        atomicAdd(&g_phase[21], 1ull);
+#endif
+                        i = got;
+                        mode = kSpec;
+                        // accepted-predecessor count, before any of the trial's reads
+                        specSnap[got] = uint32_t(ld_relaxed64(pred + got) >> 32);
+                        continue;
+                    }
+                }
+                __nanosleep(256);
             }
 #ifdef GLU_SCHED_TRACE
-            if (i >= 0) {
+            if (mode == kRun) {
                 g_trace[3 * i] = tc;
                 g_trace[3 * i + 1] = gtimer();
             }
 #endif
             sIdx = i;
+            sMode = mode;
             sNext = -1;
             sCount = 0;
             sMore = 1;
         }
         __syncthreads();
-        const int i = sIdx;
-        if (i < 0) break;
-        __threadfence();  // acquire: the predecessors' writes are visible
+        const int i = sIdx, mode = sMode;
+        if (mode == kExit) break;
+        __threadfence();  // acquire: the predecessors' committed writes are visible
         const int4 bi = boxes[i];
         const bool isBig = bi.x < 0;
         const uint32_t c = ids ? ids[i] : uint32_t(i);
         const uint32_t n = off[c + 1] - off[c];
-        int v;
         const TrialGeom geo(bi, t.S / 2, t.lw, t.lh, t.s, t.W, t.H);
         const bool onChip = !isBig && !t.literal && geo.fits(n);
-        if (onChip) {
-            const SuccScan sc{boxes, sufTop, ncomp, reach, i, bi, sList, &sCount, &sMore};
+        const SuccScan noScan{nullptr, nullptr, 0,       0,       0,      make_int4(0, 0, 0, 0),
+                              nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+        if (mode == kSpec) {
+#ifdef GLU_SCHED_TRACE
+            if (threadIdx.x == 0) g_trace[3 * ncomp + 2 * i] = gtimer();
+#endif
+            if (onChip) {
+                run_trial_smem<kSchedThreads>(t, local, sm, ss, geo, px + off[c], n, noScan,
+                                              parkBuf + parkOff[i]);
+#ifdef GLU_SCHED_TRACE
+                if (threadIdx.x == 0) atomicAdd(&g_phase[18], 1ull);
+#endif
+            }
+            if (threadIdx.x == 0) {
+#ifdef GLU_SCHED_TRACE
+                g_trace[3 * ncomp + 2 * i + 1] = gtimer();
+#endif
+                __threadfence();
+                atomicCAS(specState + i, 1, onChip ? 2 : 3);  // 2: record parked
+            }
+            __syncthreads();
+            continue;
+        }
+        // mode == kRun: all conflicting predecessors are final
+        if (threadIdx.x == 0) {
+            int use = 0;
+            if (spec) {
+                int st = ld_relaxed(specState + i);
+                // a speculation in flight that can still be valid is worth
+                // waiting for (it started before this trial became ready)
+#ifdef GLU_SCHED_TRACE
+                if (st == 1) atomicAdd(&g_phase[22], 1ull);
+                if (st == 7) atomicAdd(&g_phase[23], 1ull);
+#endif
+                const uint32_t acc = uint32_t(ld_relaxed64(pred + i) >> 32);  // final now
+                while (st == 1 && acc == ld_relaxed(reinterpret_cast<int*>(specSnap) + i)) {
+                    __nanosleep(64);
+                    st = ld_relaxed(specState + i);
+                }
+                if (st == 2 && atomicCAS(specState + i, 2, 5) == 2) {
+                    __threadfence();
+                    use = acc == specSnap[i];
+                }
+            }
+            sUse = use;
+        }
+        __syncthreads();
+        int v;
+        bool dirty = false;
+        if (sUse) {
+            v = commit_parked<kSchedThreads>(t, sm, parkBuf + parkOff[i]);
+#ifdef GLU_SCHED_TRACE
+            if (threadIdx.x == 0) atomicAdd(&g_phase[17], 1ull);
+#endif
+        } else if (onChip) {
+            const SuccScan sc{boxes,   sufTop, ncomp,     reach,     i,
+                              bi,      sList,  &sCount,   &sMore,    pred,
+                              spec ? specState : nullptr, spec ? specQ : nullptr, specTail};
             v = run_trial_smem<kSchedThreads>(t, local, sm, ss, geo, px + off[c], n, sc);
             if (v) commit_trial_smem<kSchedThreads>(t, local, sm, ss, geo);
         } else {
             v = run_trial<kSchedThreads>(t, isBig ? big : local, sm, px + off[c], n);
+            dirty = true;  // wrote in place (and rolled back if rejected)
         }
         if (threadIdx.x == 0) {
             atomicAdd(t.result + (v ? 0 : 1), 1);
 #ifdef GLU_SCHED_TRACE
-            g_trace[3 * i + 2] = (gtimer() & ~1ull) | unsigned(v != 0);  // LSB: verdict
+            // bit 0: verdict, bit 1: a parked speculative record was committed
+            g_trace[3 * i + 2] = (gtimer() & ~3ull) | unsigned(v != 0) | (sUse ? 2u : 0u);
 #endif
         }
+        __threadfence();  // release this trial's writes (after the trial's last barrier)
 #ifdef GLU_SCHED_TRACE
         long long tph = clock64();
 #endif
         // Release the conflicting successors (those found early, then the
-        // rest).  One successor whose count reaches zero runs next on this CTA
-        // (a dependency chain stays put); the others go to the FIFO.
-        __threadfence();  // release this trial's writes (ordered after run_trial's barrier)
+        // rest).  One successor whose count reaches zero runs next on this CTA;
+        // the others go to the FIFO.
+        // one predecessor fewer; one more accepted (or in-place) predecessor
+        const unsigned long long delta = spec && (v || dirty) ? 0xffffffffull : ~0ull;
         auto release = [&](int j) {
-            if (atomicSub(pred + j, 1) == 1 && atomicCAS(&sNext, -1, j) != -1) {
+            const int left = int(uint32_t(atomicAdd(pred + j, delta)));
+            if (left == 1 && atomicCAS(&sNext, -1, j) != -1) {
                 __threadfence();
                 st_release(queue + atomicAdd(qTail, 1), j);
+            } else if (left == 2 && spec && atomicCAS(specState + j, 0, 7) == 0) {
+                st_release(specQ + atomicAdd(specTail, 1), j);  // one predecessor to go
+#ifdef GLU_SCHED_TRACE
+                atomicAdd(&g_phase[20], 1ull);
+#endif
             }
         };
-        if (threadIdx.x < sCount) release(sList[threadIdx.x]);
+        const int early = sUse ? 0 : sCount;
+        if (threadIdx.x < early) release(sList[threadIdx.x]);
         if (sMore) {
             const int lim = bi.w + reach;
-            for (int base = onChip ? i + 1 + kSchedThreads : i + 1; base < ncomp; base += kSchedThreads) {
+            for (int base = (onChip && !sUse) ? i + 1 + kSchedThreads : i + 1; base < ncomp;
+                 base += kSchedThreads) {
                 if (sufTop[base] > lim) break;
                 const int j = base + int(threadIdx.x);
                 if (j < ncomp && boxes_conflict(bi, boxes[j], reach)) release(j);
@@ -1287,94 +1529,136 @@ TrialState trial_state(const float* high, float* low, glu_pixel_params* field, f
     return t;
 }
 
-int sched_grid(glu_ctx* ctx) {
+template <typename K>
+int sched_grid(glu_ctx* ctx, K kernel) {
     static thread_local int cached = -1, cachedDev = -1;
     if (cached > 0 && cachedDev == ctx->device) return cached;
     int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
-    cudaFuncSetAttribute(k_trial_sched, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(kTrialSmemBytes));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_trial_sched, kSchedThreads,
-                                                  kTrialSmemBytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, kSchedThreads, kTrialSmemBytes);
     cached = sms * std::max(1, std::min(per, 2));
     cachedDev = ctx->device;
     return cached;
 }
 
-// Parallel conflict-aware schedule of the listed components (all when
-// ids == NULL), k_trial_sched.  Asynchronous on ctx->stream.
-int run_sched(glu_ctx* ctx, const TrialState& t, const JointScratch& js, const glu_grid& g,
-              const glu_config& cfg, const uint32_t* off, const uint32_t* px,
-              const uint32_t* ids, size_t n) {
-    const int grid = sched_grid(ctx);
-    const size_t per = size_t(kCtaCells) * 16 + size_t(kCtaPixels) * 20;
-    char* ctaBufs = static_cast<char*>(scratch(ctx, S_SCHED, per * grid));
-    // boxes (int4) | sufTop | queue | pred | qHead, qTail, finished (4-byte words)
-    char* meta = static_cast<char*>(scratch(ctx, S_SCHED_META, n * 28 + 64));
-    if (!ctaBufs || !meta) return GLU_ENOMEM;
-    int4* boxes = reinterpret_cast<int4*>(meta);
-    int* sufTop = reinterpret_cast<int*>(meta + n * 16);
-    int* queue = sufTop + n;
-    int* pred = queue + n;
-    int* qHead = pred + n;
-    int* qTail = qHead + 1;
-    int* finished = qHead + 2;
-    cudaError_t e = cudaMemsetAsync(pred, 0, (n + 3) * sizeof(int), ctx->stream);
-    if (e == cudaSuccess) e = cudaMemsetAsync(queue, 0xff, n * sizeof(int), ctx->stream);
-    if (e != cudaSuccess) return fail_cuda(e, "trial schedule");
-    const int reach = 2 * (cfg.windowSide / 2);
-    k_trial_boxes<<<blocks_for(n * 32, 256), 256, 0, ctx->stream>>>(
-        off, px, ids, int(n), g.highW, g.scale, g.lowW, g.lowH, cfg.windowSide / 2,
-        cfg.literalComponentUpdate, 0, boxes);
-    k_suffix_top<<<1, 1024, 0, ctx->stream>>>(boxes, int(n), sufTop);
-    k_trial_preds<<<blocks_for(n * 32, 256), 256, 0, ctx->stream>>>(boxes, sufTop, int(n), reach,
-                                                                    pred);
-    k_trial_seed<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(pred, int(n), queue, qTail);
-    ctx->launches += 4;
-    TrialState ts = t;
-    TrialBuffers big = js.big;
-    int nc = int(n), rch = reach;
-    void* args[] = {&ts,    &big,   &ctaBufs, &off,  &px,    &ids,   &nc,
-                    &boxes, &sufTop, &pred,   &queue, &qHead, &qTail, &finished, &rch};
 #ifdef GLU_SCHED_TRACE
+unsigned long long* trace_begin(glu_ctx* ctx, size_t n) {
     unsigned long long* trace = nullptr;
-    cudaMalloc(&trace, n * 24 + 8);
+    cudaMalloc(&trace, n * 40 + 8);
+    cudaMemsetAsync(trace, 0, n * 40 + 8, ctx->stream);
     cudaMemcpyToSymbolAsync(g_trace, &trace, sizeof(trace), 0, cudaMemcpyHostToDevice,
                             ctx->stream);
+    return trace;
+}
+
+void trace_end(glu_ctx* ctx, unsigned long long* trace, const int4* boxes, size_t n) {
+    std::vector<unsigned long long> h(5 * n);
+    std::vector<int4> hb(n);
+    cudaMemcpyAsync(h.data(), trace, n * 40, cudaMemcpyDeviceToHost, ctx->stream);
+    cudaMemcpyAsync(hb.data(), boxes, n * 16, cudaMemcpyDeviceToHost, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(trace);
+    if (const char* f = getenv("GLU_SCHED_TRACE_FILE")) {
+        if (FILE* fp = fopen(f, "ab")) {
+            const unsigned long long hdr[2] = {0x5452414346ull, n};
+            fwrite(hdr, 8, 2, fp);
+            fwrite(h.data(), 8, 5 * n, fp);
+            fwrite(hb.data(), 16, n, fp);
+            fclose(fp);
+        }
+    }
+    unsigned long long ph[24];
+    cudaMemcpyFromSymbol(ph, g_phase, sizeof(ph));
+    const unsigned long long z[24] = {};
+    cudaMemcpyToSymbol(g_phase, z, sizeof(z));
+    if (const char* f = getenv("GLU_SCHED_TRACE_FILE")) {
+        if (FILE* fp = fopen((std::string(f) + ".phases").c_str(), "a")) {
+            for (int k = 0; k < 24; ++k) fprintf(fp, "%llu ", ph[k]);
+            fprintf(fp, "%zu\n", n);
+            fclose(fp);
+        }
+    }
+}
+#endif
+
+// Parallel conflict-aware schedule of the listed components (all when
+// ids == NULL), k_trial_sched; `spec` enables speculation (one more host
+// synchronisation: the parked-record sizes are summed to size their storage).
+// Asynchronous on ctx->stream otherwise.
+int run_sched(glu_ctx* ctx, const TrialState& t, const JointScratch& js, const glu_grid& g,
+              const glu_config& cfg, const uint32_t* off, const uint32_t* px,
+              const uint32_t* ids, size_t n, bool spec) {
+    const int grid = sched_grid(ctx, k_trial_sched);
+    const size_t per = size_t(kCtaCells) * 16 + size_t(kCtaPixels) * 20;
+    char* ctaBufs = static_cast<char*>(scratch(ctx, S_SCHED, per * grid));
+    // boxes (int4) | pred (u64: accepted << 32 | unfinished) | counters (16) | sufTop |
+    // queue | specState | specSnap | specQ | parkOff (n + 1)
+    char* meta = static_cast<char*>(scratch(ctx, S_SCHED_META, n * 48 + 128));
+    if (!ctaBufs || !meta) return GLU_ENOMEM;
+    int4* boxes = reinterpret_cast<int4*>(meta);
+    unsigned long long* pred = reinterpret_cast<unsigned long long*>(meta + n * 16);
+    int* ctr = reinterpret_cast<int*>(pred + n);
+    int *qHead = ctr, *qTail = ctr + 1, *finished = ctr + 2, *specTail = ctr + 3;
+    int* sufTop = ctr + 16;
+    int* queue = sufTop + n;
+    int* specState = queue + n;
+    uint32_t* specSnap = reinterpret_cast<uint32_t*>(specState + n);
+    int* specQ = reinterpret_cast<int*>(specSnap + n);
+    uint32_t* parkOff = reinterpret_cast<uint32_t*>(specQ + n);
+    cudaStream_t st = ctx->stream;
+    cudaError_t e = cudaMemsetAsync(pred, 0, n * 8 + 64, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(queue, 0xff, n * sizeof(int), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(specState, 0, n * sizeof(int), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(specSnap, 0x7f, n * sizeof(int), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(specQ, 0xff, n * sizeof(int), st);
+    if (e != cudaSuccess) return fail_cuda(e, "trial schedule");
+    const int reach = 2 * (cfg.windowSide / 2);
+    k_trial_boxes<<<blocks_for(n * 32, 256), 256, 0, st>>>(
+        off, px, ids, int(n), g.highW, g.scale, g.lowW, g.lowH, cfg.windowSide / 2,
+        cfg.literalComponentUpdate, 0, boxes);
+    k_suffix_top<<<1, 1024, 0, st>>>(boxes, int(n), sufTop);
+    k_trial_preds<<<blocks_for(n * 32, 256), 256, 0, st>>>(boxes, sufTop, int(n), reach, pred);
+    k_trial_seed<<<blocks_for(n, 256), 256, 0, st>>>(pred, int(n), queue, qTail);
+    ctx->launches += 4;
+    uint32_t* parkBuf = nullptr;
+    if (spec) {
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, parkOff, parkOff, int(n) + 1, st);
+        // record sizes, then the scan's temporary storage, in one slot
+        const size_t wBytes = ((n + 1) * 4 + 255) & ~size_t(255);
+        char* temp = static_cast<char*>(scratch(ctx, S_PARK_TMP, wBytes + tb + 64));
+        if (!temp) return GLU_ENOMEM;
+        uint32_t* w = reinterpret_cast<uint32_t*>(temp);
+        k_park_words<<<blocks_for(n + 1, 256), 256, 0, st>>>(
+            boxes, int(n), cfg.windowSide / 2, g.scale, g.lowW, g.lowH, g.highW, g.highH,
+            cfg.literalComponentUpdate, w);
+        ++ctx->launches;
+        e = cub::DeviceScan::ExclusiveSum(temp + wBytes, tb, w, parkOff, int(n) + 1, st);
+        if (e != cudaSuccess) return fail_cuda(e, "trial schedule");
+        ctx->launches += 2;
+        // fixed arena, no host round trip: records past its end are simply
+        // not speculated (C4 needs ~280 MB, C2 ~60 MB)
+        parkBuf = static_cast<uint32_t*>(scratch(ctx, S_PARK, size_t(kParkWords) * 4));
+        if (!parkBuf) return GLU_ENOMEM;
+    }
+    TrialState ts = t;
+    TrialBuffers big = js.big;
+    int nc = int(n), rch = reach, sp = spec ? 1 : 0;
+    void* args[] = {&ts,    &big,      &ctaBufs, &off,       &px,       &ids,
+                    &nc,    &boxes,    &sufTop,  &pred,      &queue,    &qHead,
+                    &qTail, &finished, &rch,     &sp,        &specState, &specSnap,
+                    &specQ, &specTail, &parkOff, &parkBuf};
+#ifdef GLU_SCHED_TRACE
+    unsigned long long* trace = trace_begin(ctx, n);
 #endif
     e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_trial_sched), grid, kSchedThreads,
-                                    args, kTrialSmemBytes, ctx->stream);
+                                    args, kTrialSmemBytes, st);
     ++ctx->launches;
     if (e != cudaSuccess) return fail_cuda(e, "trial schedule");
 #ifdef GLU_SCHED_TRACE
-    {
-        std::vector<unsigned long long> h(3 * n);
-        std::vector<int4> hb(n);
-        cudaMemcpyAsync(h.data(), trace, n * 24, cudaMemcpyDeviceToHost, ctx->stream);
-        cudaMemcpyAsync(hb.data(), boxes, n * 16, cudaMemcpyDeviceToHost, ctx->stream);
-        cudaStreamSynchronize(ctx->stream);
-        cudaFree(trace);
-        if (const char* f = getenv("GLU_SCHED_TRACE_FILE")) {
-            if (FILE* fp = fopen(f, "ab")) {
-                const unsigned long long hdr[2] = {0x5452414345ull, n};
-                fwrite(hdr, 8, 2, fp);
-                fwrite(h.data(), 8, 3 * n, fp);
-                fwrite(hb.data(), 16, n, fp);
-                fclose(fp);
-            }
-        }
-        unsigned long long ph[24];
-        cudaMemcpyFromSymbol(ph, g_phase, sizeof(ph));
-        const unsigned long long z[24] = {};
-        cudaMemcpyToSymbol(g_phase, z, sizeof(z));
-        if (const char* f = getenv("GLU_SCHED_TRACE_FILE")) {
-            if (FILE* fp = fopen((std::string(f) + ".phases").c_str(), "a")) {
-                for (int k = 0; k < 17; ++k) fprintf(fp, "%llu ", ph[k]);
-                fprintf(fp, "%zu\n", n);
-                fclose(fp);
-            }
-        }
-    }
+    trace_end(ctx, trace, boxes, n);
 #endif
     return GLU_OK;
 }
@@ -1550,7 +1834,9 @@ int joint_sweep(glu_ctx* ctx, const float* high, float* low, glu_pixel_params* f
         ++ctx->launches;
         e = cudaGetLastError();
     } else {
-        rc = run_sched(ctx, t, js, g, cfg, off, px, nullptr, ncomp);
+        rc = ctx->trials == 2 || cfg.literalComponentUpdate
+                 ? run_sched(ctx, t, js, g, cfg, off, px, nullptr, ncomp, false)
+                 : run_sched(ctx, t, js, g, cfg, off, px, nullptr, ncomp, true);
         if (rc) return rc;
         e = cudaSuccess;
     }
@@ -1646,7 +1932,9 @@ int run_trials(glu_ctx* ctx, const float* high, float* low, glu_pixel_params* fi
         if (e != cudaSuccess) return fail_cuda(e, "run_trials");
     }
     if (n) {
-        rc = run_sched(ctx, t, js, g, cfg, off, px, ids, n);
+        rc = ctx->trials == 2 || cfg.literalComponentUpdate
+                 ? run_sched(ctx, t, js, g, cfg, off, px, ids, n, false)
+                 : run_sched(ctx, t, js, g, cfg, off, px, ids, n, true);
         if (rc) return rc;
     }
     int res[4];

@@ -173,7 +173,8 @@ class Context:
         N.check(N.lib().glu_ctx_set_option(self.handle, 1, int(value)))
 
     def set_trials(self, value: int) -> None:
-        """GLU_OPT_TRIALS: 0 conflict-aware parallel schedule, 1 one CTA in order."""
+        """GLU_OPT_TRIALS: 0 speculative parallel schedule, 1 one CTA in order,
+        2 dependency-counting dataflow schedule."""
         N.check(N.lib().glu_ctx_set_option(self.handle, 2, int(value)))
 
     @property

@@ -300,22 +300,24 @@ def test_reference_unit_tests_pass_against_dropin_api(glu):
     (480, 360, 6, 3, False, "fast"), (512, 384, 8, 3, False, "gnu"),
     (384, 256, 8, 3, False, "exact"), (250, 190, 5, 5, False, "exact")])
 def test_parallel_trial_schedule_matches_sequential(glu, W, H, s, S, literal, mode):
-    """The conflict-aware parallel trial schedule (on-chip trial path, full and
-    clipped footprints, power-of-two and other scales) is bit-identical to the
-    reference's sequential component loop (jointopt.cpp:195-202)."""
+    """The parallel trial schedules -- speculative (default) and dataflow -- on
+    the on-chip trial path (full and clipped footprints, power-of-two and other
+    scales) are bit-identical to the reference's sequential component loop
+    (jointopt.cpp:195-202)."""
     from paper_2307_09582_b200 import workloads
     high = dev(workloads.scene(W, H, 40 + s))
     cfg = glu.GluConfig(windowSide=S, literalComponentUpdate=literal)
     md = {"fast": glu.Mode.Fast, "gnu": glu.Mode.Gnu, "exact": glu.Mode.Exact}[mode]
     ctx = glu.glu.context()
     out = []
-    for trials in (1, 0):
+    for trials in (1, 0, 2):
         ctx.set_trials(trials)
         out.append(glu.joint_optimize(high, s, cfg, md))
     ctx.set_trials(0)
-    a, b = out
+    a = out[0]
     assert a.trialsAccepted + a.trialsRejected > 10
-    assert (a.iterations, a.trialsAccepted, a.trialsRejected) == \
-        (b.iterations, b.trialsAccepted, b.trialsRejected)
-    assert torch.equal(a.low, b.low) and torch.equal(a.field.params, b.field.params)
-    assert torch.equal(a.errors, b.errors)
+    for b in out[1:]:  # speculative and dataflow schedules
+        assert (a.iterations, a.trialsAccepted, a.trialsRejected) == \
+            (b.iterations, b.trialsAccepted, b.trialsRejected)
+        assert torch.equal(a.low, b.low) and torch.equal(a.field.params, b.field.params)
+        assert torch.equal(a.errors, b.errors)

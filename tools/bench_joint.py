@@ -24,6 +24,7 @@ p = argparse.ArgumentParser()
 p.add_argument("--config", type=int, nargs="+", default=[2, 4])
 p.add_argument("--reps", type=int, default=3)
 p.add_argument("--cpu", action="store_true")
+p.add_argument("--trials", type=int, default=0, help="GLU_OPT_TRIALS (0 speculative, 2 dataflow)")
 a = p.parse_args()
 
 # Under torchrun (WORLD_SIZE > 1) the level-synchronous multi-rank loop runs
@@ -58,6 +59,7 @@ if WORLD > 1:
     dist.destroy_process_group()
     sys.exit(0)
 
+glu.glu.context().set_trials(a.trials)
 for c in a.config:
     cfg = workloads.CONFIGS[c]
     W, H, s = cfg["W"], cfg["H"], cfg["scale"]

@@ -38,18 +38,21 @@ def launches(path):
     o = 0
     while o < len(raw):
         magic, n = np.frombuffer(raw, np.uint64, 2, o)
-        assert magic == 0x5452414345
+        assert magic in (0x5452414345, 0x5452414346)
+        words = 3 if magic == 0x5452414345 else 5
         n = int(n)
         o += 16
-        st = np.frombuffer(raw, np.uint64, 3 * n, o).reshape(n, 3).astype(np.int64)
-        o += 24 * n
+        allw = np.frombuffer(raw, np.uint64, words * n, o).astype(np.int64)
+        st = allw[:3 * n].reshape(n, 3)
+        sp = allw[3 * n:].reshape(n, 2) if words == 5 else np.zeros((n, 2), np.int64)
+        o += 8 * words * n
         bx = np.frombuffer(raw, np.int32, 4 * n, o).reshape(n, 4).astype(np.int64)
         o += 16 * n
-        yield st, bx
+        yield st, bx, sp
 
 
 def show(path, reach=2):
-    for k, (st, bx) in enumerate(launches(path)):
+    for k, (st, bx, sp) in enumerate(launches(path)):
         n = len(st)
         t0 = st[:, 0].min()
         wait = (st[:, 1] - st[:, 0]) / 1e3
@@ -76,6 +79,31 @@ def show(path, reach=2):
               f"sum run {runt.sum():.0f} us, critical path {fin.max():.0f} us "
               f"({depth.max()} trials deep); accepted {acc.sum()}, critical path through "
               f"accepted predecessors only {fin2.max():.0f} us")
+        used = (st[:, 2] & 2).astype(bool)
+        if True:
+            print(f"   parked records used {used.sum()}: finalize mean {runt[used].mean():.1f} us, "
+                  f"normal runs mean {runt[~used].mean():.1f} us; speculative runs "
+                  f"{(sp[:, 0] > 0).sum()}, mean {((sp[:, 1] - sp[:, 0])[sp[:, 0] > 0]).mean() / 1e3:.1f} us")
+        # the realised critical chain: walk back from the last trial to finish
+        # through the predecessor that finished last before it became ready
+        x = int(np.argmax(st[:, 2] >> 2))
+        links = []
+        endt = (st[:, 2] >> 2) << 2
+        while True:
+            dx = np.maximum(0, np.maximum(bx[:x, 0] - bx[x, 2], bx[x, 0] - bx[:x, 2]))
+            dy = np.maximum(0, np.maximum(bx[:x, 1] - bx[x, 3], bx[x, 1] - bx[:x, 3]))
+            dep = np.nonzero(np.maximum(dx, dy) <= reach)[0]
+            links.append(x)
+            if len(dep) == 0:
+                break
+            x = int(dep[np.argmax(endt[dep])])
+        links = links[::-1]
+        gaps = [(st[b, 1] - endt[a]) / 1e3 for a, b in zip(links, links[1:])]
+        runs = [runt[b] for b in links]
+        print(f"   realised chain: {len(links)} trials, run {np.sum(runs):.0f} us "
+              f"(mean {np.mean(runs):.1f}), gaps {np.sum(gaps):.0f} us, parked used "
+              f"{int(used[links].sum()) if used.any() else 0}, accepted {int(acc[links].sum())}; "
+              f"starts at {(st[links[0], 1] - t0) / 1e3:.0f} us")
         # claim timeline: when did the last trial get claimed / become ready
         print(f"   last claim at {(st[:, 0].max() - t0) / 1e3:.0f} us, "
               f"last ready at {(st[:, 1].max() - t0) / 1e3:.0f} us")
@@ -96,6 +124,11 @@ def show_phases(path):
         if len(v) > 10:
             print(f"   re-solved pixels / trial {v[10] / n:.0f}, fp64 fallbacks {v[9]} "
                   f"({100.0 * v[9] / max(1, v[10]):.3f}%)")
+        if len(v) > 19:
+            print(f"   speculative runs {v[18]}, parked records committed {v[17]}")
+        if len(v) > 24:
+            print(f"   spec pushes at start {v[19]}, at release {v[20]}, pops {v[21]}, "
+                  f"finalizer saw in-flight {v[22]}, still queued {v[23]}")
         if len(v) > 17:
             print("   fallback rule: nan %d, no-a/tiny %d, a-tie %d, zero-b %d, b-tie %d; "
                   "b close calls settled in double %d" % tuple(v[11:17]))
