@@ -470,6 +470,20 @@ namespace {
 int frame_kernels(glu_ctx* ctx, const float* frame, const glu_grid* g, const glu_config* cfg,
                   int mode, int targetOp, float* low, float* target, float* out,
                   glu_pixel_params* params) {
+    if (ctx->solver != 1 && solve32_supported(mode, cfg->windowSide, g->scale)) {
+        // downsample + matte + LR packing fused into one launch before the solve
+        const bool matte = targetOp == GLU_TARGET_MATTE;
+        SolveArgs a = solve_args(frame, low, g, cfg, mode);
+        a.params = params;
+        a.lowT = matte ? target : low;
+        a.channels = matte ? 1 : 3;
+        a.clamp = 1;
+        a.out = out;
+        a.fallbacks = ctx->d_counters;
+        GLU_CUDA(launch_frame_solve32(ctx, a, low, matte ? target : nullptr, ctx->solver == 2),
+                 "upsample_frames");
+        return GLU_OK;
+    }
     GLU_CUDA(launch_grid_downsample(ctx, frame, g->highW, g->highH, g->scale, g->lowW, g->lowH,
                                     low),
              "upsample_frames");

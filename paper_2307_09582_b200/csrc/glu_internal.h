@@ -69,6 +69,11 @@ cudaError_t launch_solve(glu_ctx* ctx, const SolveArgs& a);
 // S = 3, s >= 3 via glu_solve32x.cu).
 bool solve32_supported(int mode, int S, int s);
 cudaError_t launch_solve32(glu_ctx* ctx, const SolveArgs& a, int forceFallback);
+// One frame of the video path: grid_downsample of a.high into `low`, optional
+// 1-ch matte of it into `matte`, and the LR packing in one kernel, then the
+// solve (a.lowT must already point at `low` or `matte`).
+cudaError_t launch_frame_solve32(glu_ctx* ctx, const SolveArgs& a, float* low, float* matte,
+                                 int forceFallback);
 bool solve32x_supported(int mode, int S, int s);
 cudaError_t launch_solve32x(glu_ctx* ctx, const SolveArgs& a, const float4* packed,
                             int forceFallback, const unsigned* nanFlag);

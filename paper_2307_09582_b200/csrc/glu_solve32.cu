@@ -331,13 +331,60 @@ bool solve32_supported(int mode, int S, int s) {
            solve32x_supported(mode, S, s);
 }
 
-cudaError_t launch_solve32(glu_ctx* ctx, const SolveArgs& a0, int forceFallback) {
+namespace {
+
+SolveArgs prepared(const SolveArgs& a0) {
     SolveArgs a = a0;
     // x / s as a multiply-high: exact for x, s < 2^16 with m = ceil(2^32 / s).
     a.sdiv = (a.W < 65536 && a.H < 65536)
                  ? unsigned((0x100000000ull + unsigned(a.s) - 1) / unsigned(a.s))
                  : 0u;
     a.epsf = float(a.eps);
+    return a;
+}
+
+cudaError_t dispatch(glu_ctx* ctx, const SolveArgs& a, const float4* packed, int forceFallback,
+                     const unsigned* nanFlag) {
+    if (a.mode == GLU_MODE_EXACT) return launch_solve32x(ctx, a, packed, forceFallback, nanFlag);
+    if (a.mode == GLU_MODE_GNU)
+        return a.S == 3 ? launch_t<3, GLU_MODE_GNU>(ctx, a, packed, forceFallback, nanFlag)
+                        : launch_t<5, GLU_MODE_GNU>(ctx, a, packed, forceFallback, nanFlag);
+    return a.S == 3 ? launch_t<3, GLU_MODE_FAST>(ctx, a, packed, forceFallback, nanFlag)
+                    : launch_t<5, GLU_MODE_FAST>(ctx, a, packed, forceFallback, nanFlag);
+}
+
+// Per-frame preparation in one launch: grid_downsample (grid.cpp:41-52) into
+// `low`, the packed / inf-bordered LR the solve reads, and optionally the 1-ch
+// matte target (k_op_matte's expression); raises *nanFlag like k_pack_low.
+__global__ void k_frame_prep(const float* __restrict__ high, int W, int H, int s, int lw,
+                             int lh, int h, float* __restrict__ low, float4* __restrict__ packed,
+                             float* __restrict__ matte, unsigned* nanFlag) {
+    const int pw = lw + 2 * h, ph = lh + 2 * h;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= pw * ph) return;
+    const int cy = i / pw - h, cx = i % pw - h;
+    float4 v = make_float4(kInf, kInf, kInf, 0.0f);
+    if (cx >= 0 && cy >= 0 && cx < lw && cy < lh) {
+        const int x = min(cx * s + s / 2, W - 1), y = min(cy * s + s / 2, H - 1);
+        const float* src = high + 3 * (size_t(y) * W + x);
+        v = make_float4(src[0], src[1], src[2], 0.0f);
+        const size_t c = size_t(cy) * lw + cx;
+        low[3 * c] = v.x;
+        low[3 * c + 1] = v.y;
+        low[3 * c + 2] = v.z;
+        if (matte) {
+            const double Y = 0.299 * v.x + 0.587 * v.y + 0.114 * v.z;
+            matte[c] = float(1.0 / (1.0 + exp(-10.0 * (Y - 0.5))));
+        }
+        if (v.x != v.x || v.y != v.y || v.z != v.z) atomicOr(nanFlag, 1u);
+    }
+    packed[i] = v;
+}
+
+}  // namespace
+
+cudaError_t launch_solve32(glu_ctx* ctx, const SolveArgs& a0, int forceFallback) {
+    const SolveArgs a = prepared(a0);
     const int h = a.S / 2;
     const size_t cells = size_t(a.lw + 2 * h) * (a.lh + 2 * h);
     float4* packed = static_cast<float4*>(scratch(ctx, S_PACKED, cells * sizeof(float4)));
@@ -348,12 +395,23 @@ cudaError_t launch_solve32(glu_ctx* ctx, const SolveArgs& a0, int forceFallback)
     k_pack_low<<<unsigned((cells + 255) / 256), 256, 0, ctx->stream>>>(a.low, a.lw, a.lh, h,
                                                                         packed, nanFlag);
     ++ctx->launches;
-    if (a.mode == GLU_MODE_EXACT) return launch_solve32x(ctx, a, packed, forceFallback, nanFlag);
-    if (a.mode == GLU_MODE_GNU)
-        return a.S == 3 ? launch_t<3, GLU_MODE_GNU>(ctx, a, packed, forceFallback, nanFlag)
-                        : launch_t<5, GLU_MODE_GNU>(ctx, a, packed, forceFallback, nanFlag);
-    return a.S == 3 ? launch_t<3, GLU_MODE_FAST>(ctx, a, packed, forceFallback, nanFlag)
-                    : launch_t<5, GLU_MODE_FAST>(ctx, a, packed, forceFallback, nanFlag);
+    return dispatch(ctx, a, packed, forceFallback, nanFlag);
+}
+
+cudaError_t launch_frame_solve32(glu_ctx* ctx, const SolveArgs& a0, float* low, float* matte,
+                                 int forceFallback) {
+    const SolveArgs a = prepared(a0);
+    const int h = a.S / 2;
+    const size_t cells = size_t(a.lw + 2 * h) * (a.lh + 2 * h);
+    float4* packed = static_cast<float4*>(scratch(ctx, S_PACKED, cells * sizeof(float4)));
+    if (!packed) return cudaErrorMemoryAllocation;
+    unsigned* nanFlag = reinterpret_cast<unsigned*>(ctx->d_counters + 3);
+    cudaError_t e = cudaMemsetAsync(nanFlag, 0, sizeof(unsigned), ctx->stream);
+    if (e != cudaSuccess) return e;
+    k_frame_prep<<<unsigned((cells + 255) / 256), 256, 0, ctx->stream>>>(
+        a.high, a.W, a.H, a.s, a.lw, a.lh, h, low, packed, matte, nanFlag);
+    ++ctx->launches;
+    return dispatch(ctx, a, packed, forceFallback, nanFlag);
 }
 
 }  // namespace glu_cu
