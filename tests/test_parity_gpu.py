@@ -321,3 +321,32 @@ def test_parallel_trial_schedule_matches_sequential(glu, W, H, s, S, literal, mo
             (b.iterations, b.trialsAccepted, b.trialsRejected)
         assert torch.equal(a.low, b.low) and torch.equal(a.field.params, b.field.params)
         assert torch.equal(a.errors, b.errors)
+
+
+@pytest.mark.parametrize("mode", ["fast", "gnu", "exact"])
+@pytest.mark.parametrize("target", ["matte", "identity"])
+@pytest.mark.parametrize("solver", [0, 1, 2])
+def test_frame_pipeline_matches_composed_reference_path(glu, oracle, mode, target, solver):
+    """glu_cu_upsample_frames / glu_h_upsample_frames (fused k_frame_prep +
+    solve + apply) equal the composition of the reference calls: grid_downsample
+    (grid.cpp:41-52), the matte operator, optimize_field (upsample.cpp:194-216)
+    and apply_field (235-252) -- checked against the oracle, bit for bit."""
+    from paper_2307_09582_b200 import workloads
+    W, H, s = 328, 200, 8
+    frames = np.stack([workloads.scene(W, H, 30 + k, k) for k in range(3)])
+    ctx = glu.glu.context()
+    ctx.set_solver(solver)
+    try:
+        got = glu.glu.upsample_frames(dev(frames), s, target, mode=mode_of(glu, mode)).cpu()
+        pin_in = torch.from_numpy(frames).pin_memory()
+        host = torch.empty(tuple(got.shape), dtype=torch.float32).pin_memory()
+        glu.glu.upsample_frames_host(pin_in, s, host, target, mode=mode_of(glu, mode))
+    finally:
+        ctx.set_solver(0)
+    assert torch.equal(got, host)
+    for k in range(3):
+        low = oracle.grid_downsample(frames[k], s)
+        tgt = glu.op_matte(dev(low)).cpu().numpy() if target == "matte" else low
+        P = oracle.optimize_field(frames[k], low, s, 3, EPS_DEFAULT, mode)
+        want = oracle.apply_field(P, tgt)
+        assert got[k].numpy().tobytes() == want.tobytes(), (k, mode, target)
