@@ -299,10 +299,15 @@ __global__ void __launch_bounds__(kThreads, GLU_SOLVE_MIN_BLOCKS)
         o[2] = __float_as_uint(w);
     }
     if (a.lowT) {
-        const int C = a.channels;
-        for (int k = 0; k < C; ++k)
-            a.out[C * p + k] = lerp_clamp(w, __ldg(a.lowT + size_t(C) * ia + k),
-                                          __ldg(a.lowT + size_t(C) * ib + k), a.clamp != 0);
+        const bool clamp = a.clamp != 0;
+        if (a.channels == 1) {  // the video path's matte target
+            a.out[p] = lerp_clamp(w, __ldg(a.lowT + ia), __ldg(a.lowT + ib), clamp);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                a.out[3 * p + k] = lerp_clamp(w, __ldg(a.lowT + 3 * size_t(ia) + k),
+                                              __ldg(a.lowT + 3 * size_t(ib) + k), clamp);
+        }
     }
     if (a.errOut) {  // pixel_error of the clamped self reconstruction (jointopt.cpp:190)
         float r[3];
