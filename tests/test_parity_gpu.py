@@ -350,3 +350,40 @@ def test_frame_pipeline_matches_composed_reference_path(glu, oracle, mode, targe
         P = oracle.optimize_field(frames[k], low, s, 3, EPS_DEFAULT, mode)
         want = oracle.apply_field(P, tgt)
         assert got[k].numpy().tobytes() == want.tobytes(), (k, mode, target)
+
+
+@pytest.mark.parametrize("kind", ["noise", "blocks"])
+def test_parallel_schedule_with_off_chip_and_whole_grid_trials(glu, kind):
+    """Components too large for the on-chip trial (box > 2048 cells, > 2048
+    pixels) take the global-memory path inside the speculative and dataflow
+    schedules -- in place, never speculated, invalidating speculating
+    successors -- and whole-grid trials run alone; all bit-identical to the
+    sequential loop."""
+    rng = np.random.default_rng(11)
+    if kind == "noise":
+        img = rng.random((192, 256, 3), dtype=np.float32)  # one huge component
+    else:
+        img = np.zeros((200, 240, 3), np.float32)
+        img[:, :, :] = rng.random((1, 1, 3))
+        for k in range(12):  # large noisy blocks = big components, plus small ones
+            y, x = rng.integers(0, 150), rng.integers(0, 190)
+            hh, ww = rng.integers(8, 60), rng.integers(8, 60)
+            img[y:y + hh, x:x + ww] = rng.random((hh, ww, 3))
+    high = dev(img)
+    r0 = glu.joint_optimize(high, 4, glu.GluConfig(maxIterations=0))
+    sizes = [len(c) for c in glu.find_large_error(r0.errors, glu.GluConfig().errorThreshold)
+             .components]
+    assert max(sizes) > 2048 and min(sizes) < 2048  # off-chip and on-chip trials
+    ctx = glu.glu.context()
+    out = []
+    for trials in (1, 0, 2):
+        ctx.set_trials(trials)
+        out.append(glu.joint_optimize(high, 4))
+    ctx.set_trials(0)
+    a = out[0]
+    assert a.trialsAccepted + a.trialsRejected > 0
+    for b in out[1:]:
+        assert (a.iterations, a.trialsAccepted, a.trialsRejected) == \
+            (b.iterations, b.trialsAccepted, b.trialsRejected)
+        assert torch.equal(a.low, b.low) and torch.equal(a.field.params, b.field.params)
+        assert torch.equal(a.errors, b.errors)
