@@ -319,6 +319,16 @@ def run_ours(args, ws, rank, local):
         "hbm_achieved_gbs": nbytes / (k_ms * 1e-3) / 1e9,
         "peak_source": f"FFMA probe in this run ({fp32_mhz:.0f} MHz implied)",
     }
+    winstr = load_traffic().get("solve_apply_fast_c3_warp_instr") if args.mode == "fast" else None
+    if winstr:
+        # The kernel is instruction-issue bound: the floor of its executed
+        # instruction stream (ncu count per launch, profiles/) at 4 warp
+        # instructions / cycle / SM, at the clock the FFMA probe measured.
+        sms = torch.cuda.get_device_properties(local).multi_processor_count
+        floor_ms = winstr / (4 * sms * fp32_mhz * 1e6) * 1e3
+        roofline["issue_bound"] = {
+            "warp_instr_per_launch": winstr, "floor_ms": floor_ms,
+            "frac": floor_ms / k_ms, "source": "profiles/r01_ncu_solve32.md (ncu --set full)"}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             hbm = json.load(fh)["hbm_gbs"]

@@ -125,6 +125,8 @@ def kernel(rep: str, out: str, traffic_key: str | None) -> None:
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         d = json.load(open(tp)) if os.path.exists(tp) else {}
         d[traffic_key] = dram_r + dram_w
+        if tot:  # executed warp instructions per launch (bench.py's issue bound)
+            d[traffic_key + "_warp_instr"] = tot
         json.dump(d, open(tp, "w"), indent=1)
 
 
