@@ -29,6 +29,7 @@
 // double sums (150-165): the CTA forms parallel fp64 sums and decides when
 // |e1 - e0| exceeds a rigorous bound on parallel-vs-sequential rounding;
 // otherwise one thread redoes both sums in the exact reference order.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
@@ -50,6 +51,18 @@ constexpr uint32_t kNone = 0xffffffffu;
 #define GLU_SCHED_THREADS 512
 #endif
 constexpr int kSchedThreads = GLU_SCHED_THREADS;  // CTA size of the parallel trial scheduler
+// A scheduled trial can run on a cluster of kCS CTAs (one per SM): each CTA
+// stages the trial's window and offsets itself, the re-solve and the commit
+// are split between them, partial sums meet in distributed shared memory.
+// Measured (C2 / C4 joint): kCS = 1 2.43 / 3.65 ms, 2 2.64 / 3.56 ms, 4 3.56 /
+// 4.49 ms -- a trial's latency is dominated by its staging, scans and
+// barriers, not the re-solve, while clusters halve the trials in flight; so
+// one CTA per trial is the default.
+#ifndef GLU_TRIAL_CLUSTER
+#define GLU_TRIAL_CLUSTER 1
+#endif
+constexpr int kCS = GLU_TRIAL_CLUSTER;
+static_assert(kCS == 1 || kCS == 2 || kCS == 4, "trial cluster of 1, 2 or 4 CTAs");
 constexpr int kSeqThreads = 1024;    // CTA size of the sequential (single-CTA) sweep
 // Per-CTA private trial buffers (one 512-thread CTA per SM): a diagonal 200-pixel line
 // at s = 8 has a 27 x 27-cell dilated box (46,656 pixels), so 64 Ki pixels
@@ -189,6 +202,28 @@ __global__ void k_sparse_keys(const uint32_t* __restrict__ parent, const uint32_
 
 // ---- trials -------------------------------------------------------------------
 
+__device__ __forceinline__ unsigned cluster_rank() {
+    return kCS > 1 ? cooperative_groups::this_cluster().block_rank() : 0u;
+}
+// Barrier over the trial's cluster (release / acquire at cluster scope: the
+// CTAs' global and shared writes before it are visible to all after it).
+__device__ __forceinline__ void cluster_barrier() {
+    if (kCS > 1)
+        cooperative_groups::this_cluster().sync();
+    else
+        __syncthreads();
+}
+// `v` into the same shared variable of every CTA of the cluster.
+template <typename T>
+__device__ __forceinline__ void cluster_bcast(T* var, T v) {
+    if (kCS > 1) {
+        auto cl = cooperative_groups::this_cluster();
+        for (unsigned r = 0; r < unsigned(kCS); ++r) *cl.map_shared_rank(var, r) = v;
+    } else {
+        *var = v;
+    }
+}
+
 #ifdef GLU_SCHED_TRACE
 // Development builds only (-DGLU_SCHED_TRACE): per trial {claim, ready, end}
 // %globaltimer stamps, dumped by run_sched to $GLU_SCHED_TRACE_FILE, and SM
@@ -201,7 +236,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return v;
 }
 #define GLU_PHASE(k)                                            \
-    if (threadIdx.x == 0) {                                     \
+    if (threadIdx.x == 0 && cluster_rank() == 0) {              \
         const long long c_ = clock64();                         \
         atomicAdd(&g_phase[k], (unsigned long long)(c_ - tph)); \
         tph = c_;                                               \
@@ -718,11 +753,16 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
                               uint32_t n, const SuccScan& sc, uint32_t* park = nullptr) {
     using BlockScan = typename TrialSmem<NT>::BlockScan;
     __shared__ double red[2][NT / 32];
+    __shared__ double xred[kCS][3];  // per-CTA partials {e0, e1, changed} of the cluster
     // park != nullptr (speculative run): the result goes to the trial's parked
     // record {verdict, nt, na, na x {p, a, b, w, e}, nt x {cell, r, g, b}}
     // instead of this CTA's buffers; see k_trial_sched.
     uint32_t* parkPix = park ? park + 3 : nullptr;
     const int tid = threadIdx.x;
+    // Every CTA of the cluster stages the trial (phases A-C) in its own shared
+    // memory; the affected pixels are split in blocks of NT (pixel i goes to
+    // CTA (i / NT) % kCS) and the partial sums meet in distributed shared memory.
+    const uint32_t rank = cluster_rank();
     const int h = t.S / 2;
     const uint32_t W = uint32_t(t.W), s = uint32_t(t.s);
 #ifdef GLU_SCHED_TRACE
@@ -748,7 +788,7 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
             (static_cast<unsigned long long>(__float_as_uint(e)) << 32) | (0xffffffffu - i);
         atomicMax(ss.key + (cy - g.qy0) * g.qw + (cx - g.qx0), key);
     }
-    if (sc.list) {
+    if (sc.list && rank == 0) {
         // conflicting successors among the next NT trials (loads overlap the
         // staging above); one waiting on this trial alone is worth speculating
         const int j = sc.self + 1 + tid;
@@ -829,13 +869,14 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
         q.i2 = t.high[3 * size_t(q.p) + 2];
         return q;
     };
+    constexpr uint32_t kStride = uint32_t(kCS) * NT;
     PixIn cur{};
-    if (uint32_t(tid) < na) cur = load(tid);
+    if (rank * NT + tid < na) cur = load(rank * NT + tid);
     double part0 = 0, part1 = 0;
     bool changed = false;
-    for (uint32_t i = tid; i < na; i += NT) {
+    for (uint32_t i = rank * NT + tid; i < na; i += kStride) {
         PixIn nxt{};
-        if (i + NT < na) nxt = load(i + NT);
+        if (i + kStride < na) nxt = load(i + kStride);
         const uint32_t p = cur.p;
         const int cx = cur.cx, cy = cur.cy;
         const float oe = cur.oe;
@@ -927,12 +968,26 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
         red[0][tid >> 5] = part0;
         red[1][tid >> 5] = part1;
     }
-    const bool anyChanged = __syncthreads_or(changed);
+    const bool anyChangedCta = __syncthreads_or(changed);
     if (tid == 0) {
         double s0 = 0, e1 = 0;
         for (int k = 0; k < NT / 32; ++k) {
             s0 += red[0][k];
             e1 += red[1][k];
+        }
+        cluster_bcast(&xred[rank][0], s0);
+        cluster_bcast(&xred[rank][1], e1);
+        cluster_bcast(&xred[rank][2], anyChangedCta ? 1.0 : 0.0);
+    }
+    cluster_barrier();  // partials (and every CTA's new values in b / park) visible
+    if (tid == 0) {
+        // the same sums in the same order in every CTA: the same verdict
+        double s0 = 0, e1 = 0;
+        bool anyChanged = false;
+        for (int r = 0; r < kCS; ++r) {
+            s0 += xred[r][0];
+            e1 += xred[r][1];
+            anyChanged |= xred[r][2] != 0.0;
         }
         const double bound = 4.0 * (double(na) + 64.0) * 0x1.0p-53 * (s0 + e1);
         if (!anyChanged || e1 + bound < s0)
@@ -966,7 +1021,7 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
         }
         if (tid == 0) {
             sm.verdict = q1 <= q0;
-            atomicAdd(t.result + 2, 1);
+            if (rank == 0) atomicAdd(t.result + 2, 1);
         }
         __syncthreads();
     }
@@ -975,7 +1030,7 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
         sm.touched = nt;
         sm.base = na;
     }
-    if (park) {
+    if (park && rank == 0) {
         if (tid == 0) {
             park[0] = uint32_t(verdict);
             park[1] = nt;
@@ -1005,26 +1060,28 @@ template <int NT>
 __device__ void commit_trial_smem(const TrialState& t, const TrialBuffers& b, TrialSmem<NT>& sm,
                                   const TrialShared& ss, const TrialGeom& g) {
     const int tid = threadIdx.x;
-    const uint32_t nt = sm.touched, na = sm.base;
+    const uint32_t nt = sm.touched, na = sm.base, rank = cluster_rank();
 #ifdef GLU_SCHED_TRACE
     long long tph = clock64();
 #endif
-    for (uint32_t i = tid; i < nt; i += NT) {
-        const int k = int(ss.touched[i]);
-        const int qx = g.qx0 + k % g.qw, qy = g.qy0 + k / g.qw;
-        const float4 c = ss.win[(qy - g.vy0) * g.vw + (qx - g.vx0)];
-        float* lc = t.low + 3 * (size_t(qy) * t.lw + qx);
-        lc[0] = c.x;
-        lc[1] = c.y;
-        lc[2] = c.z;
-    }
-    for (uint32_t i = tid; i < na; i += NT) {
+    if (rank == 0)
+        for (uint32_t i = tid; i < nt; i += NT) {
+            const int k = int(ss.touched[i]);
+            const int qx = g.qx0 + k % g.qw, qy = g.qy0 + k / g.qw;
+            const float4 c = ss.win[(qy - g.vy0) * g.vw + (qx - g.vx0)];
+            float* lc = t.low + 3 * (size_t(qy) * t.lw + qx);
+            lc[0] = c.x;
+            lc[1] = c.y;
+            lc[2] = c.z;
+        }
+    // each CTA commits the pixels it solved
+    for (uint32_t i = rank * NT + tid; i < na; i += uint32_t(kCS) * NT) {
         int cx, cy;
         const uint32_t p = affected_pixel(t, g, ss, i, cx, cy);
         t.field[p] = b.bkParams[i];
         t.errors[p] = b.bkE[i];
     }
-    if (t.dCount) {
+    if (t.dCount && rank == 0) {
         if (tid == 0) {
             sm.logCells = atomicAdd(t.dCount, nt);
             sm.logPixels = atomicAdd(t.dCount + 1, na);
@@ -1066,19 +1123,20 @@ __device__ void commit_trial_smem(const TrialState& t, const TrialBuffers& b, Tr
 template <int NT>
 __device__ int commit_parked(const TrialState& t, TrialSmem<NT>& sm, const uint32_t* park) {
     const int tid = threadIdx.x;
+    const uint32_t rank = cluster_rank();
     const int verdict = int(park[0]);
     const uint32_t nt = park[1], na = park[2];
     const uint32_t* pix = park + 3;
     const uint32_t* cells = pix + 5 * size_t(na);
     if (verdict) {
-        for (uint32_t i = tid; i < nt; i += NT) {
+        for (uint32_t i = rank * NT + tid; i < nt; i += uint32_t(kCS) * NT) {
             const uint32_t* c = cells + 4 * size_t(i);
             float* lc = t.low + 3 * size_t(c[0]);
             lc[0] = __uint_as_float(c[1]);
             lc[1] = __uint_as_float(c[2]);
             lc[2] = __uint_as_float(c[3]);
         }
-        for (uint32_t i = tid; i < na; i += NT) {
+        for (uint32_t i = rank * NT + tid; i < na; i += uint32_t(kCS) * NT) {
             const uint32_t* q = pix + 5 * size_t(i);
             glu_pixel_params pp;
             pp.a = q[1];
@@ -1087,7 +1145,7 @@ __device__ int commit_parked(const TrialState& t, TrialSmem<NT>& sm, const uint3
             t.field[q[0]] = pp;
             t.errors[q[0]] = __uint_as_float(q[4]);
         }
-        if (t.dCount) {
+        if (t.dCount && rank == 0) {
             if (tid == 0) {
                 sm.logCells = atomicAdd(t.dCount, nt);
                 sm.logPixels = atomicAdd(t.dCount + 1, na);
@@ -1270,8 +1328,11 @@ __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
     __shared__ int sIdx, sMode, sUse;
     extern __shared__ __align__(16) char dyn[];
     const TrialShared ss = TrialShared::carve(dyn);
-    // this CTA's private buffers
-    char* mine = ctaBufs + size_t(blockIdx.x) *
+    // The cluster's private buffers (one set per cluster).  CTA rank 0 of the
+    // cluster schedules; every CTA of the cluster runs the trial.
+    const uint32_t rank = cluster_rank();
+    const bool lead = rank == 0;
+    char* mine = ctaBufs + size_t(blockIdx.x / kCS) *
                                (size_t(kCtaCells) * 16 + size_t(kCtaPixels) * 20);
     TrialBuffers local;
     local.touched = reinterpret_cast<uint32_t*>(mine);
@@ -1287,7 +1348,7 @@ __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
     if (threadIdx.x == 0) sNext = -1;
     enum { kExit = 0, kRun = 1, kSpec = 2 };
     for (;;) {
-        if (threadIdx.x == 0) {
+        if (lead && threadIdx.x == 0) {
             int i = sNext, mode = kRun;
 #ifdef GLU_SCHED_TRACE
             const unsigned long long tc = gtimer();
@@ -1341,13 +1402,13 @@ __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
                 g_trace[3 * i + 1] = gtimer();
             }
 #endif
-            sIdx = i;
-            sMode = mode;
+            cluster_bcast(&sIdx, i);
+            cluster_bcast(&sMode, mode);
             sNext = -1;
             sCount = 0;
             sMore = 1;
         }
-        __syncthreads();
+        cluster_barrier();
         const int i = sIdx, mode = sMode;
         if (mode == kExit) break;
         __threadfence();  // acquire: the predecessors' committed writes are visible
@@ -1370,18 +1431,19 @@ __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
                 if (threadIdx.x == 0) atomicAdd(&g_phase[18], 1ull);
 #endif
             }
-            if (threadIdx.x == 0) {
+            cluster_barrier();  // every CTA's share of the record is written
+            if (lead && threadIdx.x == 0) {
 #ifdef GLU_SCHED_TRACE
                 g_trace[3 * ncomp + 2 * i + 1] = gtimer();
 #endif
                 __threadfence();
                 atomicCAS(specState + i, 1, onChip ? 2 : 3);  // 2: record parked
             }
-            __syncthreads();
+            cluster_barrier();
             continue;
         }
         // mode == kRun: all conflicting predecessors are final
-        if (threadIdx.x == 0) {
+        if (lead && threadIdx.x == 0) {
             int use = 0;
             if (spec) {
                 int st = ld_relaxed(specState + i);
@@ -1401,10 +1463,10 @@ __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
                     use = acc == specSnap[i];
                 }
             }
-            sUse = use;
+            cluster_bcast(&sUse, use);
         }
-        __syncthreads();
-        int v;
+        cluster_barrier();
+        int v = 0;
         bool dirty = false;
         if (sUse) {
             v = commit_parked<kSchedThreads>(t, sm, parkBuf + parkOff[i]);
@@ -1418,9 +1480,11 @@ __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
             v = run_trial_smem<kSchedThreads>(t, local, sm, ss, geo, px + off[c], n, sc);
             if (v) commit_trial_smem<kSchedThreads>(t, local, sm, ss, geo);
         } else {
-            v = run_trial<kSchedThreads>(t, isBig ? big : local, sm, px + off[c], n);
+            if (lead) v = run_trial<kSchedThreads>(t, isBig ? big : local, sm, px + off[c], n);
             dirty = true;  // wrote in place (and rolled back if rejected)
         }
+        cluster_barrier();  // the trial's writes, from every CTA, are complete
+        if (!lead) continue;
         if (threadIdx.x == 0) {
             atomicAdd(t.result + (v ? 0 : 1), 1);
 #ifdef GLU_SCHED_TRACE
@@ -1529,6 +1593,7 @@ TrialState trial_state(const float* high, float* low, glu_pixel_params* field, f
     return t;
 }
 
+// Resident CTAs of the persistent scheduler: whole clusters of kCS CTAs.
 template <typename K>
 int sched_grid(glu_ctx* ctx, K kernel) {
     static thread_local int cached = -1, cachedDev = -1;
@@ -1539,8 +1604,49 @@ int sched_grid(glu_ctx* ctx, K kernel) {
                          int(kTrialSmemBytes));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, kSchedThreads, kTrialSmemBytes);
     cached = sms * std::max(1, std::min(per, 2));
+    if (kCS > 1) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(unsigned(cached));
+        cfg.blockDim = dim3(kSchedThreads);
+        cfg.dynamicSmemBytes = kTrialSmemBytes;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = kCS;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int clusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&clusters, kernel, &cfg) == cudaSuccess && clusters > 0)
+            cached = std::min(cached, clusters * kCS) / kCS * kCS;
+        else
+            cached = cached / kCS * kCS;
+        cudaGetLastError();
+    }
     cachedDev = ctx->device;
     return cached;
+}
+
+// Cooperative launch of the persistent scheduler in clusters of kCS CTAs.
+cudaError_t launch_persistent(const void* kernel, int grid, void** args, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(kSchedThreads);
+    cfg.dynamicSmemBytes = kTrialSmemBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    at[na].id = cudaLaunchAttributeCooperative;
+    at[na++].val.cooperative = 1;
+    if (kCS > 1) {
+        at[na].id = cudaLaunchAttributeClusterDimension;
+        at[na].val.clusterDim.x = kCS;
+        at[na].val.clusterDim.y = 1;
+        at[na++].val.clusterDim.z = 1;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelExC(&cfg, kernel, args);
 }
 
 #ifdef GLU_SCHED_TRACE
@@ -1653,8 +1759,7 @@ int run_sched(glu_ctx* ctx, const TrialState& t, const JointScratch& js, const g
 #ifdef GLU_SCHED_TRACE
     unsigned long long* trace = trace_begin(ctx, n);
 #endif
-    e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_trial_sched), grid, kSchedThreads,
-                                    args, kTrialSmemBytes, st);
+    e = launch_persistent(reinterpret_cast<const void*>(k_trial_sched), grid, args, st);
     ++ctx->launches;
     if (e != cudaSuccess) return fail_cuda(e, "trial schedule");
 #ifdef GLU_SCHED_TRACE
