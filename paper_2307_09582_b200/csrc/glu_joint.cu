@@ -790,18 +790,10 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
     }
     if (sc.list && rank == 0) {
         // conflicting successors among the next NT trials (loads overlap the
-        // staging above); one waiting on this trial alone is worth speculating
+        // staging above)
         const int j = sc.self + 1 + tid;
-        if (j < sc.ncomp && boxes_conflict(sc.box, sc.boxes[j], sc.reach)) {
+        if (j < sc.ncomp && boxes_conflict(sc.box, sc.boxes[j], sc.reach))
             sc.list[atomicAdd(sc.count, 1)] = j;
-            if (sc.specQ && uint32_t(ld_relaxed64(sc.pred + j)) == 1 &&
-                atomicCAS(sc.specState + j, 0, 7) == 0) {
-                st_release(sc.specQ + atomicAdd(sc.specTail, 1), j);
-#ifdef GLU_SCHED_TRACE
-                atomicAdd(&g_phase[19], 1ull);
-#endif
-            }
-        }
         if (tid == 0)
             *sc.more = sc.self + 1 + NT < sc.ncomp && sc.sufTop[sc.self + 1 + NT] <= sc.box.w + sc.reach;
     }
