@@ -93,3 +93,20 @@ def test_cpp_dropin_io_api(glu, tmp_path):
     r = subprocess.run([str(exe), str(tmp_path / "x.glup")], capture_output=True, text=True,
                        timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_dropin_api_concurrent_host_threads(tmp_path):
+    """The drop-in C++ API from four std::threads at once (thread-local contexts
+    and streams) gives the single-threaded results bit for bit: optimize_field,
+    apply_field and joint_optimize (SURVEY 8(b) threading contract)."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(root, "paper_2307_09582_b200", "lib")
+    exe = tmp_path / "dropin_threads_test"
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I" + os.path.join(root, "include"),
+                    os.path.join(root, "tests", "cpp", "dropin_threads_test.cpp"), "-L" + lib,
+                    "-lglu", "-lglu_cuda", "-Wl,-rpath," + lib, "-pthread", "-o", str(exe)],
+                   check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
