@@ -145,6 +145,10 @@ def test_scalar_pins(glu):
 CASES = [  # (W, H, s, S, seed): ragged sizes, every supported window class
     (131, 77, 4, 3, 11), (200, 120, 8, 3, 12), (97, 203, 3, 5, 13), (160, 90, 5, 7, 14),
     (64, 64, 2, 9, 15), (257, 129, 16, 3, 16), (33, 300, 6, 11, 17),
+    # degenerate geometries: 2 x N / N x 2 LR grids, one-cell-wide LR, scale 32,
+    # tiles narrower than a warp, windows wider than the LR grid
+    (33, 5, 4, 3, 18), (7, 300, 3, 5, 19), (1000, 9, 8, 3, 20), (257, 129, 32, 5, 21),
+    (5, 5, 2, 3, 22), (17, 200, 16, 7, 23), (96, 64, 2, 3, 24),
 ]
 
 
@@ -190,12 +194,15 @@ def test_single_channel_apply_matches_rgb(glu, oracle):
     assert same(fused.cpu().numpy(), one)
 
 
-def test_joint_vs_oracle_seeded(glu, oracle):
+@pytest.mark.parametrize("mode", ["fast", "gnu", "exact"])
+def test_joint_vs_oracle_seeded(glu, oracle, mode):
     from paper_2307_09582_b200 import workloads
-    for (W, H, s, seed) in ((256, 192, 8, 21), (300, 170, 6, 22)):
+    # regular, ragged, tall-thin, scale-2 and scale-32 grids
+    for (W, H, s, seed) in ((256, 192, 8, 21), (300, 170, 6, 22), (40, 260, 4, 23),
+                            (130, 90, 2, 24), (400, 200, 32, 25)):
         img = workloads.scene(W, H, seed)
-        r = glu.joint_optimize(dev(img), s)
-        o = oracle.joint_optimize(img, s)
+        r = glu.joint_optimize(dev(img), s, None, mode_of(glu, mode))
+        o = oracle.joint_optimize(img, s, mode=mode)
         assert [r.iterations, r.trialsAccepted, r.trialsRejected] == \
             [o["iterations"], o["accepted"], o["rejected"]]
         assert same(r.low.cpu().numpy(), o["low"])
