@@ -29,6 +29,7 @@ constexpr int kTX = 32, kTY = 8, kThreads = kTX * kTY;
 constexpr int kPairs = 36;       // i < j over 9 candidates
 constexpr int kCellStride = 37;  // float4 per owner cell (592 B: bank-spread)
 constexpr int kMaxCells = 48;    // (31/3 + 2) x (7/3 + 2) owner cells for s >= 3
+constexpr int kMaxWinCells = 96;  // their candidate cells: (ncw + 2) x (nch + 2) <= 14 x 6
 constexpr float kU = 5.9604645e-08f;
 constexpr float kCE = 64.0f;  // objective error bound, in u * |e_j|^2
 constexpr float kCA = 32.0f;
@@ -69,13 +70,14 @@ __device__ __forceinline__ void pair_ij(int k, int& i, int& j) {
 }
 
 #ifndef GLU_X_MIN_BLOCKS
-#define GLU_X_MIN_BLOCKS 3  // 80 registers: 24 warps per SM (0.49 -> 0.44 ms per 4K frame)
+#define GLU_X_MIN_BLOCKS 6  // 40 registers: 48 warps per SM
 #endif
 __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS) k_solve32x(SolveArgs a, const float4* packed,
                                                           int forceFallback,
                                                           const unsigned* nanFlag) {
     forceFallback |= int(__ldg(nanFlag));
     __shared__ float4 table[kMaxCells * kCellStride];
+    __shared__ float4 wcells[kMaxWinCells];  // the tile's candidate cells (owner cells +- 1)
     const int pw = a.lw + 2;  // h = 1
     const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
     const int ocx0 = div_s(x0, a), ocy0 = div_s(y0, a);
@@ -93,6 +95,9 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS) k_solve32x(SolveAr
         const float den = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmaf_rn(d0, d0, eps)));
         table[cell * kCellStride + pr] = make_float4(d0, d1, d2, rcp_approx(den));
     }
+    const int cw = ncw + 2;
+    for (int k = threadIdx.x; k < cw * (nch + 2); k += kThreads)
+        wcells[k] = __ldg(packed + size_t(ocy0 + k / cw) * pw + (ocx0 + k % cw));
     __syncthreads();
 
     const int x = x0 + (threadIdx.x % kTX), y = y0 + (threadIdx.x / kTX);
@@ -100,102 +105,118 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS) k_solve32x(SolveAr
     const size_t p = size_t(y) * a.W + x;
     const int cx = div_s(x, a), cy = div_s(y, a);
     const float4* win = packed + size_t(cy) * pw + cx;
+    // the same window in shared memory: candidate j is swin[(j / 3) * cw + j % 3]
+    const float4* swin = wcells + (cy - ocy0) * cw + (cx - ocx0);
     const float4* tab = table + ((cy - ocy0) * ncw + (cx - ocx0)) * kCellStride;
     const float ip0 = __ldg(a.high + 3 * p), ip1 = __ldg(a.high + 3 * p + 1),
                 ip2 = __ldg(a.high + 3 * p + 2);
 
-    float e0[9], e1[9], e2[9], q[9];
-    float qmin = kInf;
+    // j-outer scan: pair (i, j) needs only e_j = I_j - I_p and q_j = |e_j|^2
+    // (D_ij and 1/den come from the cell's table), so nothing per candidate
+    // stays live across the scan.  Track the strict argmin b1 (pair bk =
+    // i << 4 | j) and, for the close-call test, t = o - E per pair (E = kCE u
+    // q_j + 1e-36, its error bound): m2 = min of t over the pairs that are not
+    // the current best, bme = the best pair's t.  This order is not the
+    // reference's lexicographic (i <= j) order, so among exactly tied pairs
+    // the lexicographic first is recovered below (exact zeros directly, other
+    // ties in the re-check of close calls).
+    constexpr float kE = kCE * kU;
+    float qmin = kInf, b1 = kInf, m2 = kInf, bme = kInf;
+    int bk = 0, i0 = -1, j0 = -1;
 #pragma unroll
-    for (int k = 0; k < 9; ++k) {
-        const float4 v = __ldg(win + (k / 3) * pw + k % 3);
-        e0[k] = v.x - ip0;
-        e1[k] = v.y - ip1;
-        e2[k] = v.z - ip2;
-        q[k] = __fmaf_rn(e2[k], e2[k], __fmaf_rn(e1[k], e1[k], __fmul_rn(e0[k], e0[k])));
-        qmin = fminf(qmin, q[k]);
-    }
-    // lexicographic scan over (i <= j), first strict argmin.  Alongside, m2
-    // = min over the other pairs of (o - E), E = the pair's error bound
-    // (kCE u q_j), and eb = the best pair's bound: a close call exists only
-    // if m2 <= b1 + eb, so the per-pair re-check below runs just for those.
-    float qe[9];
+    for (int j = 0; j < 9; ++j) {
+        const float4 v = swin[(j / 3) * cw + j % 3];
+        const float e0 = v.x - ip0, e1 = v.y - ip1, e2 = v.z - ip2;
+        const float qj = __fmaf_rn(e2, e2, __fmaf_rn(e1, e1, __fmul_rn(e0, e0)));
+        const float qej = __fmaf_rn(kE, qj, 1e-36f);
+        qmin = fminf(qmin, qj);
+        i0 = (i0 < 0 && qj < kInf) ? j : i0;    // first in-grid candidate
+        j0 = (j0 < 0 && qj == 0.0f) ? j : j0;  // first exact colour match
 #pragma unroll
-    for (int k = 0; k < 9; ++k) qe[k] = __fmaf_rn(kCE * kU, q[k], 1e-36f);
-    float b1 = kInf, m2 = kInf, eb = 0.0f;
-    int bi = 0, bj = 0;
-    {
-        int pr = 0;
-#pragma unroll
-        for (int i = 0; i < 9; ++i) {
-            {
-                const float o = q[i];  // (i, i): w = 0
-                const bool lt = o < b1;
-                m2 = lt ? fminf(m2, b1 - eb) : fminf(m2, o - qe[i]);
-                eb = lt ? qe[i] : eb;
-                b1 = lt ? o : b1;
-                bi = lt ? i : bi;
-                bj = lt ? i : bj;
-            }
-#pragma unroll
-            for (int j = i + 1; j < 9; ++j, ++pr) {
-                const float4 t = tab[pr];
-                const float num = -__fmaf_rn(e0[j], t.x, __fmaf_rn(e1[j], t.y, e2[j] * t.z));
-                const float o = __fmaf_rn(-num * num, t.w, q[j]);
-                const bool lt = o < b1;
-                m2 = lt ? fminf(m2, b1 - eb) : fminf(m2, o - qe[j]);
-                eb = lt ? qe[j] : eb;
-                b1 = lt ? o : b1;
-                bi = lt ? i : bi;
-                bj = lt ? j : bj;
-            }
+        for (int i = 0; i < j; ++i) {
+            const float4 t = tab[i * 8 - i * (i - 1) / 2 + (j - i - 1)];
+            const float num = -__fmaf_rn(e0, t.x, __fmaf_rn(e1, t.y, e2 * t.z));
+            const float o = __fmaf_rn(-num * num, t.w, qj);
+            const float tt = o - qej;
+            const bool lt = o < b1;
+            m2 = fminf(m2, lt ? bme : tt);
+            bme = lt ? tt : bme;
+            b1 = lt ? o : b1;
+            bk = lt ? (i << 4 | j) : bk;
+        }
+        {
+            const float o = qj;  // (j, j): w = 0
+            const float tt = o - qej;
+            const bool lt = o < b1;
+            m2 = fminf(m2, lt ? bme : tt);
+            bme = lt ? tt : bme;
+            b1 = lt ? o : b1;
+            bk = lt ? (j << 4 | j) : bk;
         }
     }
-    const float4 ci = __ldg(win + (bi / 3) * pw + bi % 3), cj = __ldg(win + (bj / 3) * pw + bj % 3);
+    int bi = bk >> 4, bj = bk & 15;
+    float4 ci = swin[(bi / 3) * cw + bi % 3], cj = swin[(bj / 3) * cw + bj % 3];
+    // the best pair's bound E_best (the same q_bj as in the scan)
+    const float eb0 = cj.x - ip0, eb1 = cj.y - ip1, eb2 = cj.z - ip2;
+    const float eb = __fmaf_rn(kE, __fmaf_rn(eb2, eb2, __fmaf_rn(eb1, eb1, __fmul_rn(eb0, eb0))),
+                               1e-36f);
     bool ok = !forceFallback && b1 < kInf && ip0 == ip0 && ip1 == ip1 && ip2 == ip2 &&
               (qmin >= 1e-27f || qmin == 0.0f);
     // An exact zero with I_bj == I_p is exact in double too (w = 0, v = 0);
-    // every other true zero also has e_j = 0 and evaluates to exactly 0 in
-    // fp32, so the first zero in lexicographic order is the reference's pick.
-    // (Every LR sample pixel lands here: all pairs (i, k) with I_k = I_p tie.)
+    // every true zero is a pair (i, j) with e_j = 0, which evaluates to exactly
+    // 0 in fp32, so the reference's pick is the lexicographically first: (i0,
+    // j0), i0 the first in-grid candidate, j0 the first exact colour match.
+    // (Every LR sample pixel lands here.)
     const bool exactZero = b1 == 0.0f && cj.x == ip0 && cj.y == ip1 && cj.z == ip2;
+    if (exactZero && j0 >= 0) {
+        bi = i0;
+        bj = j0;
+        ci = swin[(bi / 3) * cw + bi % 3];
+        cj = swin[(bj / 3) * cw + bj % 3];
+    }
     bool wSet = false;  // w settled in double over the close set
     float wClose = 0.0f;
     if (ok && !exactZero && m2 <= b1 + eb) {
-        // rare: per-pair bounds.  The close pairs (bit k = lexicographic pair
-        // k, the winner included) hold the reference's first argmin: if they
-        // all carry the winner's colours the fp32 pick stands; otherwise they
-        // are evaluated in double, in lexicographic order.
+        // rare: per-pair bounds, in lexicographic order.  The close pairs
+        // (bit k = lexicographic pair k, the winner included) hold the
+        // reference's first argmin: if they all carry the winner's colour
+        // tuple, the first of them is the pick; otherwise they are evaluated in
+        // double, in lexicographic order.
         unsigned long long close = 0;
         bool mixed = false;
-        int pr = 0, k = 0;
-#pragma unroll
+        int fi = -1, fj = -1, k = 0;
+#pragma unroll 1
         for (int i = 0; i < 9; ++i) {
-#pragma unroll
+            const float4 vi = swin[(i / 3) * cw + i % 3];
+            const bool ini = vi.x < kInf;  // the +inf sentinel marks off-grid cells
+#pragma unroll 1
             for (int j = i; j < 9; ++j, ++k) {
-                float o;
-                if (j == i) {
-                    o = q[i];
-                } else {
-                    const float4 t = tab[pr++];
-                    const float num = -__fmaf_rn(e0[j], t.x, __fmaf_rn(e1[j], t.y, e2[j] * t.z));
-                    o = __fmaf_rn(-num * num, t.w, q[j]);
+                const float4 vj = swin[(j / 3) * cw + j % 3];
+                const float e0 = vj.x - ip0, e1 = vj.y - ip1, e2 = vj.z - ip2;
+                const float qj = __fmaf_rn(e2, e2, __fmaf_rn(e1, e1, __fmul_rn(e0, e0)));
+                float o = qj;
+                if (j != i) {
+                    const float4 t = tab[i * 8 - i * (i - 1) / 2 + (j - i - 1)];
+                    const float num = -__fmaf_rn(e0, t.x, __fmaf_rn(e1, t.y, e2 * t.z));
+                    o = __fmaf_rn(-num * num, t.w, qj);
                 }
-                if (i == bi && j == bj) {
-                    close |= 1ull << k;
-                    continue;
-                }
-                if (!(o <= kInf)) continue;  // NaN: outside the grid
-                if (o - qe[j] <= b1 + eb) {
-                    const float4 vi = __ldg(win + (i / 3) * pw + i % 3);
-                    const float4 vj = __ldg(win + (j / 3) * pw + j % 3);
-                    if (!(q[i] < kInf && q[j] < kInf)) ok = false;  // off-grid member
-                    close |= 1ull << k;
-                    mixed |= !(same_rgb(vi, ci) && same_rgb(vj, cj));
+                const bool best = i == bi && j == bj;
+                if (!best && (!(o <= kInf) || !(o - __fmaf_rn(kE, qj, 1e-36f) <= b1 + eb)))
+                    continue;  // not close (NaN: outside the grid)
+                if (!(ini && qj < kInf)) ok = false;  // off-grid member
+                close |= 1ull << k;
+                const bool same = same_rgb(vi, ci) && same_rgb(vj, cj);
+                mixed |= !same;
+                if (same && fi < 0) {
+                    fi = i;
+                    fj = j;
                 }
             }
         }
-        if (ok && mixed) {
+        if (ok && !mixed) {
+            bi = fi;  // identical colours: identical objectives and weight
+            bj = fj;
+        } else if (ok && mixed) {
             const float ip[3] = {ip0, ip1, ip2};
             double best = 0, bw = 0;
             int ni = -1, nj = -1;
@@ -203,8 +224,8 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS) k_solve32x(SolveAr
 #pragma unroll 1
             for (int kk = 0; kk < 45; ++kk) {
                 if (close >> kk & 1ull) {
-                    const float4 vi = __ldg(win + (i / 3) * pw + i % 3);
-                    const float4 vj = __ldg(win + (j / 3) * pw + j % 3);
+                    const float4 vi = swin[(i / 3) * cw + i % 3];
+                    const float4 vj = swin[(j / 3) * cw + j % 3];
                     const float a3[3] = {vi.x, vi.y, vi.z}, b3[3] = {vj.x, vj.y, vj.z};
                     const double wv = weight_exact64(ip, a3, b3, a.eps);
                     const double o = objective64(ip, a3, b3, wv, a.eps);
@@ -226,8 +247,13 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS) k_solve32x(SolveAr
     }
     // stage-A style guard: an exact-zero distance must be a true colour match
     if (ok && qmin == 0.0f) {
-        for (int k = 0; k < 9; ++k)
-            if (q[k] == 0.0f && !(e0[k] == 0.0f && e1[k] == 0.0f && e2[k] == 0.0f)) ok = false;
+#pragma unroll 1
+        for (int k = 0; k < 9; ++k) {
+            const float4 v = swin[(k / 3) * cw + k % 3];
+            const float e0 = v.x - ip0, e1 = v.y - ip1, e2 = v.z - ip2;
+            const float qk = __fmaf_rn(e2, e2, __fmaf_rn(e1, e1, __fmul_rn(e0, e0)));
+            if (qk == 0.0f && !(e0 == 0.0f && e1 == 0.0f && e2 == 0.0f)) ok = false;
+        }
     }
     (void)kCA;
     uint32_t ia, ib;
