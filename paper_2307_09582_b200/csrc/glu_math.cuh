@@ -64,6 +64,20 @@ GLU_HD double weight_exact64(const float* ip, const float* ia, const float* ib, 
     return num / (den + eps);
 }
 
+// (float)weight_exact64 with a zero numerator short-cut: num = +-0 (an exact
+// colour match I_b = I_p, e.g. every LR sample pixel) gives +-0 / (den + eps)
+// = num, bit for bit, without the IEEE division's special-case path.
+GLU_HD float weight_exact64_f(const float* ip, const float* ia, const float* ib, double eps) {
+    double num = 0, den = 0;
+    for (int c = 0; c < 3; ++c) {
+        const double pb = double(ip[c]) - double(ib[c]);
+        const double ab = double(ia[c]) - double(ib[c]);
+        num += pb * ab;
+        den += ab * ab;
+    }
+    return float(num == 0.0 ? num : num / (den + eps));
+}
+
 // weight_fast: upsample.cpp:169-172.
 GLU_HD double weight_fast64(const float* ip, const float* ia, const float* ib, double eps) {
     const double db = dist64(ip, ib);

@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS) k_solve32x(SolveAr
         ib = uint32_t(cy - 1 + bj / 3) * uint32_t(a.lw) + uint32_t(cx - 1 + bj % 3);
         const float ip[3] = {ip0, ip1, ip2};
         const float a3[3] = {ci.x, ci.y, ci.z}, b3[3] = {cj.x, cj.y, cj.z};
-        w = wSet ? wClose : float(weight_exact64(ip, a3, b3, a.eps));
+        w = wSet ? wClose : weight_exact64_f(ip, a3, b3, a.eps);
     } else {
         const int wx0 = max(0, cx - 1), wy0 = max(0, cy - 1);
         const int nwx = min(a.lw - 1, cx + 1) - wx0 + 1;
