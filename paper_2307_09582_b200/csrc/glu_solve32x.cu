@@ -58,17 +58,6 @@ struct PackedWindow {
     }
 };
 
-// pair index (i < j) -> i, j
-__device__ __forceinline__ void pair_ij(int k, int& i, int& j) {
-    i = 0;
-    int rem = k;
-    while (rem >= 8 - i) {
-        rem -= 8 - i;
-        ++i;
-    }
-    j = i + 1 + rem;
-}
-
 #ifndef GLU_X_MIN_BLOCKS
 #define GLU_X_MIN_BLOCKS 6  // 40 registers: 48 warps per SM
 #endif
@@ -84,20 +73,23 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS) k_solve32x(SolveAr
     const int ncw = div_s(min(x0 + kTX - 1, a.W - 1), a) - ocx0 + 1;
     const int nch = div_s(min(y0 + kTY - 1, a.H - 1), a) - ocy0 + 1;
     const float eps = a.epsf;
+    const int cw = ncw + 2;
+    for (int k = threadIdx.x; k < cw * (nch + 2); k += kThreads)
+        wcells[k] = __ldg(packed + size_t(ocy0 + k / cw) * pw + (ocx0 + k % cw));
+    __syncthreads();
     for (int idx = threadIdx.x; idx < ncw * nch * kPairs; idx += kThreads) {
         const int cell = idx / kPairs, pr = idx - cell * kPairs;
-        const int cx = ocx0 + cell % ncw, cy = ocy0 + cell / ncw;
-        int i, j;
-        pair_ij(pr, i, j);
-        const float4* win = packed + size_t(cy) * pw + cx;
-        const float4 ci = __ldg(win + (i / 3) * pw + i % 3), cj = __ldg(win + (j / 3) * pw + j % 3);
+        const int ly = cell / ncw, lx = cell - ly * ncw;
+        // pair pr (lexicographic i < j) -> (i, j) without a loop
+        const int i = (pr >= 8) + (pr >= 15) + (pr >= 21) + (pr >= 26) + (pr >= 30) + (pr >= 33) +
+                      (pr >= 35);
+        const int j = pr - (i * 8 - i * (i - 1) / 2) + i + 1;
+        const float4* w = wcells + ly * cw + lx;
+        const float4 ci = w[(i / 3) * cw + i % 3], cj = w[(j / 3) * cw + j % 3];
         const float d0 = ci.x - cj.x, d1 = ci.y - cj.y, d2 = ci.z - cj.z;
         const float den = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmaf_rn(d0, d0, eps)));
         table[cell * kCellStride + pr] = make_float4(d0, d1, d2, rcp_approx(den));
     }
-    const int cw = ncw + 2;
-    for (int k = threadIdx.x; k < cw * (nch + 2); k += kThreads)
-        wcells[k] = __ldg(packed + size_t(ocy0 + k / cw) * pw + (ocx0 + k % cw));
     __syncthreads();
 
     const int x = x0 + (threadIdx.x % kTX), y = y0 + (threadIdx.x / kTX);
