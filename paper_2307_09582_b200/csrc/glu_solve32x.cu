@@ -35,9 +35,9 @@ constexpr float kCE = 64.0f;  // objective error bound, in u * |e_j|^2
 constexpr float kCA = 32.0f;
 constexpr float kInf = __builtin_huge_valf();
 
-__device__ __forceinline__ float rcp_approx(float x) {
+__device__ __forceinline__ float rsqrt_approx(float x) {
     float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
 
@@ -88,7 +88,9 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS) k_solve32x(SolveAr
         const float4 ci = w[(i / 3) * cw + i % 3], cj = w[(j / 3) * cw + j % 3];
         const float d0 = ci.x - cj.x, d1 = ci.y - cj.y, d2 = ci.z - cj.z;
         const float den = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmaf_rn(d0, d0, eps)));
-        table[cell * kCellStride + pr] = make_float4(d0, d1, d2, rcp_approx(den));
+        // D' = D / sqrt(den): then obj_ij = q_j - (e_j . D')^2
+        const float r = rsqrt_approx(den);
+        table[cell * kCellStride + pr] = make_float4(d0 * r, d1 * r, d2 * r, 0.0f);
     }
     __syncthreads();
 
@@ -104,8 +106,8 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS) k_solve32x(SolveAr
                 ip2 = __ldg(a.high + 3 * p + 2);
 
     // j-outer scan: pair (i, j) needs only e_j = I_j - I_p and q_j = |e_j|^2
-    // (D_ij and 1/den come from the cell's table), so nothing per candidate
-    // stays live across the scan.  Track the strict argmin b1 (pair bk =
+    // (D'_ij = D_ij / sqrt(den) comes from the cell's table: obj = q_j -
+    // (e_j . D')^2), so nothing per candidate stays live across the scan.  Track the strict argmin b1 (pair bk =
     // i << 4 | j) and, for the close-call test, t = o - E per pair (E = kCE u
     // q_j + 1e-36, its error bound): m2 = min of t over the pairs that are not
     // the current best, bme = the best pair's t.  This order is not the
@@ -126,9 +128,9 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS) k_solve32x(SolveAr
         j0 = (j0 < 0 && qj == 0.0f) ? j : j0;  // first exact colour match
 #pragma unroll
         for (int i = 0; i < j; ++i) {
-            const float4 t = tab[i * 8 - i * (i - 1) / 2 + (j - i - 1)];
-            const float num = -__fmaf_rn(e0, t.x, __fmaf_rn(e1, t.y, e2 * t.z));
-            const float o = __fmaf_rn(-num * num, t.w, qj);
+            const float4 d = tab[i * 8 - i * (i - 1) / 2 + (j - i - 1)];
+            const float dn = __fmaf_rn(e0, d.x, __fmaf_rn(e1, d.y, e2 * d.z));
+            const float o = __fmaf_rn(-dn, dn, qj);
             const float tt = o - qej;
             const bool lt = o < b1;
             m2 = fminf(m2, lt ? bme : tt);
@@ -188,9 +190,9 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS) k_solve32x(SolveAr
                 const float qj = __fmaf_rn(e2, e2, __fmaf_rn(e1, e1, __fmul_rn(e0, e0)));
                 float o = qj;
                 if (j != i) {
-                    const float4 t = tab[i * 8 - i * (i - 1) / 2 + (j - i - 1)];
-                    const float num = -__fmaf_rn(e0, t.x, __fmaf_rn(e1, t.y, e2 * t.z));
-                    o = __fmaf_rn(-num * num, t.w, qj);
+                    const float4 d = tab[i * 8 - i * (i - 1) / 2 + (j - i - 1)];
+                    const float dn = __fmaf_rn(e0, d.x, __fmaf_rn(e1, d.y, e2 * d.z));
+                    o = __fmaf_rn(-dn, dn, qj);
                 }
                 const bool best = i == bi && j == bj;
                 if (!best && (!(o <= kInf) || !(o - __fmaf_rn(kE, qj, 1e-36f) <= b1 + eb)))
