@@ -171,6 +171,9 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS) k_solve32x(SolveAr
     bool wSet = false;  // w settled in double over the close set
     float wClose = 0.0f;
     if (ok && !exactZero && m2 <= b1 + eb) {
+#ifdef GLU_X_COUNT_RECHECK
+        if (a.fallbacks) atomicAdd(a.fallbacks + 1, 1ull);
+#endif
         // rare: per-pair bounds, in lexicographic order.  The close pairs
         // (bit k = lexicographic pair k, the winner included) hold the
         // reference's first argmin: if they all carry the winner's colour
