@@ -77,15 +77,19 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS) k_solve32x(SolveAr
     for (int k = threadIdx.x; k < cw * (nch + 2); k += kThreads)
         wcells[k] = __ldg(packed + size_t(ocy0 + k / cw) * pw + (ocx0 + k % cw));
     __syncthreads();
-    for (int idx = threadIdx.x; idx < ncw * nch * kPairs; idx += kThreads) {
-        const int cell = idx / kPairs, pr = idx - cell * kPairs;
+    // thread t builds pair pr = t % 36 for cells t / 36, t / 36 + 7, ... (the
+    // pair decode is paid once per thread)
+    const int pr = int(threadIdx.x) % kPairs;
+    const int ti = (pr >= 8) + (pr >= 15) + (pr >= 21) + (pr >= 26) + (pr >= 30) + (pr >= 33) +
+                   (pr >= 35);
+    const int tj = pr - (ti * 8 - ti * (ti - 1) / 2) + ti + 1;
+    const int oi = (ti / 3) * cw + ti % 3, oj = (tj / 3) * cw + tj % 3;
+    constexpr int kCellStep = kThreads / kPairs;  // 7 cells per pass; threads 252.. idle
+    for (int cell = int(threadIdx.x) / kPairs; cell < ncw * nch && threadIdx.x < kCellStep * kPairs;
+         cell += kCellStep) {
         const int ly = cell / ncw, lx = cell - ly * ncw;
-        // pair pr (lexicographic i < j) -> (i, j) without a loop
-        const int i = (pr >= 8) + (pr >= 15) + (pr >= 21) + (pr >= 26) + (pr >= 30) + (pr >= 33) +
-                      (pr >= 35);
-        const int j = pr - (i * 8 - i * (i - 1) / 2) + i + 1;
         const float4* w = wcells + ly * cw + lx;
-        const float4 ci = w[(i / 3) * cw + i % 3], cj = w[(j / 3) * cw + j % 3];
+        const float4 ci = w[oi], cj = w[oj];
         const float d0 = ci.x - cj.x, d1 = ci.y - cj.y, d2 = ci.z - cj.z;
         const float den = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmaf_rn(d0, d0, eps)));
         // D' = D / sqrt(den): then obj_ij = q_j - (e_j . D')^2
