@@ -123,11 +123,7 @@ __global__ void __launch_bounds__(kThreads, GLU_SOLVE_MIN_BLOCKS)
     forceFallback |= int(__ldg(nanFlag));
     constexpr int N = S * S;
     constexpr int h = S / 2;
-#ifdef GLU_S3_RELOAD
-    constexpr int NE = 1;
-#else
     constexpr int NE = S == 3 ? N : 1;  // S = 3 keeps e_j in registers; S = 5 reloads
-#endif
     const int pw = a.lw + 2 * h;
     // 32 x 4 pixel tiles: a warp covers 32 consecutive pixels of one row
     const int x = blockIdx.x * 32 + (threadIdx.x & 31);

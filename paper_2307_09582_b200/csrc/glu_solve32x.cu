@@ -32,7 +32,6 @@ constexpr int kMaxCells = 48;    // (31/3 + 2) x (7/3 + 2) owner cells for s >= 
 constexpr int kMaxWinCells = 96;  // their candidate cells: (ncw + 2) x (nch + 2) <= 14 x 6
 constexpr float kU = 5.9604645e-08f;
 constexpr float kCE = 64.0f;  // objective error bound, in u * |e_j|^2
-constexpr float kCA = 32.0f;
 constexpr float kInf = __builtin_huge_valf();
 
 __device__ __forceinline__ float rsqrt_approx(float x) {
@@ -256,7 +255,6 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS) k_solve32x(SolveAr
             if (qk == 0.0f && !(e0 == 0.0f && e1 == 0.0f && e2 == 0.0f)) ok = false;
         }
     }
-    (void)kCA;
     uint32_t ia, ib;
     float w;
     if (ok) {
