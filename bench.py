@@ -206,7 +206,7 @@ def run_reference(args, ws, rank):
         "metric": METRIC, "value": value, "unit": "HR Mpix/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded Voronoi+lines+noise generator, BASELINE configs[0])",
+        "data": "synthetic (seeded Voronoi+lines+noise generator, BASELINE configs[0] generator, configs[2] workload)",
         "config": {"workload": WORKLOAD + "; reference step = 1 frame", "frames_per_step": 1,
                    "parallelism": "cpu threads"},
         "impl": "reference",
@@ -352,7 +352,7 @@ def run_ours(args, ws, rank, local):
             "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None,
             "dtype": "f32 selection filter + f64 verify/weights (bit-exact to the f64 reference)",
-            "data": "synthetic (seeded Voronoi+lines+noise generator, BASELINE configs[0]/[2])",
+            "data": "synthetic (seeded Voronoi+lines+noise generator, BASELINE configs[0] generator, configs[2] workload)",
             "config": {"workload": WORKLOAD, "frames_per_step": nf, "width": W_, "height": H_,
                        "scale": SCALE, "window": 3, "mode": args.mode,
                        "parallelism": f"frames sharded, {ws} rank(s)",
