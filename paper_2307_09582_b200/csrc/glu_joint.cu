@@ -663,51 +663,81 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
     __syncthreads();
     GLU_PHASE(0)
     // C. replace the touched cells; affected-pixel offsets over D (76-110)
-    uint32_t nt = 0;
-    for (int b0 = 0; b0 < nq; b0 += NT) {
-        const int k = b0 + tid;
-        const unsigned long long key = k < nq ? ss.key[k] : 0ull;
-        uint32_t pos, total;
-        BlockScan(sm.tmp.scan).ExclusiveSum(key ? 1u : 0u, pos, total);
-        if (key) {
-            const uint32_t slot = nt + pos;
-            const int qx = g.qx0 + k % g.qw, qy = g.qy0 + k / g.qw;
-            const float4 bc = ss.compC[0xffffffffu - uint32_t(key & 0xffffffffu)];
-            float4& wc = ss.win[(qy - g.vy0) * g.vw + (qx - g.vx0)];
-            ss.touched[slot] = uint32_t(k);
-            ss.old[3 * slot] = wc.x;
-            ss.old[3 * slot + 1] = wc.y;
-            ss.old[3 * slot + 2] = wc.z;
-            wc = bc;  // global LR written at commit
-        }
-        nt += total;
-        __syncthreads();
-    }
-    uint32_t na = 0;
-    for (int b0 = 0; b0 < nd; b0 += NT) {
-        const int k = b0 + tid;
-        uint32_t fs = 0;
-        if (k < nd) {
-            const int x = g.dx0 + k % g.dw, y = g.dy0 + k / g.dw;
-            bool hit = false;
-            for (int yy = max(y - h, g.qy0); yy <= min(y + h, g.qy0 + g.qh - 1) && !hit; ++yy)
-                for (int xx = max(x - h, g.qx0); xx <= min(x + h, g.qx0 + g.qw - 1); ++xx)
-                    if (ss.key[(yy - g.qy0) * g.qw + (xx - g.qx0)]) {
-                        hit = true;
-                        break;
-                    }
-            if (hit)
-                fs = uint32_t(min(x * t.s + t.s, t.W) - x * t.s) *
-                     uint32_t(min(y * t.s + t.s, t.H) - y * t.s);
-        }
-        uint32_t pos, total;
-        BlockScan(sm.tmp.scan).ExclusiveSum(fs, pos, total);
-        if (k < nd) ss.pre[k] = na + pos;
+    auto footprint = [&](int k) -> uint32_t {  // affected pixels of D cell k (0: not affected)
+        const int x = g.dx0 + k % g.dw, y = g.dy0 + k / g.dw;
+        for (int yy = max(y - h, g.qy0); yy <= min(y + h, g.qy0 + g.qh - 1); ++yy)
+            for (int xx = max(x - h, g.qx0); xx <= min(x + h, g.qx0 + g.qw - 1); ++xx)
+                if (ss.key[(yy - g.qy0) * g.qw + (xx - g.qx0)])
+                    return uint32_t(min(x * t.s + t.s, t.W) - x * t.s) *
+                           uint32_t(min(y * t.s + t.s, t.H) - y * t.s);
+        return 0u;
+    };
+    auto replace = [&](int k, unsigned long long key, uint32_t slot) {
+        const int qx = g.qx0 + k % g.qw, qy = g.qy0 + k / g.qw;
+        const float4 bc = ss.compC[0xffffffffu - uint32_t(key & 0xffffffffu)];
+        float4& wc = ss.win[(qy - g.vy0) * g.vw + (qx - g.vx0)];
+        ss.touched[slot] = uint32_t(k);
+        ss.old[3 * slot] = wc.x;
+        ss.old[3 * slot + 1] = wc.y;
+        ss.old[3 * slot + 2] = wc.z;
+        wc = bc;  // global LR written at commit
+    };
+    auto place = [&](int k, uint32_t fs, uint32_t pos) {
+        ss.pre[k] = pos;
         if (fs && g.full)
-            ss.cellOf[(na + pos) / uint32_t(t.s * t.s)] =
+            ss.cellOf[pos / uint32_t(t.s * t.s)] =
                 (uint32_t(g.dy0 + k / g.dw) << 16) | uint32_t(g.dx0 + k % g.dw);
-        na += total;
+    };
+    uint32_t nt = 0, na = 0;
+    if (nq <= NT && nd <= NT) {
+        // the common case in one pass: both compactions by warp ballot /
+        // shuffle scan, one barrier for the per-warp totals
+        __shared__ uint32_t wtot[2][NT / 32];
+        const int lane = tid & 31, wid = tid >> 5;
+        const unsigned long long key = tid < nq ? ss.key[tid] : 0ull;
+        const uint32_t fs = tid < nd ? footprint(tid) : 0u;
+        const unsigned bal = __ballot_sync(0xffffffffu, key != 0);
+        uint32_t incl = fs;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (lane == 31) {
+            wtot[0][wid] = __popc(bal);
+            wtot[1][wid] = incl;
+        }
         __syncthreads();
+        uint32_t baseT = 0, baseA = 0;
+#pragma unroll
+        for (int w = 0; w < NT / 32; ++w) {
+            const uint32_t c0 = wtot[0][w], c1 = wtot[1][w];
+            baseT += w < wid ? c0 : 0u;
+            baseA += w < wid ? c1 : 0u;
+            nt += c0;
+            na += c1;
+        }
+        if (key) replace(tid, key, baseT + __popc(bal & ((1u << lane) - 1u)));
+        if (tid < nd) place(tid, fs, baseA + incl - fs);
+    } else {
+        for (int b0 = 0; b0 < nq; b0 += NT) {
+            const int k = b0 + tid;
+            const unsigned long long key = k < nq ? ss.key[k] : 0ull;
+            uint32_t pos, total;
+            BlockScan(sm.tmp.scan).ExclusiveSum(key ? 1u : 0u, pos, total);
+            if (key) replace(k, key, nt + pos);
+            nt += total;
+            __syncthreads();
+        }
+        for (int b0 = 0; b0 < nd; b0 += NT) {
+            const int k = b0 + tid;
+            const uint32_t fs = k < nd ? footprint(k) : 0u;
+            uint32_t pos, total;
+            BlockScan(sm.tmp.scan).ExclusiveSum(fs, pos, total);
+            if (k < nd) place(k, fs, na + pos);
+            na += total;
+            __syncthreads();
+        }
     }
     if (tid == 0) ss.pre[nd] = na;
     __syncthreads();
@@ -824,36 +854,50 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
         red[1][tid >> 5] = part1;
     }
     const bool anyChangedCta = __syncthreads_or(changed);
-    if (tid == 0) {
+    int verdict;
+    if (kCS == 1) {
+        // every thread forms the same sums in the same order: the same verdict
         double s0 = 0, e1 = 0;
+#pragma unroll
         for (int k = 0; k < NT / 32; ++k) {
             s0 += red[0][k];
             e1 += red[1][k];
         }
-        cluster_bcast(&xred[rank][0], s0);
-        cluster_bcast(&xred[rank][1], e1);
-        cluster_bcast(&xred[rank][2], anyChangedCta ? 1.0 : 0.0);
-    }
-    cluster_barrier();  // partials (and every CTA's new values in b / park) visible
-    if (tid == 0) {
-        // the same sums in the same order in every CTA: the same verdict
-        double s0 = 0, e1 = 0;
-        bool anyChanged = false;
-        for (int r = 0; r < kCS; ++r) {
-            s0 += xred[r][0];
-            e1 += xred[r][1];
-            anyChanged |= xred[r][2] != 0.0;
-        }
         const double bound = 4.0 * (double(na) + 64.0) * 0x1.0p-53 * (s0 + e1);
-        if (!anyChanged || e1 + bound < s0)
-            sm.verdict = 1;
-        else if (e1 > s0 + bound)
-            sm.verdict = 0;
-        else
-            sm.verdict = -1;
+        verdict = (!anyChangedCta || e1 + bound < s0) ? 1 : (e1 > s0 + bound ? 0 : -1);
+    } else {
+        if (tid == 0) {
+            double s0 = 0, e1 = 0;
+            for (int k = 0; k < NT / 32; ++k) {
+                s0 += red[0][k];
+                e1 += red[1][k];
+            }
+            cluster_bcast(&xred[rank][0], s0);
+            cluster_bcast(&xred[rank][1], e1);
+            cluster_bcast(&xred[rank][2], anyChangedCta ? 1.0 : 0.0);
+        }
+        cluster_barrier();  // partials (and every CTA's new values in b / park) visible
+        if (tid == 0) {
+            // the same sums in the same order in every CTA: the same verdict
+            double s0 = 0, e1 = 0;
+            bool anyChanged = false;
+            for (int r = 0; r < kCS; ++r) {
+                s0 += xred[r][0];
+                e1 += xred[r][1];
+                anyChanged |= xred[r][2] != 0.0;
+            }
+            const double bound = 4.0 * (double(na) + 64.0) * 0x1.0p-53 * (s0 + e1);
+            if (!anyChanged || e1 + bound < s0)
+                sm.verdict = 1;
+            else if (e1 > s0 + bound)
+                sm.verdict = 0;
+            else
+                sm.verdict = -1;
+        }
+        __syncthreads();
+        verdict = sm.verdict;
     }
-    __syncthreads();
-    if (sm.verdict < 0) {
+    if (verdict < 0) {
         // exact reference order, as in run_trial
         double q0 = 0, q1 = 0;
         float* stage = reinterpret_cast<float*>(&sm.tmp);
@@ -879,8 +923,8 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
             if (rank == 0) atomicAdd(t.result + 2, 1);
         }
         __syncthreads();
+        verdict = sm.verdict;
     }
-    const int verdict = sm.verdict;
     if (tid == 0) {
         sm.touched = nt;
         sm.base = na;
