@@ -292,7 +292,7 @@ __device__ int run_trial(const TrialState& t, const TrialBuffers& b, TrialSmem<N
         const int nwx = min(t.lw - 1, cx + h) - x0 + 1, nwy = min(t.lh - 1, cy + h) - y0 + 1;
         glu_pixel_params np;
         bool done = false;
-        if (t.S == 3 && t.mode != GLU_MODE_EXACT) {
+        if (t.S == 3) {
             // fp32 filter + fp64 verify (glu_filter32.cuh) on the live LR image
             float4 c[9];
 #pragma unroll
@@ -306,7 +306,9 @@ __device__ int run_trial(const TrialState& t, const TrialBuffers& b, TrialSmem<N
                 }
             }
             const Filter32Result fr =
-                filter32_pixel(c, ip, float(t.eps), t.eps, t.mode == GLU_MODE_GNU);
+                t.mode == GLU_MODE_EXACT
+                    ? filter32x_pixel(c, ip, float(t.eps), t.eps)
+                    : filter32_pixel(c, ip, float(t.eps), t.eps, t.mode == GLU_MODE_GNU);
             if (fr.ok) {
                 np.a = uint32_t(cy - 1 + fr.ja / 3) * uint32_t(t.lw) + uint32_t(cx - 1 + fr.ja % 3);
                 np.b = uint32_t(cy - 1 + fr.jb / 3) * uint32_t(t.lw) + uint32_t(cx - 1 + fr.jb % 3);
@@ -775,7 +777,7 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
 #ifdef GLU_SCHED_TRACE
         float4 c_dbg[9];
 #endif
-        if (t.S == 3 && t.mode != GLU_MODE_EXACT) {
+        if (t.S == 3) {
             float4 c[9];
 #pragma unroll
             for (int k = 0; k < 9; ++k) {
@@ -786,7 +788,9 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
                     c[k] = ss.win[(gy - g.vy0) * g.vw + (gx - g.vx0)];
             }
             const Filter32Result fr =
-                filter32_pixel(c, ip, float(t.eps), t.eps, t.mode == GLU_MODE_GNU);
+                t.mode == GLU_MODE_EXACT
+                    ? filter32x_pixel(c, ip, float(t.eps), t.eps)
+                    : filter32_pixel(c, ip, float(t.eps), t.eps, t.mode == GLU_MODE_GNU);
 #ifdef GLU_SCHED_TRACE
             for (int k = 0; k < 9; ++k) c_dbg[k] = c[k];
             if (fr.ok && fr.why == 6) atomicAdd(&g_phase[16], 1ull);
