@@ -210,6 +210,25 @@ def test_joint_vs_oracle_seeded(glu, oracle, mode):
         assert same(r.errors.cpu().numpy(), o["errors"])
 
 
+@pytest.mark.parametrize("mode", ["fast", "gnu", "exact"])
+def test_joint_vs_oracle_tie_heavy(glu, oracle, mode):
+    """Joint loop on quantised (duplicate-colour, tie-heavy) and noise images:
+    the trial filters' exact-zero, close-call and close-set paths against the
+    oracle."""
+    from paper_2307_09582_b200 import workloads
+    rng = np.random.default_rng(5)
+    base = workloads.scene(200, 144, 31)
+    for img in ((np.round(base * 3) / 3).astype(np.float32),
+                rng.random((120, 160, 3), dtype=np.float32)):
+        r = glu.joint_optimize(dev(img), 4, None, mode_of(glu, mode))
+        o = oracle.joint_optimize(img, 4, mode=mode)
+        assert [r.iterations, r.trialsAccepted, r.trialsRejected] == \
+            [o["iterations"], o["accepted"], o["rejected"]]
+        assert same(r.low.cpu().numpy(), o["low"])
+        assert same(host_params(r.field.params), o["field"])
+        assert same(r.errors.cpu().numpy(), o["errors"])
+
+
 def test_full_size_properties(glu, oracle):
     """C3 size (3840x2160, s=8): determinism, oracle rows, gain linearity."""
     from paper_2307_09582_b200 import workloads
