@@ -28,8 +28,9 @@ namespace {
 constexpr int kTX = 32, kTY = 8, kThreads = kTX * kTY;
 constexpr int kPairs = 36;       // i < j over 9 candidates
 constexpr int kCellStride = 37;  // float4 per owner cell (592 B: bank-spread)
-constexpr int kMaxCells = 48;    // (31/3 + 2) x (7/3 + 2) owner cells for s >= 3
-constexpr int kMaxWinCells = 96;  // their candidate cells: (ncw + 2) x (nch + 2) <= 14 x 6
+constexpr int kMaxRows = 8;               // pixels per thread (rows y, y + kTY, ...): 1..8
+constexpr int kSmemCap = 40 * 1024;       // per CTA, so that GLU_X_MIN_BLOCKS CTAs fit
+constexpr float kStageCost = 0.3f;        // a tile's staging, in units of one row of pixels
 constexpr float kU = 5.9604645e-08f;
 constexpr float kCE = 64.0f;  // objective error bound, in u * |e_j|^2
 constexpr float kInf = __builtin_huge_valf();
@@ -48,6 +49,37 @@ __device__ __forceinline__ bool same_rgb(float4 a, float4 b) {
     return a.x == b.x && a.y == b.y && a.z == b.z;
 }
 
+// A pair's key: t with its low 4 mantissa bits replaced by the row index i
+// (the perturbation is below 15 ulp; NaN stays NaN).  `mask` = 0xfffffff0 is
+// held in a register so that (t & mask) | i is one LOP3 with i as immediate.
+__device__ __forceinline__ float pack_key(float t, int i, unsigned mask) {
+    unsigned r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEC;" : "=r"(r) : "r"(__float_as_uint(t)), "r"(unsigned(i)),
+        "r"(mask));
+    return __uint_as_float(r);
+}
+
+// Smallest (K1) and second smallest (K2) key so far; a NaN key changes
+// neither (fminf / fmaxf return the other operand).
+__device__ __forceinline__ void track_key(float& K1, float& K2, float k) {
+    K2 = fmaxf(fminf(K2, k), K1);
+    K1 = fminf(K1, k);
+}
+
+__device__ __forceinline__ float fmax_nan(float a, float b) {  // NaN if either is NaN
+    float r;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
+
+// Two keys at once (5 instructions, three-input min): the second smallest of
+// {K1 <= K2, a, b} is max(min(K2, a, b), min(K1, max(a, b))); with max
+// propagating NaN a NaN key drops out (the one-key update for the other).
+__device__ __forceinline__ void track_key2(float& K1, float& K2, float a, float b) {
+    K2 = fmaxf(fminf(fminf(K2, a), b), fminf(K1, fmax_nan(a, b)));
+    K1 = fminf(fminf(K1, a), b);
+}
+
 struct PackedWindow {
     const float4* win;
     int pw, nwx;
@@ -58,201 +90,183 @@ struct PackedWindow {
 };
 
 #ifndef GLU_X_MIN_BLOCKS
-#define GLU_X_MIN_BLOCKS 6  // 40 registers: 48 warps per SM
+#define GLU_X_MIN_BLOCKS 5  // 48 registers: 40 warps per SM
 #endif
-__global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS) k_solve32x(SolveArgs a, const float4* packed,
-                                                          int forceFallback,
-                                                          const unsigned* nanFlag) {
-    forceFallback |= int(__ldg(nanFlag));
-    __shared__ float4 table[kMaxCells * kCellStride];
-    __shared__ float4 wcells[kMaxWinCells];  // the tile's candidate cells (owner cells +- 1)
-    const int pw = a.lw + 2;  // h = 1
-    const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * kTY;
-    const int ocx0 = div_s(x0, a), ocy0 = div_s(y0, a);
-    const int ncw = div_s(min(x0 + kTX - 1, a.W - 1), a) - ocx0 + 1;
-    const int nch = div_s(min(y0 + kTY - 1, a.H - 1), a) - ocy0 + 1;
-    const float eps = a.epsf;
-    const int cw = ncw + 2;
-    for (int k = threadIdx.x; k < cw * (nch + 2); k += kThreads)
-        wcells[k] = __ldg(packed + size_t(ocy0 + k / cw) * pw + (ocx0 + k % cw));
-    __syncthreads();
-    // thread t builds pair pr = t % 36 for cells t / 36, t / 36 + 7, ... (the
-    // pair decode is paid once per thread)
-    const int pr = int(threadIdx.x) % kPairs;
-    const int ti = (pr >= 8) + (pr >= 15) + (pr >= 21) + (pr >= 26) + (pr >= 30) + (pr >= 33) +
-                   (pr >= 35);
-    const int tj = pr - (ti * 8 - ti * (ti - 1) / 2) + ti + 1;
-    const int oi = (ti / 3) * cw + ti % 3, oj = (tj / 3) * cw + tj % 3;
-    constexpr int kCellStep = kThreads / kPairs;  // 7 cells per pass; threads 252.. idle
-    for (int cell = int(threadIdx.x) / kPairs; cell < ncw * nch && threadIdx.x < kCellStep * kPairs;
-         cell += kCellStep) {
-        const int ly = cell / ncw, lx = cell - ly * ncw;
-        const float4* w = wcells + ly * cw + lx;
-        const float4 ci = w[oi], cj = w[oj];
-        const float d0 = ci.x - cj.x, d1 = ci.y - cj.y, d2 = ci.z - cj.z;
-        const float den = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmaf_rn(d0, d0, eps)));
-        // D' = D / sqrt(den): then obj_ij = q_j - (e_j . D')^2
-        const float r = rsqrt_approx(den);
-        table[cell * kCellStride + pr] = make_float4(d0 * r, d1 * r, d2 * r, 0.0f);
-    }
-    __syncthreads();
 
-    const int x = x0 + (threadIdx.x % kTX), y = y0 + (threadIdx.x / kTX);
-    if (x >= a.W || y >= a.H) return;
+// The tile's staged candidate cells and pair table (shared memory).
+struct XTile {
+    const float4* wcells;  // candidate cells of the tile's owner cells (+- 1), cw per row
+    const float4* table;   // kCellStride float4 per owner cell: D' of its 36 pairs
+    int cw, ncw, ocx0, ocy0;
+};
+
+// One HR pixel (x, y) with guide colour (ip0, ip1, ip2): the pair search,
+// tie recovery, weight and the fused epilogues.
+__device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* packed, const XTile& t,
+                                            int forceFallback, int x, int y, float ip0, float ip1,
+                                            float ip2) {
+    const int pw = a.lw + 2;  // h = 1
+    const int cw = t.cw;
     const size_t p = size_t(y) * a.W + x;
     const int cx = div_s(x, a), cy = div_s(y, a);
-    const float4* win = packed + size_t(cy) * pw + cx;
-    // the same window in shared memory: candidate j is swin[(j / 3) * cw + j % 3]
-    const float4* swin = wcells + (cy - ocy0) * cw + (cx - ocx0);
-    const float4* tab = table + ((cy - ocy0) * ncw + (cx - ocx0)) * kCellStride;
-    const float ip0 = __ldg(a.high + 3 * p), ip1 = __ldg(a.high + 3 * p + 1),
-                ip2 = __ldg(a.high + 3 * p + 2);
+    // the window in shared memory: candidate j is swin[(j / 3) * cw + j % 3]
+    const float4* swin = t.wcells + (cy - t.ocy0) * cw + (cx - t.ocx0);
+    const float4* tab = t.table + ((cy - t.ocy0) * t.ncw + (cx - t.ocx0)) * kCellStride;
 
     // j-outer scan: pair (i, j) needs only e_j = I_j - I_p and q_j = |e_j|^2
     // (D'_ij = D_ij / sqrt(den) comes from the cell's table: obj = q_j -
-    // (e_j . D')^2), so nothing per candidate stays live across the scan.  Track the strict argmin b1 (pair bk =
-    // i << 4 | j) and, for the close-call test, t = o - E per pair (E = kCE u
-    // q_j + 1e-36, its error bound): m2 = min of t over the pairs that are not
-    // the current best, bme = the best pair's t.  This order is not the
-    // reference's lexicographic (i <= j) order, so among exactly tied pairs
-    // the lexicographic first is recovered below (exact zeros directly, other
-    // ties in the re-check of close calls).
+    // (e_j . D')^2), so nothing per candidate stays live across the scan.
+    //
+    // Each pair is reduced to one key: t = q_j (1 - kE) - 1e-36 - (e_j . D')^2
+    // (the fp32 objective lowered by its error bound) with the low 4 mantissa
+    // bits replaced by i (the pair's row within column j).  |key - obj| is
+    // within (kE +- 57u) q_j (objective 22u, t's roundings 3u, the packing
+    // 15 ulp = 30u), so a key is a lower bound of its pair's objective and
+    // key + kT q_j an upper bound.  The scan keeps the smallest key K1 (its
+    // column bj, its row in the low bits) and the second smallest K2; if K2 >
+    // K1 + kT q_bj the winner's objective is provably below every other pair's
+    // and it is the reference's unique argmin.  Otherwise (close call, tie)
+    // the close pairs are re-checked in the reference's lexicographic order
+    // below.  Off-grid pairs give NaN keys (inf - inf, inf * 0), which the
+    // NaN-ignoring min / max updates skip.
     constexpr float kE = kCE * kU;
-    float qmin = kInf, b1 = kInf, m2 = kInf, bme = kInf;
-    int bk = 0, i0 = -1, j0 = -1;
+    constexpr float kOneMinusE = 1.0f - kE;         // exact: 1 - 2^-18
+    constexpr float kT = (2.0f * kCE + 8.0f) * kU;  // >= kE + 57u + the rounding of K1 + kT q
+    // 0xfffffff0, opaque to the compiler (W > 0) so it stays in a register
+    const unsigned kmask = 0xfffffff0u | (unsigned(a.W) >> 31);
+    float qmin = kInf, K1 = kInf, K2 = kInf;
+    int bj = 0;
 #pragma unroll
     for (int j = 0; j < 9; ++j) {
         const float4 v = swin[(j / 3) * cw + j % 3];
         const float e0 = v.x - ip0, e1 = v.y - ip1, e2 = v.z - ip2;
         const float qj = __fmaf_rn(e2, e2, __fmaf_rn(e1, e1, __fmul_rn(e0, e0)));
-        const float qej = __fmaf_rn(kE, qj, 1e-36f);
+        const float qm = __fmaf_rn(qj, kOneMinusE, -1e-36f);
         qmin = fminf(qmin, qj);
-        i0 = (i0 < 0 && qj < kInf) ? j : i0;    // first in-grid candidate
-        j0 = (j0 < 0 && qj == 0.0f) ? j : j0;  // first exact colour match
+        const float k1in = K1;
+        float pend = 0.0f;  // keys are tracked two at a time: (0, 1), (2, 3), ...
 #pragma unroll
         for (int i = 0; i < j; ++i) {
             const float4 d = tab[i * 8 - i * (i - 1) / 2 + (j - i - 1)];
             const float dn = __fmaf_rn(e0, d.x, __fmaf_rn(e1, d.y, e2 * d.z));
-            const float o = __fmaf_rn(-dn, dn, qj);
-            const float tt = o - qej;
-            const bool lt = o < b1;
-            m2 = fminf(m2, lt ? bme : tt);
-            bme = lt ? tt : bme;
-            b1 = lt ? o : b1;
-            bk = lt ? (i << 4 | j) : bk;
+            const float key = pack_key(__fmaf_rn(-dn, dn, qm), i, kmask);
+            if (i & 1)
+                track_key2(K1, K2, pend, key);
+            else
+                pend = key;
         }
-        {
-            const float o = qj;  // (j, j): w = 0
-            const float tt = o - qej;
-            const bool lt = o < b1;
-            m2 = fminf(m2, lt ? bme : tt);
-            bme = lt ? tt : bme;
-            b1 = lt ? o : b1;
-            bk = lt ? (j << 4 | j) : bk;
-        }
+        const float kd = pack_key(qm, j, kmask);  // (j, j): w = 0, obj = q_j
+        if (j & 1)
+            track_key2(K1, K2, pend, kd);
+        else
+            track_key(K1, K2, kd);
+        bj = K1 != k1in ? j : bj;
     }
-    int bi = bk >> 4, bj = bk & 15;
-    float4 ci = swin[(bi / 3) * cw + bi % 3], cj = swin[(bj / 3) * cw + bj % 3];
-    // the best pair's bound E_best (the same q_bj as in the scan)
-    const float eb0 = cj.x - ip0, eb1 = cj.y - ip1, eb2 = cj.z - ip2;
-    const float eb = __fmaf_rn(kE, __fmaf_rn(eb2, eb2, __fmaf_rn(eb1, eb1, __fmul_rn(eb0, eb0))),
-                               1e-36f);
-    bool ok = !forceFallback && b1 < kInf && ip0 == ip0 && ip1 == ip1 && ip2 == ip2 &&
+    int bi = int(__float_as_uint(K1) & 15u);
+    bool ok = !forceFallback && K1 < kInf && ip0 == ip0 && ip1 == ip1 && ip2 == ip2 &&
               (qmin >= 1e-27f || qmin == 0.0f);
-    // An exact zero with I_bj == I_p is exact in double too (w = 0, v = 0);
-    // every true zero is a pair (i, j) with e_j = 0, which evaluates to exactly
-    // 0 in fp32, so the reference's pick is the lexicographically first: (i0,
-    // j0), i0 the first in-grid candidate, j0 the first exact colour match.
-    // (Every LR sample pixel lands here.)
-    const bool exactZero = b1 == 0.0f && cj.x == ip0 && cj.y == ip1 && cj.z == ip2;
-    if (exactZero && j0 >= 0) {
-        bi = i0;
-        bj = j0;
-        ci = swin[(bi / 3) * cw + bi % 3];
-        cj = swin[(bj / 3) * cw + bj % 3];
-    }
-    bool wSet = false;  // w settled in double over the close set
-    float wClose = 0.0f;
-    if (ok && !exactZero && m2 <= b1 + eb) {
-#ifdef GLU_X_COUNT_RECHECK
-        if (a.fallbacks) atomicAdd(a.fallbacks + 1, 1ull);
-#endif
-        // rare: per-pair bounds, in lexicographic order.  The close pairs
-        // (bit k = lexicographic pair k, the winner included) hold the
-        // reference's first argmin: if they all carry the winner's colour
-        // tuple, the first of them is the pick; otherwise they are evaluated in
-        // double, in lexicographic order.
-        unsigned long long close = 0;
-        bool mixed = false;
-        int fi = -1, fj = -1, k = 0;
-#pragma unroll 1
-        for (int i = 0; i < 9; ++i) {
-            const float4 vi = swin[(i / 3) * cw + i % 3];
-            const bool ini = vi.x < kInf;  // the +inf sentinel marks off-grid cells
-#pragma unroll 1
-            for (int j = i; j < 9; ++j, ++k) {
-                const float4 vj = swin[(j / 3) * cw + j % 3];
-                const float e0 = vj.x - ip0, e1 = vj.y - ip1, e2 = vj.z - ip2;
-                const float qj = __fmaf_rn(e2, e2, __fmaf_rn(e1, e1, __fmul_rn(e0, e0)));
-                float o = qj;
-                if (j != i) {
-                    const float4 d = tab[i * 8 - i * (i - 1) / 2 + (j - i - 1)];
-                    const float dn = __fmaf_rn(e0, d.x, __fmaf_rn(e1, d.y, e2 * d.z));
-                    o = __fmaf_rn(-dn, dn, qj);
-                }
-                const bool best = i == bi && j == bj;
-                if (!best && (!(o <= kInf) || !(o - __fmaf_rn(kE, qj, 1e-36f) <= b1 + eb)))
-                    continue;  // not close (NaN: outside the grid)
-                if (!(ini && qj < kInf)) ok = false;  // off-grid member
-                close |= 1ull << k;
-                const bool same = same_rgb(vi, ci) && same_rgb(vj, cj);
-                mixed |= !same;
-                if (same && fi < 0) {
-                    fi = i;
-                    fj = j;
-                }
-            }
-        }
-        if (ok && !mixed) {
-            bi = fi;  // identical colours: identical objectives and weight
-            bj = fj;
-        } else if (ok && mixed) {
-            const float ip[3] = {ip0, ip1, ip2};
-            double best = 0, bw = 0;
-            int ni = -1, nj = -1;
-            int i = 0, j = 0;
-#pragma unroll 1
-            for (int kk = 0; kk < 45; ++kk) {
-                if (close >> kk & 1ull) {
-                    const float4 vi = swin[(i / 3) * cw + i % 3];
-                    const float4 vj = swin[(j / 3) * cw + j % 3];
-                    const float a3[3] = {vi.x, vi.y, vi.z}, b3[3] = {vj.x, vj.y, vj.z};
-                    const double wv = weight_exact64(ip, a3, b3, a.eps);
-                    const double o = objective64(ip, a3, b3, wv, a.eps);
-                    if (ni < 0 || o < best) {
-                        best = o;
-                        bw = wv;
-                        ni = i;
-                        nj = j;
-                    }
-                }
-                if (++j == 9) j = ++i;
-            }
-            bi = ni;
-            bj = nj;
-            wClose = float(bw);
-            wSet = true;
-            if (a.fallbacks) atomicAdd(a.fallbacks + 1, 1ull);
-        }
-    }
-    // stage-A style guard: an exact-zero distance must be a true colour match
+    // An exact colour match I_j0 == I_p: the pairs (i, j0) have objective 0
+    // in double (w = 0, v = 0) and every other pair a positive one, so the
+    // reference's pick is the lexicographically first: (i0, j0), i0 the first
+    // in-grid candidate, j0 the first exact match.  (Every LR sample pixel
+    // lands here.)  A zero fp32 distance must be a true colour match (else
+    // the pixel takes the double path).
+    bool exactZero = false;
     if (ok && qmin == 0.0f) {
+        int j0 = -1;
 #pragma unroll 1
         for (int k = 0; k < 9; ++k) {
             const float4 v = swin[(k / 3) * cw + k % 3];
             const float e0 = v.x - ip0, e1 = v.y - ip1, e2 = v.z - ip2;
             const float qk = __fmaf_rn(e2, e2, __fmaf_rn(e1, e1, __fmul_rn(e0, e0)));
-            if (qk == 0.0f && !(e0 == 0.0f && e1 == 0.0f && e2 == 0.0f)) ok = false;
+            if (qk != 0.0f) continue;
+            if (!(e0 == 0.0f && e1 == 0.0f && e2 == 0.0f)) ok = false;
+            if (j0 < 0) j0 = k;
+        }
+        exactZero = ok;
+        bi = (cy == 0 ? 3 : 0) + (cx == 0 ? 1 : 0);
+        bj = j0;
+    }
+    float4 ci = swin[(bi / 3) * cw + bi % 3], cj = swin[(bj / 3) * cw + bj % 3];
+    bool wSet = false;  // w settled in double over the close set
+    float wClose = 0.0f;
+    if (ok && !exactZero) {
+        // the winner's q (the scan's instruction sequence, so the same value)
+        const float eb0 = cj.x - ip0, eb1 = cj.y - ip1, eb2 = cj.z - ip2;
+        const float qb = __fmaf_rn(eb2, eb2, __fmaf_rn(eb1, eb1, __fmul_rn(eb0, eb0)));
+        const float lim = K1 + __fmaf_rn(kT, qb, 2e-36f);
+        if (K2 <= lim) {
+#ifdef GLU_X_COUNT_RECHECK
+            if (a.fallbacks) atomicAdd(a.fallbacks + 1, 1ull);
+#endif
+            // rare: the pairs whose key is within lim (bit k = lexicographic
+            // pair k, the winner included) hold the reference's first argmin
+            // (every other pair's objective exceeds the winner's): if they all
+            // carry the winner's colour tuple, the first of them is the pick;
+            // otherwise they are evaluated in double, in lexicographic order.
+            unsigned long long close = 0;
+            bool mixed = false;
+            int fi = -1, fj = -1, k = 0;
+#pragma unroll 1
+            for (int i = 0; i < 9; ++i) {
+                const float4 vi = swin[(i / 3) * cw + i % 3];
+                const bool ini = vi.x < kInf;  // the +inf sentinel marks off-grid cells
+#pragma unroll 1
+                for (int j = i; j < 9; ++j, ++k) {
+                    const float4 vj = swin[(j / 3) * cw + j % 3];
+                    const float e0 = vj.x - ip0, e1 = vj.y - ip1, e2 = vj.z - ip2;
+                    const float qj = __fmaf_rn(e2, e2, __fmaf_rn(e1, e1, __fmul_rn(e0, e0)));
+                    const float qm = __fmaf_rn(qj, kOneMinusE, -1e-36f);
+                    float key;
+                    if (j != i) {
+                        const float4 d = tab[i * 8 - i * (i - 1) / 2 + (j - i - 1)];
+                        const float dn = __fmaf_rn(e0, d.x, __fmaf_rn(e1, d.y, e2 * d.z));
+                        key = pack_key(__fmaf_rn(-dn, dn, qm), i, kmask);
+                    } else {
+                        key = pack_key(qm, j, kmask);
+                    }
+                    if (!(key <= lim)) continue;  // not close (NaN: outside the grid)
+                    if (!(ini && qj < kInf)) ok = false;  // off-grid member
+                    close |= 1ull << k;
+                    const bool same = same_rgb(vi, ci) && same_rgb(vj, cj);
+                    mixed |= !same;
+                    if (same && fi < 0) {
+                        fi = i;
+                        fj = j;
+                    }
+                }
+            }
+            if (ok && !mixed) {
+                bi = fi;  // identical colours: identical objectives and weight
+                bj = fj;
+            } else if (ok && mixed) {
+                const float ip[3] = {ip0, ip1, ip2};
+                double best = 0, bw = 0;
+                int ni = -1, nj = -1;
+                int i = 0, j = 0;
+#pragma unroll 1
+                for (int kk = 0; kk < 45; ++kk) {
+                    if (close >> kk & 1ull) {
+                        const float4 vi = swin[(i / 3) * cw + i % 3];
+                        const float4 vj = swin[(j / 3) * cw + j % 3];
+                        const float a3[3] = {vi.x, vi.y, vi.z}, b3[3] = {vj.x, vj.y, vj.z};
+                        const double wv = weight_exact64(ip, a3, b3, a.eps);
+                        const double o = objective64(ip, a3, b3, wv, a.eps);
+                        if (ni < 0 || o < best) {
+                            best = o;
+                            bw = wv;
+                            ni = i;
+                            nj = j;
+                        }
+                    }
+                    if (++j == 9) j = ++i;
+                }
+                bi = ni;
+                bj = nj;
+                wClose = float(bw);
+                wSet = true;
+                if (a.fallbacks) atomicAdd(a.fallbacks + 1, 1ull);
+            }
         }
     }
     uint32_t ia, ib;
@@ -292,7 +306,8 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS) k_solve32x(SolveAr
                 a.out[3 * p + k] = lerp_clamp(w, __ldg(a.lowT + 3 * size_t(ia) + k),
                                               __ldg(a.lowT + 3 * size_t(ib) + k), clamp);
         }
-    }    if (a.errOut) {  // pixel_error of the clamped self reconstruction (jointopt.cpp:190)
+    }
+    if (a.errOut) {  // pixel_error of the clamped self reconstruction (jointopt.cpp:190)
         float r[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k)
@@ -300,6 +315,70 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS) k_solve32x(SolveAr
                               true);
         const float ipx[3] = {ip0, ip1, ip2};
         a.errOut[p] = pixel_error(ipx, r);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS)
+    k_solve32x(SolveArgs a, const float4* packed, int forceFallback, const unsigned* nanFlag,
+               int maxCells, int rows) {
+    extern __shared__ float4 smem[];
+    float4* table = smem;                         // maxCells * kCellStride
+    float4* wcells = smem + maxCells * kCellStride;  // the tile's candidate cells
+    forceFallback |= int(__ldg(nanFlag));
+    const int pw = a.lw + 2;  // h = 1
+    const int tileH = kTY * rows;  // a CTA solves a kTX x tileH tile
+    const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * tileH;
+    const int ocx0 = div_s(x0, a), ocy0 = div_s(y0, a);
+    const int ncw = div_s(min(x0 + kTX - 1, a.W - 1), a) - ocx0 + 1;
+    const int nch = div_s(min(y0 + tileH - 1, a.H - 1), a) - ocy0 + 1;
+    const float eps = a.epsf;
+    const int cw = ncw + 2;
+    // the first pixel's guide colour is requested before the staging barriers
+    const int x = x0 + (threadIdx.x % kTX), yb = y0 + (threadIdx.x / kTX);
+    const bool xin = x < a.W;
+    float g0 = 0.0f, g1 = 0.0f, g2 = 0.0f;
+    if (xin && yb < a.H) {
+        const float* g = a.high + 3 * (size_t(yb) * a.W + x);
+        g0 = __ldg(g);
+        g1 = __ldg(g + 1);
+        g2 = __ldg(g + 2);
+    }
+    for (int k = threadIdx.x; k < cw * (nch + 2); k += kThreads)
+        wcells[k] = __ldg(packed + size_t(ocy0 + k / cw) * pw + (ocx0 + k % cw));
+    __syncthreads();
+    // thread t builds pair pr = t % 36 for cells t / 36, t / 36 + 7, ... (the
+    // pair decode is paid once per thread)
+    const int pr = int(threadIdx.x) % kPairs;
+    const int ti = (pr >= 8) + (pr >= 15) + (pr >= 21) + (pr >= 26) + (pr >= 30) + (pr >= 33) +
+                   (pr >= 35);
+    const int tj = pr - (ti * 8 - ti * (ti - 1) / 2) + ti + 1;
+    const int oi = (ti / 3) * cw + ti % 3, oj = (tj / 3) * cw + tj % 3;
+    constexpr int kCellStep = kThreads / kPairs;  // 7 cells per pass; threads 252.. idle
+    for (int cell = int(threadIdx.x) / kPairs; cell < ncw * nch && threadIdx.x < kCellStep * kPairs;
+         cell += kCellStep) {
+        const int ly = cell / ncw, lx = cell - ly * ncw;
+        const float4* w = wcells + ly * cw + lx;
+        const float4 ci = w[oi], cj = w[oj];
+        const float d0 = ci.x - cj.x, d1 = ci.y - cj.y, d2 = ci.z - cj.z;
+        const float den = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmaf_rn(d0, d0, eps)));
+        // D' = D / sqrt(den): then obj_ij = q_j - (e_j . D')^2
+        const float r = rsqrt_approx(den);
+        table[cell * kCellStride + pr] = make_float4(d0 * r, d1 * r, d2 * r, 0.0f);
+    }
+    __syncthreads();
+
+    const XTile t{wcells, table, cw, ncw, ocx0, ocy0};
+#pragma unroll 1
+    for (int k = 0; k < rows; ++k) {
+        const int y = yb + k * kTY;
+        const float ip0 = g0, ip1 = g1, ip2 = g2;
+        if (k + 1 < rows && xin && y + kTY < a.H) {  // the next pixel's colour, one scan ahead
+            const float* g = a.high + 3 * (size_t(y + kTY) * a.W + x);
+            g0 = __ldg(g);
+            g1 = __ldg(g + 1);
+            g2 = __ldg(g + 2);
+        }
+        if (xin && y < a.H) solve_pixel(a, packed, t, forceFallback, x, y, ip0, ip1, ip2);
     }
 }
 
@@ -311,8 +390,50 @@ bool solve32x_supported(int mode, int S, int s) {
 
 cudaError_t launch_solve32x(glu_ctx* ctx, const SolveArgs& a, const float4* packed,
                             int forceFallback, const unsigned* nanFlag) {
-    dim3 grid((a.W + kTX - 1) / kTX, (a.H + kTY - 1) / kTY);
-    k_solve32x<<<grid, kThreads, 0, ctx->stream>>>(a, packed, forceFallback, nanFlag);
+    // Rows per thread: more rows amortise a tile's staging (cells, pair
+    // table, two barriers) over more pixels, fewer rows give more tiles and a
+    // smaller partial last wave.  Pick the count minimising waves x (rows +
+    // staging cost) among those whose tile fits kSmemCap.  Owner cells a tile
+    // can touch: ncw <= (kTX - 1) / s + 2, nch <= (tileH - 1) / s + 2.
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int mcw = (kTX - 1) / a.s + 2;
+    const long tilesX = (a.W + kTX - 1) / kTX;
+    thread_local int memo[5] = {-1, 0, 0, 0, 1};  // device, s, W, H -> rows
+    if (memo[0] != dev || memo[1] != a.s || memo[2] != a.W || memo[3] != a.H) {
+        int nsm = 148, rows = 1;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        float best = -1.0f;
+        for (int r = 1; r <= kMaxRows; ++r) {
+            const int mch = (kTY * r - 1) / a.s + 2;
+            const size_t sm =
+                sizeof(float4) * (size_t(mcw * mch) * kCellStride + (mcw + 2) * (mch + 2));
+            if (r > 1 && sm > kSmemCap) break;
+            int per = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_solve32x, kThreads, sm);
+            const long slots = long(max(per, 1)) * nsm;
+            const long tiles = tilesX * ((a.H + kTY * r - 1) / (kTY * r));
+            const float cost = float((tiles + slots - 1) / slots) * (float(r) + kStageCost);
+            if (best < 0.0f || cost <= best) {
+                best = cost;
+                rows = r;
+            }
+        }
+        memo[0] = dev;
+        memo[1] = a.s;
+        memo[2] = a.W;
+        memo[3] = a.H;
+        memo[4] = rows;
+    }
+    const int rows = memo[4];
+    const int mch = (kTY * rows - 1) / a.s + 2;
+    const int maxCells = mcw * mch;
+    const size_t smem = sizeof(float4) * (size_t(maxCells) * kCellStride + (mcw + 2) * (mch + 2));
+    if (smem > 48 * 1024)  // one row per thread at s = 3: 12 x 4 cells fit in 48 KB
+        cudaFuncSetAttribute(k_solve32x, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    dim3 grid(unsigned(tilesX), (a.H + kTY * rows - 1) / (kTY * rows));
+    k_solve32x<<<grid, kThreads, smem, ctx->stream>>>(a, packed, forceFallback, nanFlag, maxCells,
+                                                        rows);
     ++ctx->launches;
     return cudaGetLastError();
 }
