@@ -80,6 +80,14 @@ __device__ __forceinline__ void track_key2(float& K1, float& K2, float a, float 
     K1 = fminf(fminf(K1, a), b);
 }
 
+// Lexicographic pair k (i <= j over 9 candidates: rows start at 0, 9, 17,
+// 24, 30, 35, 39, 42, 44) -> (i, j).
+__device__ __forceinline__ void lex_pair(int k, int& i, int& j) {
+    i = (k >= 9) + (k >= 17) + (k >= 24) + (k >= 30) + (k >= 35) + (k >= 39) + (k >= 42) +
+        (k >= 44);
+    j = k - (i * 9 - i * (i - 1) / 2) + i;
+}
+
 struct PackedWindow {
     const float4* win;
     int pw, nwx;
@@ -90,8 +98,116 @@ struct PackedWindow {
 };
 
 #ifndef GLU_X_MIN_BLOCKS
-#define GLU_X_MIN_BLOCKS 5  // 48 registers: 40 warps per SM
+#define GLU_X_MIN_BLOCKS 4  // 64 registers: 32 warps per SM
 #endif
+
+// The close-call resolution (rare: a few pixels in 10^4; kept out of line so
+// that it does not add register pressure to the scan).  Returns the pick
+// (ok = false: an off-grid close pair, the pixel takes the double path).
+struct ClosePick {
+    int bi, bj;
+    float w;
+    bool ok, wSet;
+};
+
+__device__ __noinline__ ClosePick resolve_close(const float4* swin, const float4* tab, int cw,
+                                                float ip0, float ip1, float ip2, float lim,
+                                                unsigned kmask, float4 ci, float4 cj, int bi,
+                                                int bj, double eps,
+                                                unsigned long long* counters) {
+    constexpr float kOneMinusE = 1.0f - kCE * kU;
+    bool ok = true, wSet = false;
+    float wClose = 0.0f;
+    // rare: the pairs whose key is within lim (bit k = lexicographic
+    // pair k, i <= j, the winner included) hold the reference's first
+    // argmin (every other pair's objective exceeds the winner's): if
+    // they all carry the winner's colour tuple, the first of them is
+    // the pick; otherwise they are evaluated in double, in
+    // lexicographic order (ascending bits).  The keys are recomputed
+    // by the scan's instruction sequence, so they are the same values.
+    unsigned long long close = 0;
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+        const float4 v = swin[(j / 3) * cw + j % 3];
+        const float e0 = v.x - ip0, e1 = v.y - ip1, e2 = v.z - ip2;
+        const float qj = __fmaf_rn(e2, e2, __fmaf_rn(e1, e1, __fmul_rn(e0, e0)));
+        const float qm = __fmaf_rn(qj, kOneMinusE, -1e-36f);
+#pragma unroll
+        for (int i = 0; i <= j; ++i) {
+            float key;
+            if (i < j) {
+                const float4 d = tab[i * 8 - i * (i - 1) / 2 + (j - i - 1)];
+                const float dn = __fmaf_rn(e0, d.x, __fmaf_rn(e1, d.y, e2 * d.z));
+                key = pack_key(__fmaf_rn(-dn, dn, qm), i, kmask);
+            } else {
+                key = pack_key(qm, j, kmask);
+            }
+            if (key <= lim) close |= 1ull << (i * 9 - i * (i - 1) / 2 + (j - i));
+        }
+    }
+    bool mixed = false;
+    int fi = -1, fj = -1;
+    for (unsigned long long m = close; m; m &= m - 1) {
+        int i, j;
+        lex_pair(__ffsll(static_cast<long long>(m)) - 1, i, j);
+        const float4 vi = swin[(i / 3) * cw + i % 3], vj = swin[(j / 3) * cw + j % 3];
+        if (!(vi.x < kInf && vj.x < kInf)) ok = false;  // off-grid member (+inf sentinel)
+        const bool same = same_rgb(vi, ci) && same_rgb(vj, cj);
+        mixed |= !same;
+        if (same && fi < 0) {
+            fi = i;
+            fj = j;
+        }
+    }
+    if (ok && !mixed) {
+        bi = fi;  // identical colours: identical objectives and weight
+        bj = fj;
+    } else if (ok && mixed) {
+        const float ip[3] = {ip0, ip1, ip2};
+        double best = 0, bw = 0;
+        int ni = -1, nj = -1;
+        for (unsigned long long m = close; m; m &= m - 1) {
+            int i, j;
+            lex_pair(__ffsll(static_cast<long long>(m)) - 1, i, j);
+            const float4 vi = swin[(i / 3) * cw + i % 3];
+            const float4 vj = swin[(j / 3) * cw + j % 3];
+            const float a3[3] = {vi.x, vi.y, vi.z}, b3[3] = {vj.x, vj.y, vj.z};
+            const double wv = weight_exact64(ip, a3, b3, eps);
+            const double o = objective64(ip, a3, b3, wv, eps);
+            if (ni < 0 || o < best) {
+                best = o;
+                bw = wv;
+                ni = i;
+                nj = j;
+            }
+        }
+        bi = ni;
+        bj = nj;
+        wClose = float(bw);
+        wSet = true;
+        if (counters) atomicAdd(counters + 1, 1ull);
+    }
+    return ClosePick{bi, bj, wClose, ok, wSet};
+}
+
+// The reference's exact double-precision path for one pixel (NaN inputs,
+// underflow-sized distances, off-grid close pairs, forced fallback): out of
+// line like resolve_close.  Returns {a, b, bits(w)}.
+__device__ __noinline__ uint3 solve_double(const SolveArgs& a, const float4* packed, int cx, int cy,
+                                           float ip0, float ip1, float ip2) {
+    const int pw = a.lw + 2;  // h = 1
+    const int wx0 = max(0, cx - 1), wy0 = max(0, cy - 1);
+    const int nwx = min(a.lw - 1, cx + 1) - wx0 + 1;
+    const int nwy = min(a.lh - 1, cy + 1) - wy0 + 1;
+    const float ip[3] = {ip0, ip1, ip2};
+    PackedWindow pwin{packed + size_t(wy0 + 1) * pw + (wx0 + 1), pw, nwx};
+    const Pick pk = pick_exact64(ip, pwin, nwx * nwy, a.eps);
+    const int ar = pk.ai / nwx, br = pk.bi / nwx;
+    if (a.fallbacks) atomicAdd(a.fallbacks, 1ull);
+    return make_uint3(uint32_t(wy0 + ar) * uint32_t(a.lw) + uint32_t(wx0 + pk.ai - ar * nwx),
+                      uint32_t(wy0 + br) * uint32_t(a.lw) + uint32_t(wx0 + pk.bi - br * nwx),
+                      __float_as_uint(float(pk.w)));
+}
 
 // The tile's staged candidate cells and pair table (shared memory).
 struct XTile {
@@ -105,7 +221,6 @@ struct XTile {
 __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* packed, const XTile& t,
                                             int forceFallback, int x, int y, float ip0, float ip1,
                                             float ip2) {
-    const int pw = a.lw + 2;  // h = 1
     const int cw = t.cw;
     const size_t p = size_t(y) * a.W + x;
     const int cx = div_s(x, a), cy = div_s(y, a);
@@ -166,26 +281,24 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
     bool ok = !forceFallback && K1 < kInf && ip0 == ip0 && ip1 == ip1 && ip2 == ip2 &&
               (qmin >= 1e-27f || qmin == 0.0f);
     // An exact colour match I_j0 == I_p: the pairs (i, j0) have objective 0
-    // in double (w = 0, v = 0) and every other pair a positive one, so the
-    // reference's pick is the lexicographically first: (i0, j0), i0 the first
-    // in-grid candidate, j0 the first exact match.  (Every LR sample pixel
-    // lands here.)  A zero fp32 distance must be a true colour match (else
-    // the pixel takes the double path).
+    // in double (w = 0, v = 0) and every other pair a positive one (a
+    // non-matching colour has a nonzero double distance, even where its fp32
+    // distance underflows), so the reference's pick is the lexicographically
+    // first: (i0, j0), i0 the first in-grid candidate, j0 the first exact
+    // match.  (Every LR sample pixel lands here.)  A zero fp32 distance
+    // without an exact match (underflow) takes the double path.
     bool exactZero = false;
     if (ok && qmin == 0.0f) {
         int j0 = -1;
-#pragma unroll 1
-        for (int k = 0; k < 9; ++k) {
+#pragma unroll
+        for (int k = 8; k >= 0; --k) {
             const float4 v = swin[(k / 3) * cw + k % 3];
-            const float e0 = v.x - ip0, e1 = v.y - ip1, e2 = v.z - ip2;
-            const float qk = __fmaf_rn(e2, e2, __fmaf_rn(e1, e1, __fmul_rn(e0, e0)));
-            if (qk != 0.0f) continue;
-            if (!(e0 == 0.0f && e1 == 0.0f && e2 == 0.0f)) ok = false;
-            if (j0 < 0) j0 = k;
+            j0 = (v.x == ip0 && v.y == ip1 && v.z == ip2) ? k : j0;
         }
+        ok = j0 >= 0;
         exactZero = ok;
         bi = (cy == 0 ? 3 : 0) + (cx == 0 ? 1 : 0);
-        bj = j0;
+        bj = max(j0, 0);
     }
     float4 ci = swin[(bi / 3) * cw + bi % 3], cj = swin[(bj / 3) * cw + bj % 3];
     bool wSet = false;  // w settled in double over the close set
@@ -199,74 +312,13 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
 #ifdef GLU_X_COUNT_RECHECK
             if (a.fallbacks) atomicAdd(a.fallbacks + 1, 1ull);
 #endif
-            // rare: the pairs whose key is within lim (bit k = lexicographic
-            // pair k, the winner included) hold the reference's first argmin
-            // (every other pair's objective exceeds the winner's): if they all
-            // carry the winner's colour tuple, the first of them is the pick;
-            // otherwise they are evaluated in double, in lexicographic order.
-            unsigned long long close = 0;
-            bool mixed = false;
-            int fi = -1, fj = -1, k = 0;
-#pragma unroll 1
-            for (int i = 0; i < 9; ++i) {
-                const float4 vi = swin[(i / 3) * cw + i % 3];
-                const bool ini = vi.x < kInf;  // the +inf sentinel marks off-grid cells
-#pragma unroll 1
-                for (int j = i; j < 9; ++j, ++k) {
-                    const float4 vj = swin[(j / 3) * cw + j % 3];
-                    const float e0 = vj.x - ip0, e1 = vj.y - ip1, e2 = vj.z - ip2;
-                    const float qj = __fmaf_rn(e2, e2, __fmaf_rn(e1, e1, __fmul_rn(e0, e0)));
-                    const float qm = __fmaf_rn(qj, kOneMinusE, -1e-36f);
-                    float key;
-                    if (j != i) {
-                        const float4 d = tab[i * 8 - i * (i - 1) / 2 + (j - i - 1)];
-                        const float dn = __fmaf_rn(e0, d.x, __fmaf_rn(e1, d.y, e2 * d.z));
-                        key = pack_key(__fmaf_rn(-dn, dn, qm), i, kmask);
-                    } else {
-                        key = pack_key(qm, j, kmask);
-                    }
-                    if (!(key <= lim)) continue;  // not close (NaN: outside the grid)
-                    if (!(ini && qj < kInf)) ok = false;  // off-grid member
-                    close |= 1ull << k;
-                    const bool same = same_rgb(vi, ci) && same_rgb(vj, cj);
-                    mixed |= !same;
-                    if (same && fi < 0) {
-                        fi = i;
-                        fj = j;
-                    }
-                }
-            }
-            if (ok && !mixed) {
-                bi = fi;  // identical colours: identical objectives and weight
-                bj = fj;
-            } else if (ok && mixed) {
-                const float ip[3] = {ip0, ip1, ip2};
-                double best = 0, bw = 0;
-                int ni = -1, nj = -1;
-                int i = 0, j = 0;
-#pragma unroll 1
-                for (int kk = 0; kk < 45; ++kk) {
-                    if (close >> kk & 1ull) {
-                        const float4 vi = swin[(i / 3) * cw + i % 3];
-                        const float4 vj = swin[(j / 3) * cw + j % 3];
-                        const float a3[3] = {vi.x, vi.y, vi.z}, b3[3] = {vj.x, vj.y, vj.z};
-                        const double wv = weight_exact64(ip, a3, b3, a.eps);
-                        const double o = objective64(ip, a3, b3, wv, a.eps);
-                        if (ni < 0 || o < best) {
-                            best = o;
-                            bw = wv;
-                            ni = i;
-                            nj = j;
-                        }
-                    }
-                    if (++j == 9) j = ++i;
-                }
-                bi = ni;
-                bj = nj;
-                wClose = float(bw);
-                wSet = true;
-                if (a.fallbacks) atomicAdd(a.fallbacks + 1, 1ull);
-            }
+            const ClosePick c = resolve_close(swin, tab, cw, ip0, ip1, ip2, lim, kmask, ci, cj, bi,
+                                              bj, a.eps, a.fallbacks);
+            ok = c.ok;
+            bi = c.bi;
+            bj = c.bj;
+            wSet = c.wSet;
+            wClose = c.w;
         }
     }
     uint32_t ia, ib;
@@ -278,17 +330,10 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
         const float a3[3] = {ci.x, ci.y, ci.z}, b3[3] = {cj.x, cj.y, cj.z};
         w = wSet ? wClose : weight_exact64_f(ip, a3, b3, a.eps);
     } else {
-        const int wx0 = max(0, cx - 1), wy0 = max(0, cy - 1);
-        const int nwx = min(a.lw - 1, cx + 1) - wx0 + 1;
-        const int nwy = min(a.lh - 1, cy + 1) - wy0 + 1;
-        const float ip[3] = {ip0, ip1, ip2};
-        PackedWindow pwin{packed + size_t(wy0 + 1) * pw + (wx0 + 1), pw, nwx};
-        const Pick pk = pick_exact64(ip, pwin, nwx * nwy, a.eps);
-        const int ar = pk.ai / nwx, br = pk.bi / nwx;
-        ia = uint32_t(wy0 + ar) * uint32_t(a.lw) + uint32_t(wx0 + pk.ai - ar * nwx);
-        ib = uint32_t(wy0 + br) * uint32_t(a.lw) + uint32_t(wx0 + pk.bi - br * nwx);
-        w = float(pk.w);
-        if (a.fallbacks) atomicAdd(a.fallbacks, 1ull);
+        const uint3 r = solve_double(a, packed, cx, cy, ip0, ip1, ip2);
+        ia = r.x;
+        ib = r.y;
+        w = __uint_as_float(r.z);
     }
     if (a.params) {
         unsigned* o = reinterpret_cast<unsigned*>(a.params + p);
@@ -371,13 +416,13 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS)
 #pragma unroll 1
     for (int k = 0; k < rows; ++k) {
         const int y = yb + k * kTY;
-        const float ip0 = g0, ip1 = g1, ip2 = g2;
-        if (k + 1 < rows && xin && y + kTY < a.H) {  // the next pixel's colour, one scan ahead
-            const float* g = a.high + 3 * (size_t(y + kTY) * a.W + x);
+        if (k > 0 && xin && y < a.H) {  // (prefetching one scan ahead measured slower)
+            const float* g = a.high + 3 * (size_t(y) * a.W + x);
             g0 = __ldg(g);
             g1 = __ldg(g + 1);
             g2 = __ldg(g + 2);
         }
+        const float ip0 = g0, ip1 = g1, ip2 = g2;
         if (xin && y < a.H) solve_pixel(a, packed, t, forceFallback, x, y, ip0, ip1, ip2);
     }
 }
