@@ -241,7 +241,7 @@ def run_ours(args, ws, rank, local):
     import ctypes as C
     fp32_tflops, fp32_mhz = G.fp32_peak(local)
 
-    def step(events=None):
+    def step(events=None, md=mode, dst=out):
         # one frame per call of the public frame API (glu_cu_upsample_frames:
         # k_frame_prep = grid_downsample + matte + LR packing, then k_solve32
         # fused with the 1-ch apply), bracketed by events on the context stream
@@ -250,8 +250,8 @@ def run_ours(args, ws, rank, local):
             if events is not None:
                 events[f][0].record()
             G.N.check(lib.glu_cu_upsample_frames(ctx.handle, C.c_void_p(fr.data_ptr()), 1,
-                                                 C.byref(gc), C.byref(cc), int(mode), 1,
-                                                 C.c_void_p(out[f].data_ptr()), None))
+                                                 C.byref(gc), C.byref(cc), int(md), 1,
+                                                 C.c_void_p(dst[f].data_ptr()), None))
             if events is not None:
                 events[f][1].record()
 
@@ -329,6 +329,30 @@ def run_ours(args, ws, rank, local):
         roofline["issue_bound"] = {
             "warp_instr_per_launch": winstr, "floor_ms": floor_ms,
             "frac": floor_ms / k_ms, "source": "profiles/r01_ncu_solve32.md (ncu --set full)"}
+    if args.mode == "fast":
+        # The north star's pair search ("every LR candidate pair (i, j)") is
+        # the reference's Exact mode: the same frames through the same entry
+        # point with mode = Exact (k_solve32x), timed per launch after the
+        # main timed region (not part of `value`).
+        xmode = glu.mode_from_name("exact")
+        xout = torch.empty_like(out)
+        step(md=xmode, dst=xout)
+        torch.cuda.synchronize()
+        xev = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(nf)]
+               for _ in range(3)]
+        for k in range(3):
+            step(xev[k], md=xmode, dst=xout)
+        torch.cuda.synchronize()
+        x_ms = statistics.mean(xev[k][f][0].elapsed_time(xev[k][f][1]) for k in range(3)
+                               for f in range(nf))
+        xflops, _ = algorithmic_work(W_, H_, SCALE, 3, "exact", 1)
+        roofline["pair_search"] = {
+            "mode": "exact", "kernel": "k_solve32x (fused optimize_field + 1-ch apply_field) "
+            "with its k_frame_prep launch", "kernel_ms": x_ms,
+            "algorithmic_flops_per_launch": xflops,
+            "achieved": xflops / (x_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+            "frac": xflops / (x_ms * 1e-3) / 1e12 / fp32_tflops,
+            "value": nf * W_ * H_ / (nf * x_ms * 1e-3) / 1e6, "value_unit": "HR Mpix/s"}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             hbm = json.load(fh)["hbm_gbs"]
