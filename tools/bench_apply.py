@@ -26,6 +26,7 @@ p = argparse.ArgumentParser()
 p.add_argument("--targets", type=int, default=64)
 p.add_argument("--channels", type=int, default=3)
 p.add_argument("--cpu", action="store_true")
+p.add_argument("--tag", default="")
 a = p.parse_args()
 
 W, H, s = 7680, 4320, 16
