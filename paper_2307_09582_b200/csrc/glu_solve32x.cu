@@ -18,6 +18,8 @@
 // recomputed in double in the reference's order.
 #include <cuda_runtime.h>
 
+#include <cassert>
+
 #include "glu_internal.h"
 #include "glu_math.cuh"
 
@@ -214,6 +216,9 @@ struct XTile {
     const float4* wcells;  // candidate cells of the tile's owner cells (+- 1), cw per row
     const float4* table;   // kCellStride float4 per owner cell: D' of its 36 pairs
     int cw, ncw, ocx0, ocy0;
+#ifdef GLU_X_DEBUG
+    int nrow, nwin, ntab;  // owner-cell rows, staged cells, table float4s (bounds checks)
+#endif
 };
 
 // One HR pixel (x, y) with guide colour (ip0, ip1, ip2): the pair search,
@@ -227,6 +232,11 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
     // the window in shared memory: candidate j is swin[(j / 3) * cw + j % 3]
     const float4* swin = t.wcells + (cy - t.ocy0) * cw + (cx - t.ocx0);
     const float4* tab = t.table + ((cy - t.ocy0) * t.ncw + (cx - t.ocx0)) * kCellStride;
+#ifdef GLU_X_DEBUG  // bounds of the staged window / table (debug builds)
+    assert(cy >= t.ocy0 && cx >= t.ocx0 && cx - t.ocx0 < t.ncw && cy - t.ocy0 + 2 < t.nrow + 2);
+    assert((cy - t.ocy0 + 2) * cw + (cx - t.ocx0) + 2 < t.nwin);
+    assert(((cy - t.ocy0) * t.ncw + (cx - t.ocx0) + 1) * kCellStride <= t.ntab);
+#endif
 
     // j-outer scan: pair (i, j) needs only e_j = I_j - I_p and q_j = |e_j|^2
     // (D'_ij = D_ij / sqrt(den) comes from the cell's table: obj = q_j -
@@ -365,7 +375,7 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
 
 __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS)
     k_solve32x(SolveArgs a, const float4* packed, int forceFallback, const unsigned* nanFlag,
-               int maxCells, int rows) {
+               int maxCells, int maxWin, int rows) {
     extern __shared__ float4 smem[];
     float4* table = smem;                         // maxCells * kCellStride
     float4* wcells = smem + maxCells * kCellStride;  // the tile's candidate cells
@@ -412,7 +422,12 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS)
     }
     __syncthreads();
 
+#ifdef GLU_X_DEBUG
+    assert(ncw * nch <= maxCells && cw * (nch + 2) <= maxWin);
+    const XTile t{wcells, table, cw, ncw, ocx0, ocy0, nch, cw * (nch + 2), maxCells * kCellStride};
+#else
     const XTile t{wcells, table, cw, ncw, ocx0, ocy0};
+#endif
 #pragma unroll 1
     for (int k = 0; k < rows; ++k) {
         const int y = yb + k * kTY;
@@ -478,7 +493,7 @@ cudaError_t launch_solve32x(glu_ctx* ctx, const SolveArgs& a, const float4* pack
         cudaFuncSetAttribute(k_solve32x, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     dim3 grid(unsigned(tilesX), (a.H + kTY * rows - 1) / (kTY * rows));
     k_solve32x<<<grid, kThreads, smem, ctx->stream>>>(a, packed, forceFallback, nanFlag, maxCells,
-                                                        rows);
+                                                        (mcw + 2) * (mch + 2), rows);
     ++ctx->launches;
     return cudaGetLastError();
 }
