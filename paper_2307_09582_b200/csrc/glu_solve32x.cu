@@ -103,6 +103,13 @@ struct PackedWindow {
 #define GLU_X_MIN_BLOCKS 4  // 64 registers: 32 warps per SM
 #endif
 
+// Offset of window candidate j (row j / 3, column j % 3) in a staged window
+// of pitch cw; (j * 11) >> 5 == j / 3 for j < 9.
+__device__ __forceinline__ int woff(int j, int cw) {
+    const int r = (j * 11) >> 5;
+    return r * cw + (j - 3 * r);
+}
+
 // The close-call resolution (rare: a few pixels in 10^4; kept out of line so
 // that it does not add register pressure to the scan).  Returns the pick
 // (ok = false: an off-grid close pair, the pixel takes the double path).
@@ -114,10 +121,10 @@ struct ClosePick {
 
 __device__ __noinline__ ClosePick resolve_close(const float4* swin, const float4* tab, int cw,
                                                 float ip0, float ip1, float ip2, float lim,
-                                                unsigned kmask, float4 ci, float4 cj, int bi,
-                                                int bj, double eps,
+                                                unsigned kmask, int bi, int bj, double eps,
                                                 unsigned long long* counters) {
     constexpr float kOneMinusE = 1.0f - kCE * kU;
+    const float4 ci = swin[woff(bi, cw)], cj = swin[woff(bj, cw)];
     bool ok = true, wSet = false;
     float wClose = 0.0f;
     // rare: the pairs whose key is within lim (bit k = lexicographic
@@ -195,19 +202,20 @@ __device__ __noinline__ ClosePick resolve_close(const float4* swin, const float4
 // The reference's exact double-precision path for one pixel (NaN inputs,
 // underflow-sized distances, off-grid close pairs, forced fallback): out of
 // line like resolve_close.  Returns {a, b, bits(w)}.
-__device__ __noinline__ uint3 solve_double(const SolveArgs& a, const float4* packed, int cx, int cy,
+__device__ __noinline__ uint3 solve_double(const float4* packed, int lw, int lh, double eps,
+                                           unsigned long long* counters, int cx, int cy,
                                            float ip0, float ip1, float ip2) {
-    const int pw = a.lw + 2;  // h = 1
+    const int pw = lw + 2;  // h = 1
     const int wx0 = max(0, cx - 1), wy0 = max(0, cy - 1);
-    const int nwx = min(a.lw - 1, cx + 1) - wx0 + 1;
-    const int nwy = min(a.lh - 1, cy + 1) - wy0 + 1;
+    const int nwx = min(lw - 1, cx + 1) - wx0 + 1;
+    const int nwy = min(lh - 1, cy + 1) - wy0 + 1;
     const float ip[3] = {ip0, ip1, ip2};
     PackedWindow pwin{packed + size_t(wy0 + 1) * pw + (wx0 + 1), pw, nwx};
-    const Pick pk = pick_exact64(ip, pwin, nwx * nwy, a.eps);
+    const Pick pk = pick_exact64(ip, pwin, nwx * nwy, eps);
     const int ar = pk.ai / nwx, br = pk.bi / nwx;
-    if (a.fallbacks) atomicAdd(a.fallbacks, 1ull);
-    return make_uint3(uint32_t(wy0 + ar) * uint32_t(a.lw) + uint32_t(wx0 + pk.ai - ar * nwx),
-                      uint32_t(wy0 + br) * uint32_t(a.lw) + uint32_t(wx0 + pk.bi - br * nwx),
+    if (counters) atomicAdd(counters, 1ull);
+    return make_uint3(uint32_t(wy0 + ar) * uint32_t(lw) + uint32_t(wx0 + pk.ai - ar * nwx),
+                      uint32_t(wy0 + br) * uint32_t(lw) + uint32_t(wx0 + pk.bi - br * nwx),
                       __float_as_uint(float(pk.w)));
 }
 
@@ -310,11 +318,11 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
         bi = (cy == 0 ? 3 : 0) + (cx == 0 ? 1 : 0);
         bj = max(j0, 0);
     }
-    float4 ci = swin[(bi / 3) * cw + bi % 3], cj = swin[(bj / 3) * cw + bj % 3];
     bool wSet = false;  // w settled in double over the close set
     float wClose = 0.0f;
     if (ok && !exactZero) {
         // the winner's q (the scan's instruction sequence, so the same value)
+        const float4 cj = swin[woff(bj, cw)];
         const float eb0 = cj.x - ip0, eb1 = cj.y - ip1, eb2 = cj.z - ip2;
         const float qb = __fmaf_rn(eb2, eb2, __fmaf_rn(eb1, eb1, __fmul_rn(eb0, eb0)));
         const float lim = K1 + __fmaf_rn(kT, qb, 2e-36f);
@@ -322,8 +330,8 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
 #ifdef GLU_X_COUNT_RECHECK
             if (a.fallbacks) atomicAdd(a.fallbacks + 1, 1ull);
 #endif
-            const ClosePick c = resolve_close(swin, tab, cw, ip0, ip1, ip2, lim, kmask, ci, cj, bi,
-                                              bj, a.eps, a.fallbacks);
+            const ClosePick c =
+                resolve_close(swin, tab, cw, ip0, ip1, ip2, lim, kmask, bi, bj, a.eps, a.fallbacks);
             ok = c.ok;
             bi = c.bi;
             bj = c.bj;
@@ -331,16 +339,20 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
             wClose = c.w;
         }
     }
+    // (the pair's colours are re-read here rather than kept live across the
+    // out-of-line call, which would spill them on every pixel)
+    const float4 ci = swin[woff(bi, cw)], cj = swin[woff(bj, cw)];
     uint32_t ia, ib;
     float w;
     if (ok) {
-        ia = uint32_t(cy - 1 + bi / 3) * uint32_t(a.lw) + uint32_t(cx - 1 + bi % 3);
-        ib = uint32_t(cy - 1 + bj / 3) * uint32_t(a.lw) + uint32_t(cx - 1 + bj % 3);
+        const int ri = (bi * 11) >> 5, rj = (bj * 11) >> 5;
+        ia = uint32_t(cy - 1 + ri) * uint32_t(a.lw) + uint32_t(cx - 1 + bi - 3 * ri);
+        ib = uint32_t(cy - 1 + rj) * uint32_t(a.lw) + uint32_t(cx - 1 + bj - 3 * rj);
         const float ip[3] = {ip0, ip1, ip2};
         const float a3[3] = {ci.x, ci.y, ci.z}, b3[3] = {cj.x, cj.y, cj.z};
         w = wSet ? wClose : weight_exact64_f(ip, a3, b3, a.eps);
     } else {
-        const uint3 r = solve_double(a, packed, cx, cy, ip0, ip1, ip2);
+        const uint3 r = solve_double(packed, a.lw, a.lh, a.eps, a.fallbacks, cx, cy, ip0, ip1, ip2);
         ia = r.x;
         ib = r.y;
         w = __uint_as_float(r.z);
