@@ -184,3 +184,31 @@ def test_oracle_vs_reference_fresh_seeds(oracle, reference):
         b = reference.joint_optimize(img, 4, 3, TAU_DEFAULT)
         assert same(a["low"], b["low"]) and same(a["errors"], b["errors"])
         assert (a["accepted"], a["rejected"]) == (b["accepted"], b["rejected"])
+
+
+def nonfinite_scene(W=96, H=72, seed=41):
+    """A seeded scene with NaN / +inf / -inf channels sprinkled over it (some on
+    LR sample pixels, so the LR image holds them too)."""
+    from paper_2307_09582_b200 import workloads
+    img = workloads.scene(W, H, seed).copy()
+    rng = np.random.default_rng(seed)
+    for val in (np.nan, np.inf, -np.inf):
+        ys, xs, cs = rng.integers(0, H, 12), rng.integers(0, W, 12), rng.integers(0, 3, 12)
+        img[ys, xs, cs] = val
+    img[2, 2, :] = np.inf          # an LR sample pixel at s = 4 (centre offset 2)
+    img[6, 10, 1] = np.nan
+    return img
+
+
+@pytest.mark.parametrize("S", [3, 5])
+def test_oracle_vs_reference_nonfinite(oracle, reference, S):
+    # IEEE comparisons with NaN / inf in the reference's scans (upsample.cpp:49-104):
+    # the restatement must follow them operation for operation
+    img = nonfinite_scene()
+    for s in (4, 8):
+        low = reference.grid_downsample(img, s)
+        assert same(oracle.grid_downsample(img, s), low)
+        for m in ("fast", "exact", "gnu"):
+            want = reference.optimize_field(img, low, s, S, EPS_DEFAULT, m)
+            got = oracle.optimize_field(img, low, s, S, EPS_DEFAULT, m)
+            assert same(got, want), (s, m)

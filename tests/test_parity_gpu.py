@@ -413,3 +413,27 @@ def test_parallel_schedule_with_off_chip_and_whole_grid_trials(glu, kind):
             (b.iterations, b.trialsAccepted, b.trialsRejected)
         assert torch.equal(a.low, b.low) and torch.equal(a.field.params, b.field.params)
         assert torch.equal(a.errors, b.errors)
+
+
+@pytest.mark.parametrize("S", [3, 5])
+def test_nonfinite_inputs_match_oracle(glu, oracle, S):
+    # NaN / +inf / -inf channels in the guide (and, through grid_downsample, in
+    # the LR image): every solver setting must follow the reference's IEEE
+    # comparisons bit for bit (the fp32 filters route such pixels / solves to
+    # the double path)
+    from test_oracle import nonfinite_scene
+    img = nonfinite_scene()
+    ctx = glu.glu.context()
+    for s in (4, 8):
+        high = dev(img)
+        low, grid = glu.grid_downsample(high, s)
+        lo = oracle.grid_downsample(img, s)
+        assert same(low.cpu().numpy(), lo)
+        for m in ("fast", "exact", "gnu"):
+            want = oracle.optimize_field(img, lo, s, S, EPS_DEFAULT, m)
+            for solver in (0, 1, 2):
+                ctx.set_solver(solver)
+                f = glu.optimize_field(high, low, grid, glu.GluConfig(windowSide=S), mode_of(glu, m))
+                ctx.set_solver(0)
+                got = host_params(f.params)
+                assert same(got, want), (s, m, solver, int((got != want).sum()))
