@@ -149,6 +149,9 @@ CASES = [  # (W, H, s, S, seed): ragged sizes, every supported window class
     # tiles narrower than a warp, windows wider than the LR grid
     (33, 5, 4, 3, 18), (7, 300, 3, 5, 19), (1000, 9, 8, 3, 20), (257, 129, 32, 5, 21),
     (5, 5, 2, 3, 22), (17, 200, 16, 7, 23), (96, 64, 2, 3, 24),
+    # the exact kernel's tile shapes: s = 3 (one row per thread, 12 x 4 owner
+    # cells per tile) and a larger s = 5 / s = 7 frame (several rows per thread)
+    (301, 211, 3, 3, 25), (1203, 1001, 5, 3, 26), (1500, 700, 7, 3, 27),
 ]
 
 
