@@ -352,7 +352,15 @@ def run_ours(args, ws, rank, local):
             "algorithmic_flops_per_launch": xflops,
             "achieved": xflops / (x_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
             "frac": xflops / (x_ms * 1e-3) / 1e12 / fp32_tflops,
-            "value": nf * W_ * H_ / (nf * x_ms * 1e-3) / 1e6, "value_unit": "HR Mpix/s"}
+            "value": nf * W_ * H_ / (nf * x_ms * 1e-3) / 1e6, "value_unit": "HR Mpix/s",
+            "traffic": load_traffic().get("solve_apply_exact_c3")}
+        xinstr = load_traffic().get("solve_apply_exact_c3_warp_instr")
+        if xinstr:
+            sms = torch.cuda.get_device_properties(local).multi_processor_count
+            xfloor = xinstr / (4 * sms * fp32_mhz * 1e6) * 1e3
+            roofline["pair_search"]["issue_bound"] = {
+                "warp_instr_per_launch": xinstr, "floor_ms": xfloor, "frac": xfloor / x_ms,
+                "source": "profiles/r01_ncu_solve32x_exact.md (ncu --set full)"}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             hbm = json.load(fh)["hbm_gbs"]

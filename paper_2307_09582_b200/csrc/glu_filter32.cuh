@@ -163,13 +163,37 @@ __device__ inline Filter32Result filter32_pixel(const float4 (&c)[9], const floa
 // Exact mode (S = 3) for ONE pixel on a candidate array: the selection of
 // k_solve32x (glu_solve32x.cu) with D' = D / sqrt(den)
 // formed per pair instead of read from a per-cell table.  Pairs (i <= j) are
-// scanned j-outer; exact zeros and close calls recover the reference's
-// lexicographic first; mixed close sets are settled in double; NaN, off-grid
-// close members and underflow-sized distances take the exact path (ok false).
-// ja / jb are the slots of the pair (i, j), w the stored weight.
+// scanned j-outer, each reduced to one key (the fp32 objective lowered by its
+// bound, row i in the low 4 mantissa bits); the smallest key K1 and the
+// second smallest K2 decide the pick unless K2 is within the winner's bound.
+// Exact colour matches pick (first in-grid slot, first match); close calls
+// re-derive the keys, take the first of an all-same-colour close set or
+// settle it in double in lexicographic order; NaN, off-grid close members and
+// underflow-sized distances take the exact path (ok false).  ja / jb are the
+// slots of the pair (i, j), w the stored weight.
+__device__ __forceinline__ float f32x_pack(float t, int i, unsigned mask) {
+    unsigned r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEC;" : "=r"(r) : "r"(__float_as_uint(t)), "r"(unsigned(i)),
+        "r"(mask));
+    return __uint_as_float(r);
+}
+
+__device__ __forceinline__ void f32x_track(float& K1, float& K2, float k) {
+    K2 = fmaxf(fminf(K2, k), K1);
+    K1 = fminf(K1, k);
+}
+
+__device__ __forceinline__ void f32x_track2(float& K1, float& K2, float a, float b) {
+    float mx;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(mx) : "f"(a), "f"(b));
+    K2 = fmaxf(fminf(fminf(K2, a), b), fminf(K1, mx));
+    K1 = fminf(fminf(K1, a), b);
+}
+
 __device__ inline Filter32Result filter32x_pixel(const float4 (&c)[9], const float* ip, float epsf,
                                                  double eps) {
-    constexpr float kU = 5.9604645e-08f, kE = 64.0f * kU;
+    constexpr float kU = 5.9604645e-08f, kE = 64.0f * kU, kOneMinusE = 1.0f - kE;
+    constexpr float kT = 136.0f * kU;
     constexpr float kInf = __builtin_huge_valf();
     const float ip0 = ip[0], ip1 = ip[1], ip2 = ip[2];
     Filter32Result r{false, 1, 0, 0, 0.0f};
@@ -182,118 +206,98 @@ __device__ inline Filter32Result filter32x_pixel(const float4 (&c)[9], const flo
             if (m == k) v = c[m];
         return v;
     };
-    auto dprime = [&](const float4& vi, const float4& vj, float& d0, float& d1, float& d2) {
-        d0 = vi.x - vj.x;
-        d1 = vi.y - vj.y;
-        d2 = vi.z - vj.z;
-        const float den = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmaf_rn(d0, d0, epsf)));
-        const float rr = f32_rsqrt_approx(den);
-        d0 *= rr;
-        d1 *= rr;
-        d2 *= rr;
-    };
     auto qof = [&](const float4& v, float& e0, float& e1, float& e2) {
         e0 = v.x - ip0;
         e1 = v.y - ip1;
         e2 = v.z - ip2;
         return __fmaf_rn(e2, e2, __fmaf_rn(e1, e1, __fmul_rn(e0, e0)));
     };
-    float qmin = kInf, b1 = kInf, m2 = kInf, bme = kInf;
-    int bk = 0;
+    // key of pair (i, j), i < j (the same instruction sequence in the scan and
+    // the close-call re-check)
+    auto pair_t = [&](const float4& vi, const float4& vj, float e0, float e1, float e2,
+                      float qm) {
+        const float d0 = vi.x - vj.x, d1 = vi.y - vj.y, d2 = vi.z - vj.z;
+        const float den = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmaf_rn(d0, d0, epsf)));
+        const float rr = f32_rsqrt_approx(den);
+        const float dn = __fmaf_rn(e0, d0 * rr, __fmaf_rn(e1, d1 * rr, e2 * (d2 * rr)));
+        return __fmaf_rn(-dn, dn, qm);
+    };
+    const unsigned kmask = 0xfffffff0u | (__float_as_uint(epsf) >> 31);  // opaque: a register
+    float qmin = kInf, K1 = kInf, K2 = kInf;
+    int bj = 0;
     bool nan = false;
 #pragma unroll
     for (int j = 0; j < 9; ++j) {
         float e0, e1, e2;
         const float qj = qof(c[j], e0, e1, e2);
         nan |= qj != qj;
-        const float qej = __fmaf_rn(kE, qj, 1e-36f);
         qmin = fminf(qmin, qj);
+        const float qm = __fmaf_rn(qj, kOneMinusE, -1e-36f);
+        const float k1in = K1;
+        float pend = 0.0f;
 #pragma unroll
         for (int i = 0; i < j; ++i) {
-            float d0, d1, d2;
-            dprime(c[i], c[j], d0, d1, d2);
-            const float dn = __fmaf_rn(e0, d0, __fmaf_rn(e1, d1, e2 * d2));
-            const float o = __fmaf_rn(-dn, dn, qj);
-            const float tt = o - qej;
-            const bool lt = o < b1;
-            m2 = fminf(m2, lt ? bme : tt);
-            bme = lt ? tt : bme;
-            b1 = lt ? o : b1;
-            bk = lt ? (i << 4 | j) : bk;
+            const float key = f32x_pack(pair_t(c[i], c[j], e0, e1, e2, qm), i, kmask);
+            if (i & 1)
+                f32x_track2(K1, K2, pend, key);
+            else
+                pend = key;
         }
-        const float tt = qj - qej;  // (j, j): w = 0
-        const bool lt = qj < b1;
-        m2 = fminf(m2, lt ? bme : tt);
-        bme = lt ? tt : bme;
-        b1 = lt ? qj : b1;
-        bk = lt ? (j << 4 | j) : bk;
+        const float kd = f32x_pack(qm, j, kmask);  // (j, j): w = 0
+        if (j & 1)
+            f32x_track2(K1, K2, pend, kd);
+        else
+            f32x_track(K1, K2, kd);
+        bj = K1 != k1in ? j : bj;
     }
-    if (nan || !(b1 < kInf) || ip0 != ip0 || ip1 != ip1 || ip2 != ip2 ||
+    if (nan || !(K1 < kInf) || ip0 != ip0 || ip1 != ip1 || ip2 != ip2 ||
         !(qmin >= 1e-27f || qmin == 0.0f))
         return r;
-    int bi = bk >> 4, bj = bk & 15;
-    float4 ci = c[0], cj = c[0];
-#pragma unroll
-    for (int k = 1; k < 9; ++k) {
-        if (k == bi) ci = c[k];
-        if (k == bj) cj = c[k];
-    }
-    const float eb = __fmaf_rn(kE, __fmaf_rn(cj.z - ip2, cj.z - ip2,
-                                             __fmaf_rn(cj.y - ip1, cj.y - ip1,
-                                                       __fmul_rn(cj.x - ip0, cj.x - ip0))),
-                               1e-36f);
-    // an exact-zero distance must be a true colour match (no underflow)
-    if (qmin == 0.0f) {
-#pragma unroll
-        for (int k = 0; k < 9; ++k) {
-            float e0, e1, e2;
-            if (qof(c[k], e0, e1, e2) == 0.0f && !(e0 == 0.0f && e1 == 0.0f && e2 == 0.0f))
-                return r;
-        }
-    }
+    int bi = int(__float_as_uint(K1) & 15u);
     bool wSet = false;
     float wv = 0.0f;
-    if (b1 == 0.0f && cj.x == ip0 && cj.y == ip1 && cj.z == ip2) {
-        // exact zeros: the lexicographically first is (first in-grid slot, first
-        // exact colour match)
+    if (qmin == 0.0f) {
+        // exact colour match: (first in-grid slot, first exact match); a zero
+        // distance without a match (underflow) takes the exact path
         int i0 = -1, j0 = -1;
 #pragma unroll
-        for (int k = 0; k < 9; ++k) {
+        for (int k = 8; k >= 0; --k) {
             float e0, e1, e2;
-            const float qk = qof(c[k], e0, e1, e2);
-            if (i0 < 0 && qk < kInf) i0 = k;
-            if (j0 < 0 && qk == 0.0f) j0 = k;
+            if (qof(c[k], e0, e1, e2) < kInf) i0 = k;
+            if (c[k].x == ip0 && c[k].y == ip1 && c[k].z == ip2) j0 = k;
         }
+        if (j0 < 0 || i0 < 0) return r;
         bi = i0;
         bj = j0;
+    } else {
+        float e0, e1, e2;
+        const float qb = qof(at(bj), e0, e1, e2);
+        const float lim = K1 + __fmaf_rn(kT, qb, 2e-36f);
+        if (K2 <= lim) {
+            // close call: the pairs whose key is within lim (bit k =
+            // lexicographic pair k) hold the reference's first argmin
+            unsigned long long close = 0;
 #pragma unroll
-        for (int k = 0; k < 9; ++k) {
-            if (k == bi) ci = c[k];
-            if (k == bj) cj = c[k];
-        }
-    } else if (m2 <= b1 + eb) {
-        // close call: lexicographic re-check of the close pairs
-        unsigned long long close = 0;
-        bool mixed = false;
-        int fi = -1, fj = -1, k = 0;
-        for (int i = 0; i < 9; ++i) {
-            const float4 vi = at(i);
-            for (int j = i; j < 9; ++j, ++k) {
-                const float4 vj = at(j);
-                float e0, e1, e2;
-                const float qj = qof(vj, e0, e1, e2);
-                float o = qj;
-                if (j != i) {
-                    float d0, d1, d2;
-                    dprime(vi, vj, d0, d1, d2);
-                    const float dn = __fmaf_rn(e0, d0, __fmaf_rn(e1, d1, e2 * d2));
-                    o = __fmaf_rn(-dn, dn, qj);
+            for (int j = 0; j < 9; ++j) {
+                const float qj = qof(c[j], e0, e1, e2);
+                const float qm = __fmaf_rn(qj, kOneMinusE, -1e-36f);
+#pragma unroll
+                for (int i = 0; i <= j; ++i) {
+                    const float key = i < j ? f32x_pack(pair_t(c[i], c[j], e0, e1, e2, qm), i, kmask)
+                                            : f32x_pack(qm, j, kmask);
+                    if (key <= lim) close |= 1ull << (i * 9 - i * (i - 1) / 2 + (j - i));
                 }
-                const bool best = i == bi && j == bj;
-                if (!best && (!(o <= kInf) || !(o - __fmaf_rn(kE, qj, 1e-36f) <= b1 + eb)))
-                    continue;
-                if (!(vi.x < kInf && qj < kInf)) return r;  // off-grid member
-                close |= 1ull << k;
+            }
+            const float4 ci = at(bi), cj = at(bj);
+            bool mixed = false;
+            int fi = -1, fj = -1;
+            for (unsigned long long m = close; m; m &= m - 1) {
+                const int k = __ffsll(static_cast<long long>(m)) - 1;
+                const int i = (k >= 9) + (k >= 17) + (k >= 24) + (k >= 30) + (k >= 35) +
+                              (k >= 39) + (k >= 42) + (k >= 44);
+                const int j = k - (i * 9 - i * (i - 1) / 2) + i;
+                const float4 vi = at(i), vj = at(j);
+                if (!(vi.x < kInf && vj.x < kInf)) return r;  // off-grid member
                 const bool same = vi.x == ci.x && vi.y == ci.y && vi.z == ci.z &&
                                   vj.x == cj.x && vj.y == cj.y && vj.z == cj.z;
                 mixed |= !same;
@@ -302,15 +306,17 @@ __device__ inline Filter32Result filter32x_pixel(const float4 (&c)[9], const flo
                     fj = j;
                 }
             }
-        }
-        if (!mixed) {
-            bi = fi;  // identical colours: identical objective and weight
-            bj = fj;
-        } else {
-            double best = 0, bw = 0;
-            int ni = -1, nj = -1, i = 0, j = 0;
-            for (int kk = 0; kk < 45; ++kk) {
-                if (close >> kk & 1ull) {
+            if (!mixed) {
+                bi = fi;  // identical colours: identical objective and weight
+                bj = fj;
+            } else {
+                double best = 0, bw = 0;
+                int ni = -1, nj = -1;
+                for (unsigned long long m = close; m; m &= m - 1) {
+                    const int k = __ffsll(static_cast<long long>(m)) - 1;
+                    const int i = (k >= 9) + (k >= 17) + (k >= 24) + (k >= 30) + (k >= 35) +
+                                  (k >= 39) + (k >= 42) + (k >= 44);
+                    const int j = k - (i * 9 - i * (i - 1) / 2) + i;
                     const float4 vi = at(i), vj = at(j);
                     const float a3[3] = {vi.x, vi.y, vi.z}, b3[3] = {vj.x, vj.y, vj.z};
                     const double wd = weight_exact64(ip, a3, b3, eps);
@@ -322,15 +328,15 @@ __device__ inline Filter32Result filter32x_pixel(const float4 (&c)[9], const flo
                         nj = j;
                     }
                 }
-                if (++j == 9) j = ++i;
+                bi = ni;
+                bj = nj;
+                wSet = true;
+                wv = float(bw);
             }
-            bi = ni;
-            bj = nj;
-            wSet = true;
-            wv = float(bw);
         }
     }
     if (!wSet) {
+        const float4 ci = at(bi), cj = at(bj);
         const float a3[3] = {ci.x, ci.y, ci.z}, b3[3] = {cj.x, cj.y, cj.z};
         wv = weight_exact64_f(ip, a3, b3, eps);
     }

@@ -25,6 +25,8 @@ p.add_argument("--config", type=int, nargs="+", default=[2, 4])
 p.add_argument("--reps", type=int, default=3)
 p.add_argument("--cpu", action="store_true")
 p.add_argument("--trials", type=int, default=0, help="GLU_OPT_TRIALS (0 speculative, 2 dataflow)")
+p.add_argument("--mode", default="fast", choices=["fast", "exact", "gnu"])
+p.add_argument("--tag", default="")
 a = p.parse_args()
 
 # Under torchrun (WORLD_SIZE > 1) the level-synchronous multi-rank loop runs
@@ -65,17 +67,18 @@ for c in a.config:
     W, H, s = cfg["W"], cfg["H"], cfg["scale"]
     img = workloads.scene(W, H, c, 0)
     high = torch.from_numpy(img).cuda()
-    r = glu.joint_optimize(high, s)  # warm-up
+    md = glu.mode_from_name(a.mode)
+    r = glu.joint_optimize(high, s, None, md)  # warm-up
     torch.cuda.synchronize()
     times = []
     for _ in range(a.reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        r = glu.joint_optimize(high, s)
+        r = glu.joint_optimize(high, s, None, md)
         e1.record()
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))
-    line = {"config": cfg["name"], "gpu_ms": min(times), "gpu_ms_all": times,
+    line = {"config": cfg["name"], "mode": a.mode, "tag": a.tag, "gpu_ms": min(times), "gpu_ms_all": times,
             "iterations": r.iterations, "accepted": r.trialsAccepted,
             "rejected": r.trialsRejected, "components": r.components,
             "hr_mpix_per_s": W * H / (min(times) * 1e-3) / 1e6}
@@ -84,7 +87,7 @@ for c in a.config:
         ref = oracle.Reference()
         ref.set_num_threads(0)
         t0 = time.perf_counter()
-        o = ref.joint_optimize(img, s)
+        o = ref.joint_optimize(img, s, mode=a.mode)
         line["cpu_ms"] = 1e3 * (time.perf_counter() - t0)
         line["cpu_threads"] = os.cpu_count()
         line["parity"] = bool(
