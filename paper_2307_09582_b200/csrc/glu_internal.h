@@ -37,7 +37,7 @@ namespace glu_cu {
 enum Slot {
     S_HIGH = 0, S_LOW, S_PARAMS, S_OUT, S_ERR, S_AUX, S_PIX,
     S_CCL_LABEL, S_CCL_LIST, S_CCL_OFF, S_CCL_MISC, S_TRIAL, S_TRIAL2, S_TRIAL3,
-    S_SPARE1, S_SPARE2, S_PACKED, S_SCHED, S_SCHED_META, S_PARK, S_PARK_TMP
+    S_SPARE1, S_SPARE2, S_PACKED, S_SCHED, S_SCHED_META, S_PARK, S_PARK_TMP, S_TARGET4
 };
 
 void set_error(const std::string& msg);
