@@ -24,7 +24,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
                   "-diag-suppress", "177,550",
                   "-I" + INCLUDE]
-CUDA_SRCS = ["glu_kernels.cu", "glu_solve32.cu", "glu_solve32x.cu", "glu_ccl.cu",
+CUDA_SRCS = ["glu_kernels.cu", "glu_solve32.cu", "glu_solve32f.cu", "glu_solve32x.cu", "glu_ccl.cu",
              "glu_joint.cu", "glu_glup.cu", "glu_metrics.cu", "glu_baselines.cu", "glu_capi.cu"]
 CUDA_SO = os.path.join(LIB, "libglu_cuda.so")
 CPP_SO = os.path.join(LIB, "libglu.so")

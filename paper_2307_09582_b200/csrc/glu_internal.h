@@ -74,6 +74,10 @@ cudaError_t launch_solve32(glu_ctx* ctx, const SolveArgs& a, int forceFallback);
 // solve (a.lowT must already point at `low` or `matte`).
 cudaError_t launch_frame_solve32(glu_ctx* ctx, const SolveArgs& a, float* low, float* matte,
                                  int forceFallback);
+// glu_solve32f.cu: Fast, S = 3 (tile-staged, keyed closed-form stage B).
+bool solve32f_supported(int mode, int S);
+cudaError_t launch_solve32f(glu_ctx* ctx, const SolveArgs& a, const float4* packed,
+                            int forceFallback, const unsigned* nanFlag);
 bool solve32x_supported(int mode, int S, int s);
 cudaError_t launch_solve32x(glu_ctx* ctx, const SolveArgs& a, const float4* packed,
                             int forceFallback, const unsigned* nanFlag);

@@ -111,7 +111,8 @@ __global__ void k_pack_low(const float* __restrict__ low, int lw, int lh, int h,
     float4 v = make_float4(kInf, kInf, kInf, 0.0f);
     if (x >= 0 && y >= 0 && x < lw && y < lh) {
         const float* s = low + 3 * (size_t(y) * lw + x);
-        v = make_float4(s[0], s[1], s[2], 0.0f);
+        // .w: the cell's largest |channel| (k_solve32f's rounding floor)
+        v = make_float4(s[0], s[1], s[2], fmaxf(fabsf(s[0]), fmaxf(fabsf(s[1]), fabsf(s[2]))));
         if (v.x != v.x || v.y != v.y || v.z != v.z) atomicOr(nanFlag, 1u);
     }
     packed[i] = v;
@@ -350,6 +351,11 @@ cudaError_t dispatch(glu_ctx* ctx, const SolveArgs& a, const float4* packed, int
     if (a.mode == GLU_MODE_GNU)
         return a.S == 3 ? launch_t<3, GLU_MODE_GNU>(ctx, a, packed, forceFallback, nanFlag)
                         : launch_t<5, GLU_MODE_GNU>(ctx, a, packed, forceFallback, nanFlag);
+#ifndef GLU_SOLVE_F
+#define GLU_SOLVE_F 1
+#endif
+    if (GLU_SOLVE_F && solve32f_supported(a.mode, a.S))
+        return launch_solve32f(ctx, a, packed, forceFallback, nanFlag);
     return a.S == 3 ? launch_t<3, GLU_MODE_FAST>(ctx, a, packed, forceFallback, nanFlag)
                     : launch_t<5, GLU_MODE_FAST>(ctx, a, packed, forceFallback, nanFlag);
 }
@@ -368,7 +374,8 @@ __global__ void k_frame_prep(const float* __restrict__ high, int W, int H, int s
     if (cx >= 0 && cy >= 0 && cx < lw && cy < lh) {
         const int x = min(cx * s + s / 2, W - 1), y = min(cy * s + s / 2, H - 1);
         const float* src = high + 3 * (size_t(y) * W + x);
-        v = make_float4(src[0], src[1], src[2], 0.0f);
+        v = make_float4(src[0], src[1], src[2],
+                        fmaxf(fabsf(src[0]), fmaxf(fabsf(src[1]), fabsf(src[2]))));
         const size_t c = size_t(cy) * lw + cx;
         low[3 * c] = v.x;
         low[3 * c + 1] = v.y;

@@ -1,0 +1,464 @@
+// glu_solve32f.cu -- Fast mode, S = 3: tile-staged candidates and a keyed
+// closed-form stage B (fp32 filter + fp64 verify, bit-exact with the reference).
+//
+// The reference's pixelFast (upsample.cpp:49-71): a = first argmin of the
+// distance |I_j - I_p|; then for every candidate j, w_j = d_j / (d_a + d_j +
+// eps) and obj_j = |w_j I_a + (1 - w_j) I_j - I_p|^2 + eps w_j^2; b = first
+// argmin of obj_j; all in double.
+//
+// Stage A is k_solve32's (glu_solve32.cu): fp32 squared distances, the first
+// argmin, and a check that no candidate of a different colour lies within
+// 32u q_min of it (else the pixel takes the double path).
+//
+// Stage B uses the closed form of the objective at w_j = d_j / s_j,
+// s_j = d_a + eps + d_j (with q = d^2, c_j = e_a . e_j, e = I - I_p):
+//     obj_j = (A q_j + B d_j c_j) / s_j^2,
+//     A = q_a + (d_a + eps)^2 + eps,  B = 2 (d_a + eps),
+// 12 instructions per candidate (k_solve32's form needs 22).  Each candidate
+// becomes one key: the fp32 value lowered by G q_j / s_j^2, G = 96u (A + B
+// d_a), with the candidate's index in the low 4 mantissa bits.  The fp32
+// error of the closed form is below 49u T_j / s_j^2 (T_j = q_j (A + B d_a);
+// the rounding of the key and the 15-ulp packing add 35u), and F = 2^-44 (M^2
+// + eps) covers the reference's own double rounding (<= 2^-45.8 M^2 + 2^-51
+// eps, M the largest |channel| of the pixel and its window), so a key is a
+// lower bound of the reference's objective and key + 2 G q_j / s_j^2 + F an
+// upper bound.  The smallest key K1 and the second
+// smallest K2 decide b unless K2 is within the winner's upper bound; such
+// close calls re-derive the keys and settle the close set in double in index
+// order.  The stored weight is the reference's (float)(d_b / (d_a + d_b +
+// eps)), verified in double (weight_fast_verified, glu_math.cuh).
+//
+// Layout: like k_solve32x, a CTA stages its tile's candidate cells (the
+// packed LR image: float4 cells with a +inf border, .w = the cell's largest
+// |channel|) in shared memory once and solves 1-8 rows of pixels per thread;
+// the rare paths (close calls, the double path) are out of line with scalar
+// arguments, so the scans stay in registers.
+#include <cuda_runtime.h>
+
+#include "glu_internal.h"
+#include "glu_math.cuh"
+
+namespace glu_cu {
+
+namespace {
+
+constexpr int kTX = 32, kTY = 8, kThreads = kTX * kTY;
+constexpr int kMaxRows = 8;
+constexpr float kStageCost = 0.3f;  // a tile's staging, in units of one row of pixels
+constexpr float kU = 5.9604645e-08f;  // 2^-24
+constexpr float kCA = 32.0f;          // stage A relative margin (in u)
+constexpr float kG = 96.0f * kU;      // key offset, in u (A + B d_a)
+constexpr float kF = 5.684342e-14f;   // 2^-44
+constexpr float kInf = __builtin_huge_valf();
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float fast_sqrt(float q) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(q));
+    return r;
+}
+__device__ __forceinline__ float fmax_nan(float a, float b) {  // NaN if either is NaN
+    float r;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
+
+__device__ __forceinline__ int div_s(int v, const SolveArgs& a) {
+    return a.sdiv ? int(__umulhi(unsigned(v), a.sdiv)) : v / a.s;
+}
+
+__device__ __forceinline__ bool same_rgb(float4 a, float4 b) {
+    return a.x == b.x && a.y == b.y && a.z == b.z;
+}
+
+// Offset of window candidate j (row j / 3, column j % 3) in a staged window of
+// pitch cw; (j * 11) >> 5 == j / 3 for j < 9.
+__device__ __forceinline__ int woff(int j, int cw) {
+    const int r = (j * 11) >> 5;
+    return r * cw + (j - 3 * r);
+}
+
+// Candidate j's key (see the header): the packed (B d_j c_j + (A - G) q_j) / s_j^2.  `mask` = 0xfffffff0 is held in a
+// register so that (t & mask) | j is one LOP3.  Off-grid candidates (q = inf)
+// give NaN keys.
+// (b0, b1, b2) = B e_a, so the dot is B c_j directly.
+__device__ __forceinline__ float fast_key(float e0, float e1, float e2, float qj, float b0,
+                                          float b1, float b2, float at, float Ap, int j,
+                                          unsigned mask) {
+    const float bc = __fmaf_rn(e2, b2, __fmaf_rn(e1, b1, __fmul_rn(e0, b0)));
+    const float dj = fast_sqrt(qj);
+    const float nl = __fmaf_rn(dj, bc, __fmul_rn(Ap, qj));
+    const float sj = __fadd_rn(at, dj);
+    const float t = __fmul_rn(nl, rcp_approx(__fmul_rn(sj, sj)));
+    unsigned r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEC;" : "=r"(r) : "r"(__float_as_uint(t)), "r"(unsigned(j)),
+        "r"(mask));
+    return __uint_as_float(r);
+}
+
+// Smallest (K1) and second smallest (K2) key; NaN keys change neither.
+__device__ __forceinline__ void track_key(float& K1, float& K2, float k) {
+    K2 = fmaxf(fminf(K2, k), K1);
+    K1 = fminf(K1, k);
+}
+// Two keys at once: second smallest of {K1 <= K2, a, b} = max(min(K2, a, b),
+// min(K1, max(a, b))), with max propagating NaN (a NaN key drops out).
+__device__ __forceinline__ void track_key2(float& K1, float& K2, float a, float b) {
+    K2 = fmaxf(fminf(fminf(K2, a), b), fminf(K1, fmax_nan(a, b)));
+    K1 = fminf(fminf(K1, a), b);
+}
+
+// The truncated window of the packed image as the reference's raster list.
+struct PackedWindow {
+    const float4* win;
+    int pw, nwx;
+    __device__ __forceinline__ const float* operator[](int i) const {
+        const int r = i / nwx, q = i - r * nwx;
+        return reinterpret_cast<const float*>(win + r * pw + q);
+    }
+};
+
+// ---- rare paths, out of line (scalar arguments) ----------------------------
+
+// The reference's double-precision pixelFast (upsample.cpp:49-71) for one
+// pixel: NaN inputs, underflow-sized distances, uncertain stage-A picks,
+// off-grid close members, forced fallback.  Returns {a, b, bits(w)}.
+__device__ __noinline__ uint3 solve_double_fast(const float4* packed, int lw, int lh, double eps,
+                                                unsigned long long* counters, int cx, int cy,
+                                                float ip0, float ip1, float ip2) {
+    const int pw = lw + 2;  // h = 1
+    const int wx0 = max(0, cx - 1), wy0 = max(0, cy - 1);
+    const int nwx = min(lw - 1, cx + 1) - wx0 + 1;
+    const int nwy = min(lh - 1, cy + 1) - wy0 + 1;
+    const float ip[3] = {ip0, ip1, ip2};
+    PackedWindow pwin{packed + size_t(wy0 + 1) * pw + (wx0 + 1), pw, nwx};
+    const Pick pk = pick_fast64(ip, pwin, nwx * nwy, eps);
+    const int ar = pk.ai / nwx, br = pk.bi / nwx;
+    if (counters) atomicAdd(counters, 1ull);
+    return make_uint3(uint32_t(wy0 + ar) * uint32_t(lw) + uint32_t(wx0 + pk.ai - ar * nwx),
+                      uint32_t(wy0 + br) * uint32_t(lw) + uint32_t(wx0 + pk.bi - br * nwx),
+                      __float_as_uint(float(pk.w)));
+}
+
+struct CloseFast {
+    int jb;
+    float w;
+    bool ok, wExact;
+};
+
+// Stage-B close call: the candidates whose key is within lim hold the
+// reference's first argmin (every other objective exceeds the winner's).  The
+// keys are re-derived by the scan's instruction sequence (the same values).
+// All of the winner's colour: the first of them; else the set is settled in
+// double, in index order; an off-grid member sends the pixel to the double
+// path.
+__device__ __noinline__ CloseFast resolve_close_fast(const float4* swin, int cw, float ip0,
+                                                     float ip1, float ip2, float at, float b0,
+                                                     float b1, float b2, float Ap, float lim,
+                                                     unsigned kmask, int ja, int jb, double eps,
+                                                     unsigned long long* counters) {
+    const float4 ca = swin[woff(ja, cw)], cb = swin[woff(jb, cw)];
+    CloseFast r{jb, 0.0f, true, false};
+    unsigned close = 0;
+    bool mixed = false;
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+        const float4 v = swin[woff(j, cw)];
+        const float d0 = v.x - ip0, d1 = v.y - ip1, d2 = v.z - ip2;
+        const float qj = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmul_rn(d0, d0)));
+        const float key = fast_key(d0, d1, d2, qj, b0, b1, b2, at, Ap, j, kmask);
+        if (key <= lim) {
+            if (!(qj < kInf)) r.ok = false;
+            close |= 1u << j;
+            mixed |= !same_rgb(v, cb);
+        }
+    }
+    if (!r.ok) return r;
+    if (!mixed) {
+        r.jb = __ffs(close) - 1;  // identical colours: identical objectives
+        return r;
+    }
+    const float ip[3] = {ip0, ip1, ip2};
+    const float a3[3] = {ca.x, ca.y, ca.z};
+    const double dA = dist64(ip, a3);
+    double best = 0, bw = 0;
+    int bj = -1;
+    for (unsigned m = close; m; m &= m - 1) {
+        const int j = __ffs(m) - 1;
+        const float4 v = swin[woff(j, cw)];
+        const float cj[3] = {v.x, v.y, v.z};
+        const double dj = dist64(ip, cj);
+        const double wj = dj / (dA + dj + eps);
+        const double o = objective64(ip, a3, cj, wj, eps);
+        if (bj < 0 || o < best) {
+            best = o;
+            bw = wj;
+            bj = j;
+        }
+    }
+    r.jb = bj;
+    r.w = float(bw);
+    r.wExact = true;
+    if (counters) atomicAdd(counters + 1, 1ull);
+    return r;
+}
+
+// (float) of the reference's weight for (a, b) when the verified estimate is
+// ambiguous (probability ~2^-24 per pixel): IEEE sqrt / division.
+__device__ __noinline__ float weight_fast_ieee(float ip0, float ip1, float ip2, float4 ca,
+                                               float4 cb, double eps) {
+    const float ip[3] = {ip0, ip1, ip2};
+    const float a3[3] = {ca.x, ca.y, ca.z}, b3[3] = {cb.x, cb.y, cb.z};
+    const double dA = dist64(ip, a3), dB = dist64(ip, b3);
+    return float(dB / (dA + dB + eps));
+}
+
+// The tile's staged candidate cells (shared memory).
+struct FTile {
+    const float4* wcells;  // owner cells of the tile +- 1, cw per row
+    int cw, ocx0, ocy0;
+};
+
+__device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* packed, const FTile& t,
+                                            int forceFallback, int x, int y, float ip0, float ip1,
+                                            float ip2) {
+    const int cw = t.cw;
+    const size_t p = size_t(y) * a.W + x;
+    const int cx = div_s(x, a), cy = div_s(y, a);
+    const float4* swin = t.wcells + (cy - t.ocy0) * cw + (cx - t.ocx0);
+
+    // ---- stage A: a = first argmin |I_j - I_p| (compared as squares) -------
+    // Each candidate's q_j as a key with its index in the low 4 mantissa bits
+    // (<= 15 ulp = 30u): K1a (smallest) gives a = the first argmin of the fp32
+    // distances up to keys within 30u of each other, and K2a (second
+    // smallest) screens for the near ties that need the exact check below.
+    // (q_j is recomputed where it is needed again, by the same instruction
+    // sequence: kept live across the stages it spills.)
+    const unsigned kmask = 0xfffffff0u | (unsigned(a.W) >> 31);  // opaque: a register
+    float K1a = kInf, K2a = kInf, pa = 0.0f, mw = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+        const float4 v = swin[woff(j, cw)];
+        mw = fmaxf(mw, v.w);
+        const float d0 = v.x - ip0, d1 = v.y - ip1, d2 = v.z - ip2;
+        const float qq = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmul_rn(d0, d0)));
+        unsigned kb;
+        asm("lop3.b32 %0, %1, %2, %3, 0xEC;" : "=r"(kb) : "r"(__float_as_uint(qq)), "r"(unsigned(j)),
+            "r"(kmask));
+        const float key = __uint_as_float(kb);
+        if (j & 1)
+            track_key2(K1a, K2a, pa, key);
+        else if (j == 8)
+            track_key(K1a, K2a, key);
+        else
+            pa = key;
+    }
+    const int ja = int(__float_as_uint(K1a) & 15u);
+    const float4 ca = swin[woff(ja, cw)];
+    const float ea0 = ca.x - ip0, ea1 = ca.y - ip1, ea2 = ca.z - ip2;
+    const float m1 = __fmaf_rn(ea2, ea2, __fmaf_rn(ea1, ea1, __fmul_rn(ea0, ea0)));  // q_a
+    const bool exactA = ca.x == ip0 && ca.y == ip1 && ca.z == ip2;
+    // NaN inputs and underflow-sized distances go to the exact path.
+    bool ok = !forceFallback && K1a < kInf && ip0 == ip0 && ip1 == ip1 && ip2 == ip2 &&
+              (m1 >= 1e-27f || exactA);
+    // any other candidate within (1 + 32u) q_a has a key within K1a (1 + 128u)
+    if (ok && K2a <= __fmaf_rn(K1a, 128.0f * kU, K1a) + 2e-36f) {
+        const float lim = __fmaf_rn(m1, kCA * kU, m1) + 1e-36f;
+#pragma unroll 1
+        for (int j = 0; j < 9; ++j) {
+            const float4 v = swin[woff(j, cw)];
+            const float d0 = v.x - ip0, d1 = v.y - ip1, d2 = v.z - ip2;
+            const float qq = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmul_rn(d0, d0)));
+            if (j != ja && !(qq > lim) && !same_rgb(v, ca)) ok = false;
+        }
+    }
+    int jb = ja;
+    float w = 0.0f;
+    bool wExact = false;  // w settled in double (close-set path)
+    if (ok && !exactA) {  // exact match I_a == I_p: b = a (the first exact zero), w = 0
+        // ---- stage B: b = first argmin of the objective at w_j ---------------
+        const float eps = a.epsf;
+        const float da = fast_sqrt(m1);
+        const float at = da + eps;
+        const float A = __fadd_rn(__fmaf_rn(at, at, m1), eps);
+        const float B = at + at;
+        const float G = kG * __fmaf_rn(B, da, A);
+        const float Ap = A - G;
+        const float b0 = B * ea0, b1 = B * ea1, b2 = B * ea2;
+        float K1 = kInf, K2 = kInf, pend = 0.0f;
+#pragma unroll
+        for (int j = 0; j < 9; ++j) {
+            const float4 v = swin[woff(j, cw)];
+            const float d0 = v.x - ip0, d1 = v.y - ip1, d2 = v.z - ip2;
+            const float qj = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmul_rn(d0, d0)));
+            const float key = fast_key(d0, d1, d2, qj, b0, b1, b2, at, Ap, j, kmask);
+            if (j & 1)
+                track_key2(K1, K2, pend, key);
+            else if (j == 8)
+                track_key(K1, K2, key);
+            else
+                pend = key;
+        }
+        jb = int(__float_as_uint(K1) & 15u);
+        // the winner's upper bound: K1 + 2 G q_b / s_b^2 + F
+        const float4 cb = swin[woff(jb, cw)];
+        const float qb = __fmaf_rn(cb.z - ip2, cb.z - ip2,
+                                   __fmaf_rn(cb.y - ip1, cb.y - ip1, __fmul_rn(cb.x - ip0, cb.x - ip0)));
+        const float sb = __fadd_rn(at, fast_sqrt(qb));
+        const float m = fmaxf(mw, fmaxf(fabsf(ip0), fmaxf(fabsf(ip1), fabsf(ip2))));
+        const float F = kF * __fmaf_rn(m, m, eps);
+        const float lim = K1 + __fmaf_rn(2.0f * G * qb, rcp_approx(__fmul_rn(sb, sb)), F);
+        if (!(K1 < kInf)) {
+            ok = false;
+        } else if (K2 <= lim) {
+            const CloseFast c = resolve_close_fast(swin, cw, ip0, ip1, ip2, at, b0, b1, b2, Ap, lim,
+                                                   kmask, ja, jb, a.eps, a.fallbacks);
+            ok = c.ok;
+            jb = c.jb;
+            wExact = c.wExact;
+            w = c.w;
+        }
+    }
+    uint32_t ia, ib;
+    if (ok) {
+        const int ra = (ja * 11) >> 5, rb = (jb * 11) >> 5;
+        ia = uint32_t(cy - 1 + ra) * uint32_t(a.lw) + uint32_t(cx - 1 + ja - 3 * ra);
+        ib = uint32_t(cy - 1 + rb) * uint32_t(a.lw) + uint32_t(cx - 1 + jb - 3 * rb);
+        if (!wExact) {
+            const float4 cb = swin[woff(jb, cw)];
+            const float ip[3] = {ip0, ip1, ip2};
+            const float a3[3] = {ca.x, ca.y, ca.z}, b3[3] = {cb.x, cb.y, cb.z};
+            bool wok = false;
+            w = weight_fast_verified(ip, a3, b3, a.eps, &wok);
+            if (!wok) w = weight_fast_ieee(ip0, ip1, ip2, ca, cb, a.eps);
+        }
+    } else {
+        const uint3 r =
+            solve_double_fast(packed, a.lw, a.lh, a.eps, a.fallbacks, cx, cy, ip0, ip1, ip2);
+        ia = r.x;
+        ib = r.y;
+        w = __uint_as_float(r.z);
+    }
+    if (a.params) {
+        unsigned* o = reinterpret_cast<unsigned*>(a.params + p);
+        o[0] = ia;
+        o[1] = ib;
+        o[2] = __float_as_uint(w);
+    }
+    if (a.lowT) {
+        const bool clamp = a.clamp != 0;
+        if (a.channels == 1) {  // the video path's matte target
+            a.out[p] = lerp_clamp(w, __ldg(a.lowT + ia), __ldg(a.lowT + ib), clamp);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                a.out[3 * p + k] = lerp_clamp(w, __ldg(a.lowT + 3 * size_t(ia) + k),
+                                              __ldg(a.lowT + 3 * size_t(ib) + k), clamp);
+        }
+    }
+    if (a.errOut) {  // pixel_error of the clamped self reconstruction (jointopt.cpp:190)
+        float r[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            r[k] = lerp_clamp(w, __ldg(a.low + 3 * size_t(ia) + k), __ldg(a.low + 3 * size_t(ib) + k),
+                              true);
+        const float ipx[3] = {ip0, ip1, ip2};
+        a.errOut[p] = pixel_error(ipx, r);
+    }
+}
+
+#ifndef GLU_F_MIN_BLOCKS
+#define GLU_F_MIN_BLOCKS 4  // 64 registers: 32 warps per SM
+#endif
+
+__global__ void __launch_bounds__(kThreads, GLU_F_MIN_BLOCKS)
+    k_solve32f(SolveArgs a, const float4* packed, int forceFallback, const unsigned* nanFlag,
+               int rows) {
+    extern __shared__ float4 wcells[];  // the tile's candidate cells (owner cells +- 1)
+    forceFallback |= int(__ldg(nanFlag));
+    const int pw = a.lw + 2;  // h = 1
+    const int tileH = kTY * rows;
+    const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * tileH;
+    const int ocx0 = div_s(x0, a), ocy0 = div_s(y0, a);
+    const int ncw = div_s(min(x0 + kTX - 1, a.W - 1), a) - ocx0 + 1;
+    const int nch = div_s(min(y0 + tileH - 1, a.H - 1), a) - ocy0 + 1;
+    const int cw = ncw + 2;
+    // the first pixel's guide colour is requested before the staging barrier
+    const int x = x0 + (threadIdx.x % kTX), yb = y0 + (threadIdx.x / kTX);
+    const bool xin = x < a.W;
+    float g0 = 0.0f, g1 = 0.0f, g2 = 0.0f;
+    if (xin && yb < a.H) {
+        const float* g = a.high + 3 * (size_t(yb) * a.W + x);
+        g0 = __ldg(g);
+        g1 = __ldg(g + 1);
+        g2 = __ldg(g + 2);
+    }
+    // packed cell (c - 1) of the LR grid is at padded index c
+    for (int k = threadIdx.x; k < cw * (nch + 2); k += kThreads)
+        wcells[k] = __ldg(packed + size_t(ocy0 + k / cw) * pw + (ocx0 + k % cw));
+    __syncthreads();
+    const FTile t{wcells, cw, ocx0, ocy0};
+#pragma unroll 1
+    for (int k = 0; k < rows; ++k) {
+        const int y = yb + k * kTY;
+        if (k > 0 && xin && y < a.H) {
+            const float* g = a.high + 3 * (size_t(y) * a.W + x);
+            g0 = __ldg(g);
+            g1 = __ldg(g + 1);
+            g2 = __ldg(g + 2);
+        }
+        if (xin && y < a.H) solve_pixel(a, packed, t, forceFallback, x, y, g0, g1, g2);
+    }
+}
+
+}  // namespace
+
+bool solve32f_supported(int mode, int S) { return mode == GLU_MODE_FAST && S == 3; }
+
+cudaError_t launch_solve32f(glu_ctx* ctx, const SolveArgs& a, const float4* packed,
+                            int forceFallback, const unsigned* nanFlag) {
+    // Rows per thread: as k_solve32x -- the count minimising waves x (rows +
+    // staging cost).  Cells a tile touches: ncw <= (kTX - 1) / s + 2, nch <=
+    // (tileH - 1) / s + 2, plus the +-1 border.
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int mcw = (kTX - 1) / a.s + 2;
+    const long tilesX = (a.W + kTX - 1) / kTX;
+    thread_local int memo[5] = {-1, 0, 0, 0, 1};  // device, s, W, H -> rows
+    if (memo[0] != dev || memo[1] != a.s || memo[2] != a.W || memo[3] != a.H) {
+        int nsm = 148, rows = 1;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        float best = -1.0f;
+        for (int r = 1; r <= kMaxRows; ++r) {
+            const int mch = (kTY * r - 1) / a.s + 2;
+            const size_t sm = sizeof(float4) * size_t(mcw + 2) * (mch + 2);
+            int per = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_solve32f, kThreads, sm);
+            const long slots = long(max(per, 1)) * nsm;
+            const long tiles = tilesX * ((a.H + kTY * r - 1) / (kTY * r));
+            const float cost = float((tiles + slots - 1) / slots) * (float(r) + kStageCost);
+            if (best < 0.0f || cost <= best) {
+                best = cost;
+                rows = r;
+            }
+        }
+        memo[0] = dev;
+        memo[1] = a.s;
+        memo[2] = a.W;
+        memo[3] = a.H;
+        memo[4] = rows;
+    }
+    const int rows = memo[4];
+    const int mch = (kTY * rows - 1) / a.s + 2;
+    const size_t smem = sizeof(float4) * size_t(mcw + 2) * (mch + 2);  // <= 19 x 35 cells (s = 2)
+    dim3 grid(unsigned(tilesX), (a.H + kTY * rows - 1) / (kTY * rows));
+    k_solve32f<<<grid, kThreads, smem, ctx->stream>>>(a, packed, forceFallback, nanFlag, rows);
+    ++ctx->launches;
+    return cudaGetLastError();
+}
+
+}  // namespace glu_cu

@@ -13,7 +13,7 @@ mkdir -p $V
   -std=c++17 -Xcompiler -fPIC -diag-suppress 177,550 -Iinclude -Xptxas -v "$@" \
   -c paper_2307_09582_b200/csrc/$SRC -o $V/$SRC.o 2>&1 | grep -E "registers|spill" | sed "s/^/[$NAME] /" >&2
 OBJS=""
-for f in glu_kernels glu_solve32 glu_solve32x glu_ccl glu_joint glu_glup glu_metrics glu_baselines glu_capi; do
+for f in glu_kernels glu_solve32 glu_solve32f glu_solve32x glu_ccl glu_joint glu_glup glu_metrics glu_baselines glu_capi; do
   if [ "$f.cu" = "$SRC" ]; then OBJS="$OBJS $V/$SRC.o"; else OBJS="$OBJS $L/$f.cu.o"; fi
 done
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -Xcompiler -fPIC \
