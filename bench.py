@@ -243,7 +243,7 @@ def run_ours(args, ws, rank, local):
 
     def step(events=None, md=mode, dst=out):
         # one frame per call of the public frame API (glu_cu_upsample_frames:
-        # k_frame_prep = grid_downsample + matte + LR packing, then k_solve32
+        # k_frame_prep = grid_downsample + matte + LR packing, then k_solve32f
         # fused with the 1-ch apply), bracketed by events on the context stream
         for f in range(nf):
             fr = frames[f]
@@ -310,7 +310,7 @@ def run_ours(args, ws, rank, local):
     roofline = {
         "bound": "fp32", "achieved": achieved, "peak": fp32_tflops, "unit": "TFLOP/s",
         "frac": achieved / fp32_tflops, "traffic": traffic,
-        "kernel": {"fast": "k_solve32<3,Fast>", "gnu": "k_solve32<3,Gnu>",
+        "kernel": {"fast": "k_solve32f", "gnu": "k_solve32<3,Gnu>",
                    "exact": "k_solve32x"}[args.mode] + " (fused optimize_field + 1-ch apply_field)"
                   " with its k_frame_prep launch (downsample + matte + LR packing, ~2 % of kernel_ms)",
         "fp64_verify_fraction": fallback_px / (args.steps * px_step),
@@ -328,7 +328,7 @@ def run_ours(args, ws, rank, local):
         floor_ms = winstr / (4 * sms * fp32_mhz * 1e6) * 1e3
         roofline["issue_bound"] = {
             "warp_instr_per_launch": winstr, "floor_ms": floor_ms,
-            "frac": floor_ms / k_ms, "source": "profiles/r01_ncu_solve32.md (ncu --set full)"}
+            "frac": floor_ms / k_ms, "source": "profiles/r01_ncu_solve32f.md (ncu --set full)"}
     if args.mode == "fast":
         # The north star's pair search ("every LR candidate pair (i, j)") is
         # the reference's Exact mode: the same frames through the same entry
