@@ -16,6 +16,12 @@ struct Filter32Result {
     float w;
 };
 
+// A candidate's largest |channel| (carried in the .w of staged colours: the
+// keyed Fast filter's bound on the reference's double rounding).
+__device__ __forceinline__ float max_abs3(float x, float y, float z) {
+    return fmaxf(fabsf(x), fmaxf(fabsf(y), fabsf(z)));
+}
+
 __device__ __forceinline__ float f32_sqrt_approx(float q) {
     float r;
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(q));
@@ -188,6 +194,166 @@ __device__ __forceinline__ void f32x_track2(float& K1, float& K2, float a, float
     asm("max.NaN.f32 %0, %1, %2;" : "=f"(mx) : "f"(a), "f"(b));
     K2 = fmaxf(fminf(fminf(K2, a), b), fminf(K1, mx));
     K1 = fminf(fminf(K1, a), b);
+}
+
+// Fast mode for ONE pixel with k_solve32f's closed-form keyed stage B
+// (glu_solve32f.cu): stage A as filter32_pixel; stage B
+// keys = (B d_j c_j + (A - G) q_j) / s_j^2 with the index in the low 4 bits,
+// decided by K1 / K2 unless K2 is within the winner's upper bound K1 + 2 G q_b
+// / s_b^2 + F.  F = 2^-44 (M^2 + eps) needs M, the largest |channel| of the
+// pixel and its window: the callers pass each in-grid candidate's largest
+// |channel| in c[k].w (0 for off-grid slots).
+__device__ __forceinline__ float f32k_key(float e0, float e1, float e2, float qj, float b0, float b1,
+                                          float b2, float at, float Ap, int j, unsigned mask) {
+    const float bc = __fmaf_rn(e2, b2, __fmaf_rn(e1, b1, __fmul_rn(e0, b0)));
+    const float dj = f32_sqrt_approx(qj);
+    const float nl = __fmaf_rn(dj, bc, __fmul_rn(Ap, qj));
+    const float sj = __fadd_rn(at, dj);
+    const float t = __fmul_rn(nl, f32_rcp_approx(__fmul_rn(sj, sj)));
+    unsigned r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEC;" : "=r"(r) : "r"(__float_as_uint(t)), "r"(unsigned(j)),
+        "r"(mask));
+    return __uint_as_float(r);
+}
+
+__device__ inline Filter32Result filter32k_pixel(const float4 (&c)[9], const float* ip, float epsf,
+                                                 double eps) {
+    constexpr float kU = 5.9604645e-08f, kCA = 32.0f, kG = 96.0f * kU, kF = 5.684342e-14f;
+    constexpr float kInf = __builtin_huge_valf();
+    const float ip0 = ip[0], ip1 = ip[1], ip2 = ip[2];
+    float q[9], e0[9], e1[9], e2[9];
+    float m1 = kInf, m2 = kInf;
+    int ja = 0;
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+        e0[j] = c[j].x - ip0;
+        e1[j] = c[j].y - ip1;
+        e2[j] = c[j].z - ip2;
+        const float qq = __fmaf_rn(e2[j], e2[j], __fmaf_rn(e1[j], e1[j], __fmul_rn(e0[j], e0[j])));
+        q[j] = qq;
+        const bool lt = qq < m1;
+        m2 = lt ? m1 : fminf(m2, qq);
+        m1 = lt ? qq : m1;
+        ja = lt ? j : ja;
+    }
+    Filter32Result r{false, 1, ja, ja, 1.0f};
+#pragma unroll
+    for (int j = 0; j < 9; ++j)
+        if (q[j] != q[j]) return r;  // NaN candidate: the reference's exact scan
+    float4 ca = c[0];
+    float mw = c[0].w;
+#pragma unroll
+    for (int j = 1; j < 9; ++j) {
+        if (j == ja) ca = c[j];
+        mw = fmaxf(mw, c[j].w);
+    }
+    const bool exactA = ca.x == ip0 && ca.y == ip1 && ca.z == ip2;
+    r.why = 2;
+    if (!(m1 < kInf) || ip0 != ip0 || ip1 != ip1 || ip2 != ip2 || !(m1 >= 1e-27f || exactA))
+        return r;
+    r.why = 3;
+    const float limA = __fmaf_rn(m1, kCA * kU, m1) + 1e-36f;
+    if (m2 <= limA) {
+#pragma unroll
+        for (int j = 0; j < 9; ++j)
+            if (j != ja && q[j] <= limA &&
+                !(c[j].x == ca.x && c[j].y == ca.y && c[j].z == ca.z))
+                return r;
+    }
+    int jb = ja;
+    if (!exactA) {  // exact match I_a == I_p: b = a (the first exact zero), w = 0
+        const float ea0 = ca.x - ip0, ea1 = ca.y - ip1, ea2 = ca.z - ip2;
+        const float da = f32_sqrt_approx(m1);
+        const float at = da + epsf;
+        const float A = __fadd_rn(__fmaf_rn(at, at, m1), epsf);
+        const float B = at + at;
+        const float G = kG * __fmaf_rn(B, da, A);
+        const float Ap = A - G;
+        const float b0 = B * ea0, b1 = B * ea1, b2 = B * ea2;
+        const unsigned kmask = 0xfffffff0u | (__float_as_uint(epsf) >> 31);  // opaque: a register
+        float K1 = kInf, K2 = kInf, pend = 0.0f;
+#pragma unroll
+        for (int j = 0; j < 9; ++j) {
+            const float key = f32k_key(e0[j], e1[j], e2[j], q[j], b0, b1, b2, at, Ap, j, kmask);
+            if (j & 1)
+                f32x_track2(K1, K2, pend, key);
+            else if (j == 8)
+                f32x_track(K1, K2, key);
+            else
+                pend = key;
+        }
+        r.why = 4;
+        if (!(K1 < kInf)) return r;
+        jb = int(__float_as_uint(K1) & 15u);
+        float qb = q[0];
+        float4 cb = c[0];
+#pragma unroll
+        for (int j = 1; j < 9; ++j)
+            if (j == jb) {
+                qb = q[j];
+                cb = c[j];
+            }
+        const float sb = __fadd_rn(at, f32_sqrt_approx(qb));
+        const float m = fmaxf(mw, fmaxf(fabsf(ip0), fmaxf(fabsf(ip1), fabsf(ip2))));
+        const float F = kF * __fmaf_rn(m, m, epsf);
+        const float lim = K1 + __fmaf_rn(2.0f * G * qb, f32_rcp_approx(__fmul_rn(sb, sb)), F);
+        if (K2 <= lim) {
+            // close call: the candidates whose key is within lim hold the
+            // reference's first argmin; all of the winner's colour: the first
+            // of them, else settled in double in index order
+            unsigned close = 0;
+            bool mixed = false;
+#pragma unroll
+            for (int j = 0; j < 9; ++j) {
+                const float key = f32k_key(e0[j], e1[j], e2[j], q[j], b0, b1, b2, at, Ap, j, kmask);
+                if (key <= lim) {
+                    r.why = 5;
+                    if (!(q[j] < kInf)) return r;  // off-grid member: exact path
+                    close |= 1u << j;
+                    mixed |= !(c[j].x == cb.x && c[j].y == cb.y && c[j].z == cb.z);
+                }
+            }
+            if (!mixed) {
+                jb = __ffs(close) - 1;
+            } else {
+                const float a3[3] = {ca.x, ca.y, ca.z};
+                const double dA = dist64(ip, a3);
+                double best = 0, bw = 0;
+                int bj = -1;
+                for (int j = 0; j < 9; ++j) {
+                    if (!(close >> j & 1u)) continue;
+                    const float cj[3] = {c[j].x, c[j].y, c[j].z};
+                    const double dj = dist64(ip, cj);
+                    const double w = dj / (dA + dj + eps);
+                    const double o = objective64(ip, a3, cj, w, eps);
+                    if (bj < 0 || o < best) {
+                        best = o;
+                        bw = w;
+                        bj = j;
+                    }
+                }
+                r.ok = true;
+                r.jb = bj;
+                r.w = float(bw);
+                r.why = 6;
+                return r;
+            }
+        }
+    }
+    float4 cb = c[0];
+#pragma unroll
+    for (int j = 1; j < 9; ++j)
+        if (j == jb) cb = c[j];
+    const float a3[3] = {ca.x, ca.y, ca.z}, b3[3] = {cb.x, cb.y, cb.z};
+    bool wok = false;
+    r.w = weight_fast_verified(ip, a3, b3, eps, &wok);
+    if (!wok) {
+        const double dA = dist64(ip, a3), dB = dist64(ip, b3);
+        r.w = float(dB / (dA + dB + eps));
+    }
+    r.ok = true;
+    r.jb = jb;
+    return r;
 }
 
 __device__ inline Filter32Result filter32x_pixel(const float4 (&c)[9], const float* ip, float epsf,

@@ -302,13 +302,14 @@ __device__ int run_trial(const TrialState& t, const TrialBuffers& b, TrialSmem<N
                                    __int_as_float(0x7f800000), 0.0f);
                 if (gx >= 0 && gy >= 0 && gx < t.lw && gy < t.lh) {
                     const float* s = t.low + 3 * (size_t(gy) * t.lw + gx);
-                    c[k] = make_float4(s[0], s[1], s[2], 0.0f);
+                    c[k] = make_float4(s[0], s[1], s[2], max_abs3(s[0], s[1], s[2]));
                 }
             }
             const Filter32Result fr =
                 t.mode == GLU_MODE_EXACT
                     ? filter32x_pixel(c, ip, float(t.eps), t.eps)
-                    : filter32_pixel(c, ip, float(t.eps), t.eps, t.mode == GLU_MODE_GNU);
+                    : t.mode == GLU_MODE_GNU ? filter32_pixel(c, ip, float(t.eps), t.eps, true)
+                                             : filter32k_pixel(c, ip, float(t.eps), t.eps);
             if (fr.ok) {
                 np.a = uint32_t(cy - 1 + fr.ja / 3) * uint32_t(t.lw) + uint32_t(cx - 1 + fr.ja % 3);
                 np.b = uint32_t(cy - 1 + fr.jb / 3) * uint32_t(t.lw) + uint32_t(cx - 1 + fr.jb % 3);
@@ -641,13 +642,13 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
     for (int k = tid; k < nv; k += NT) {
         const int y = g.vy0 + k / g.vw, x = g.vx0 + k % g.vw;
         const float* src = t.low + 3 * (size_t(y) * t.lw + x);
-        ss.win[k] = make_float4(src[0], src[1], src[2], 0.0f);
+        ss.win[k] = make_float4(src[0], src[1], src[2], max_abs3(src[0], src[1], src[2]));
     }
     for (uint32_t i = tid; i < n; i += NT) {
         const uint32_t p = comp[i];
         const float* src = t.high + 3 * size_t(p);
         const float e = t.errors[p];
-        ss.compC[i] = make_float4(src[0], src[1], src[2], 0.0f);
+        ss.compC[i] = make_float4(src[0], src[1], src[2], max_abs3(src[0], src[1], src[2]));
         const int cx = int((p % W) / s), cy = int((p / W) / s);
         const unsigned long long key =
             (static_cast<unsigned long long>(__float_as_uint(e)) << 32) | (0xffffffffu - i);
@@ -790,7 +791,8 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
             const Filter32Result fr =
                 t.mode == GLU_MODE_EXACT
                     ? filter32x_pixel(c, ip, float(t.eps), t.eps)
-                    : filter32_pixel(c, ip, float(t.eps), t.eps, t.mode == GLU_MODE_GNU);
+                    : t.mode == GLU_MODE_GNU ? filter32_pixel(c, ip, float(t.eps), t.eps, true)
+                                             : filter32k_pixel(c, ip, float(t.eps), t.eps);
 #ifdef GLU_SCHED_TRACE
             for (int k = 0; k < 9; ++k) c_dbg[k] = c[k];
             if (fr.ok && fr.why == 6) atomicAdd(&g_phase[16], 1ull);
