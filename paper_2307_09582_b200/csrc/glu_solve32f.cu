@@ -436,9 +436,33 @@ __global__ void __launch_bounds__(kThreads, GLU_F_MIN_BLOCKS)
     const int ncw = div_s(min(x0 + kTX - 1, a.W - 1), a) - ocx0 + 1;
     const int nch = div_s(min(y0 + tileH - 1, a.H - 1), a) - ocy0 + 1;
     const int cw = ncw + 2;
-    // the first pixel's guide colour is requested before the staging barrier
+#ifndef GLU_F_CPASYNC
+#define GLU_F_CPASYNC 1
+#endif
     const int x = x0 + (threadIdx.x % kTX), yb = y0 + (threadIdx.x / kTX);
     const bool xin = x < a.W;
+#if GLU_F_CPASYNC
+    // Each thread's guide colour for row k + 1 is copied global -> shared by
+    // cp.async (LDGSTS, no registers held) while it solves row k; row 0's is
+    // requested before the staging barrier.  Only the issuing thread reads
+    // its slot, so cp.async.wait_group alone orders the copy and the read.
+    __shared__ float gbuf[2][3 * kThreads];
+    auto fetch = [&](int k) {
+        const int y = yb + k * kTY;
+        if (xin && y < a.H) {
+            const float* g = a.high + 3 * (size_t(y) * a.W + x);
+            float* d = &gbuf[k & 1][3 * threadIdx.x];
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                                 static_cast<unsigned>(__cvta_generic_to_shared(d + c))),
+                             "l"(g + c));
+        }
+        asm volatile("cp.async.commit_group;");
+    };
+    fetch(0);
+#else
+    // the first pixel's guide colour is requested before the staging barrier
     float g0 = 0.0f, g1 = 0.0f, g2 = 0.0f;
     if (xin && yb < a.H) {
         const float* g = a.high + 3 * (size_t(yb) * a.W + x);
@@ -446,6 +470,7 @@ __global__ void __launch_bounds__(kThreads, GLU_F_MIN_BLOCKS)
         g1 = __ldg(g + 1);
         g2 = __ldg(g + 2);
     }
+#endif
     // packed cell (c - 1) of the LR grid is at padded index c
     for (int k = threadIdx.x; k < cw * (nch + 2); k += kThreads)
         wcells[k] = __ldg(packed + size_t(ocy0 + k / cw) * pw + (ocx0 + k % cw));
@@ -454,12 +479,23 @@ __global__ void __launch_bounds__(kThreads, GLU_F_MIN_BLOCKS)
 #pragma unroll 1
     for (int k = 0; k < rows; ++k) {
         const int y = yb + k * kTY;
+#if GLU_F_CPASYNC
+        if (k + 1 < rows) {
+            fetch(k + 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        const float* gb = &gbuf[k & 1][3 * threadIdx.x];
+        const float g0 = gb[0], g1 = gb[1], g2 = gb[2];
+#else
         if (k > 0 && xin && y < a.H) {
             const float* g = a.high + 3 * (size_t(y) * a.W + x);
             g0 = __ldg(g);
             g1 = __ldg(g + 1);
             g2 = __ldg(g + 2);
         }
+#endif
         if (xin && y < a.H) solve_pixel(a, packed, t, forceFallback, x, y, g0, g1, g2);
     }
 }
