@@ -154,10 +154,10 @@ __device__ inline Filter32Result filter32_pixel(const float4 (&c)[9], const floa
             return r;
         }
     }
-    const float a3[3] = {ca.x, ca.y, ca.z}, b3[3] = {cb.x, cb.y, cb.z};
     bool wok = false;
-    r.w = weight_fast_verified(ip, a3, b3, eps, &wok);
+    r.w = weight_fast_lean(ip0, ip1, ip2, ca, cb, eps, &wok);
     if (!wok) {
+        const float a3[3] = {ca.x, ca.y, ca.z}, b3[3] = {cb.x, cb.y, cb.z};
         const double dA = dist64(ip, a3), dB = dist64(ip, b3);
         r.w = float(dB / (dA + dB + eps));
     }
@@ -344,10 +344,10 @@ __device__ inline Filter32Result filter32k_pixel(const float4 (&c)[9], const flo
 #pragma unroll
     for (int j = 1; j < 9; ++j)
         if (j == jb) cb = c[j];
-    const float a3[3] = {ca.x, ca.y, ca.z}, b3[3] = {cb.x, cb.y, cb.z};
     bool wok = false;
-    r.w = weight_fast_verified(ip, a3, b3, eps, &wok);
+    r.w = weight_fast_lean(ip0, ip1, ip2, ca, cb, eps, &wok);
     if (!wok) {
+        const float a3[3] = {ca.x, ca.y, ca.z}, b3[3] = {cb.x, cb.y, cb.z};
         const double dA = dist64(ip, a3), dB = dist64(ip, b3);
         r.w = float(dB / (dA + dB + eps));
     }

@@ -131,6 +131,48 @@ __device__ __forceinline__ float weight_fast_verified(const float* ip, const flo
     *ok = E > -100 && fabs(g) + 0x1.0p-48 * wt < half;
     return f;
 }
+// (float) of the reference's weight d_b / (d_a + d_b + eps) (upsample.cpp:61)
+// from a double estimate good to ~2^-42 (relative): the squared distances
+// with DFMA, sqrt and the quotient from the MUFU double approximations (~2^-23)
+// with one Newton step each (~2^-45).  Its float rounding is the reference's
+// unless the estimate lies within 2^-36 of a float rounding midpoint (a 64x
+// margin on the error): then *ok = false and the caller takes the IEEE
+// evaluation (~2^-12 of pixels).  d_b = 0 gives exactly 0 on both sides.
+__device__ __forceinline__ float weight_fast_lean(float ip0, float ip1, float ip2, float4 ca,
+                                                  float4 cb, double eps, bool* ok) {
+    const double p0 = ip0, p1 = ip1, p2 = ip2;
+    const double a0 = p0 - double(ca.x), a1 = p1 - double(ca.y), a2 = p2 - double(ca.z);
+    const double b0 = p0 - double(cb.x), b1 = p1 - double(cb.y), b2 = p2 - double(cb.z);
+    const double sa = __fma_rn(a2, a2, __fma_rn(a1, a1, a0 * a0));
+    const double sb = __fma_rn(b2, b2, __fma_rn(b1, b1, b0 * b0));
+    if (sb == 0.0) {
+        *ok = true;
+        return 0.0f;
+    }
+    auto root = [](double x) {  // x > 0
+        double r;
+        asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+        const double y = x * r;
+        return __fma_rn(__fma_rn(-y, y, x), 0.5 * r, y);
+    };
+    const double da = sa > 0.0 ? root(sa) : 0.0;
+    const double db = root(sb);
+    const double den = (da + db) + eps;
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(den));
+    r = __fma_rn(r, __fma_rn(-den, r, 1.0), r);
+    const double wt = db * r;
+    const float f = __double2float_rn(wt);
+    const unsigned fb = __float_as_uint(f);
+    const int E = int((fb >> 23) & 0xffu) - 127;
+    const double g = wt - double(f);  // exact: same binade up to a factor 2
+    // distance from f to the rounding midpoint on g's side
+    const int he = (g < 0.0 && (fb & 0x7fffffu) == 0u) ? E - 25 : E - 24;
+    const double half = __longlong_as_double((long long)(he + 1023) << 52);
+    *ok = E > -100 && fabs(g) + 0x1.0p-36 * wt < half;
+    return f;
+}
+
 #endif
 
 // Candidate access: any type whose operator[](i) returns candidate i's colour
