@@ -495,7 +495,10 @@ cudaError_t launch_solve32f(glu_ctx* ctx, const SolveArgs& a, const float4* pack
         memo[3] = a.H;
         memo[4] = rows;
     }
-    const int rows = memo[4];
+#ifndef GLU_F_ROWS
+#define GLU_F_ROWS 0  // 0: picked per launch (A/B builds force a count)
+#endif
+    const int rows = GLU_F_ROWS > 0 ? GLU_F_ROWS : memo[4];
     const int mch = (kTY * rows - 1) / a.s + 2;
     const size_t smem = sizeof(float4) * size_t(mcw + 2) * (mch + 2);  // <= 19 x 35 cells (s = 2)
     dim3 grid(unsigned(tilesX), (a.H + kTY * rows - 1) / (kTY * rows));
