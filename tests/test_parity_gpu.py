@@ -152,6 +152,9 @@ CASES = [  # (W, H, s, S, seed): ragged sizes, every supported window class
     # the exact kernel's tile shapes: s = 3 (one row per thread, 12 x 4 owner
     # cells per tile) and a larger s = 5 / s = 7 frame (several rows per thread)
     (301, 211, 3, 3, 25), (1203, 1001, 5, 3, 26), (1500, 700, 7, 3, 27),
+    # k_solve32f's tile shapes at the extremes: s = 32 (5 x 3 LR grid), a 40 x 3
+    # image at s = 2 (one tile row, 2-row LR grid)
+    (129, 77, 32, 3, 28), (40, 3, 2, 3, 29),
 ]
 
 
