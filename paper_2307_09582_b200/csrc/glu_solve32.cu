@@ -348,14 +348,14 @@ SolveArgs prepared(const SolveArgs& a0) {
 cudaError_t dispatch(glu_ctx* ctx, const SolveArgs& a, const float4* packed, int forceFallback,
                      const unsigned* nanFlag) {
     if (a.mode == GLU_MODE_EXACT) return launch_solve32x(ctx, a, packed, forceFallback, nanFlag);
-    if (a.mode == GLU_MODE_GNU)
-        return a.S == 3 ? launch_t<3, GLU_MODE_GNU>(ctx, a, packed, forceFallback, nanFlag)
-                        : launch_t<5, GLU_MODE_GNU>(ctx, a, packed, forceFallback, nanFlag);
 #ifndef GLU_SOLVE_F
 #define GLU_SOLVE_F 1
 #endif
-    if (GLU_SOLVE_F && solve32f_supported(a.mode, a.S))
+    if (GLU_SOLVE_F && solve32f_supported(a.mode, a.S))  // Fast / GNU, S = 3
         return launch_solve32f(ctx, a, packed, forceFallback, nanFlag);
+    if (a.mode == GLU_MODE_GNU)
+        return a.S == 3 ? launch_t<3, GLU_MODE_GNU>(ctx, a, packed, forceFallback, nanFlag)
+                        : launch_t<5, GLU_MODE_GNU>(ctx, a, packed, forceFallback, nanFlag);
     return a.S == 3 ? launch_t<3, GLU_MODE_FAST>(ctx, a, packed, forceFallback, nanFlag)
                     : launch_t<5, GLU_MODE_FAST>(ctx, a, packed, forceFallback, nanFlag);
 }

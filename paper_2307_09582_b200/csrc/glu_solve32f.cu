@@ -127,6 +127,7 @@ struct PackedWindow {
 // The reference's double-precision pixelFast (upsample.cpp:49-71) for one
 // pixel: NaN inputs, underflow-sized distances, uncertain stage-A picks,
 // off-grid close members, forced fallback.  Returns {a, b, bits(w)}.
+template <int MODE>
 __device__ __noinline__ uint3 solve_double_fast(const float4* packed, int lw, int lh, double eps,
                                                 unsigned long long* counters, int cx, int cy,
                                                 float ip0, float ip1, float ip2) {
@@ -136,7 +137,8 @@ __device__ __noinline__ uint3 solve_double_fast(const float4* packed, int lw, in
     const int nwy = min(lh - 1, cy + 1) - wy0 + 1;
     const float ip[3] = {ip0, ip1, ip2};
     PackedWindow pwin{packed + size_t(wy0 + 1) * pw + (wx0 + 1), pw, nwx};
-    const Pick pk = pick_fast64(ip, pwin, nwx * nwy, eps);
+    const Pick pk = MODE == GLU_MODE_GNU ? pick_gnu64(ip, pwin, nwx * nwy)
+                                         : pick_fast64(ip, pwin, nwx * nwy, eps);
     const int ar = pk.ai / nwx, br = pk.bi / nwx;
     if (counters) atomicAdd(counters, 1ull);
     return make_uint3(uint32_t(wy0 + ar) * uint32_t(lw) + uint32_t(wx0 + pk.ai - ar * nwx),
@@ -223,6 +225,9 @@ struct FTile {
     int cw, ocx0, ocy0;
 };
 
+// MODE: GLU_MODE_FAST, or GLU_MODE_GNU (stage A only: b = a, w = 1;
+// upsample.cpp:93-104).
+template <int MODE>
 __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* packed, const FTile& t,
                                             int forceFallback, int x, int y, float ip0, float ip1,
                                             float ip2) {
@@ -279,7 +284,8 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
     int jb = ja;
     float w = 0.0f;
     bool wExact = false;  // w settled in double (close-set path)
-    if (ok && !exactA) {  // exact match I_a == I_p: b = a (the first exact zero), w = 0
+    if (MODE == GLU_MODE_FAST && ok && !exactA) {
+        // (exact match I_a == I_p: b = a, the first exact zero, and w = 0)
         // ---- stage B: b = first argmin of the objective at w_j ---------------
         const float eps = a.epsf;
         const float da = fast_sqrt(m1);
@@ -328,7 +334,9 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
         const int ra = (ja * 11) >> 5, rb = (jb * 11) >> 5;
         ia = uint32_t(cy - 1 + ra) * uint32_t(a.lw) + uint32_t(cx - 1 + ja - 3 * ra);
         ib = uint32_t(cy - 1 + rb) * uint32_t(a.lw) + uint32_t(cx - 1 + jb - 3 * rb);
-        if (!wExact) {
+        if (MODE == GLU_MODE_GNU) {
+            w = 1.0f;
+        } else if (!wExact) {
             const float4 cb = swin[woff(jb, cw)];
             bool wok = false;
 #ifndef GLU_F_LEAN_W
@@ -345,7 +353,7 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
         }
     } else {
         const uint3 r =
-            solve_double_fast(packed, a.lw, a.lh, a.eps, a.fallbacks, cx, cy, ip0, ip1, ip2);
+            solve_double_fast<MODE>(packed, a.lw, a.lh, a.eps, a.fallbacks, cx, cy, ip0, ip1, ip2);
         ia = r.x;
         ib = r.y;
         w = __uint_as_float(r.z);
@@ -382,6 +390,7 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
 #define GLU_F_MIN_BLOCKS 4  // 64 registers: 32 warps per SM
 #endif
 
+template <int MODE>
 __global__ void __launch_bounds__(kThreads, GLU_F_MIN_BLOCKS)
     k_solve32f(SolveArgs a, const float4* packed, int forceFallback, const unsigned* nanFlag,
                int rows) {
@@ -454,16 +463,21 @@ __global__ void __launch_bounds__(kThreads, GLU_F_MIN_BLOCKS)
             g2 = __ldg(g + 2);
         }
 #endif
-        if (xin && y < a.H) solve_pixel(a, packed, t, forceFallback, x, y, g0, g1, g2);
+        if (xin && y < a.H) solve_pixel<MODE>(a, packed, t, forceFallback, x, y, g0, g1, g2);
     }
 }
 
 }  // namespace
 
-bool solve32f_supported(int mode, int S) { return mode == GLU_MODE_FAST && S == 3; }
+bool solve32f_supported(int mode, int S) {
+    return (mode == GLU_MODE_FAST || mode == GLU_MODE_GNU) && S == 3;
+}
 
-cudaError_t launch_solve32f(glu_ctx* ctx, const SolveArgs& a, const float4* packed,
-                            int forceFallback, const unsigned* nanFlag) {
+namespace {
+
+template <int MODE>
+cudaError_t launch_f(glu_ctx* ctx, const SolveArgs& a, const float4* packed, int forceFallback,
+                     const unsigned* nanFlag) {
     // Rows per thread: as k_solve32x -- the count minimising waves x (rows +
     // staging cost).  Cells a tile touches: ncw <= (kTX - 1) / s + 2, nch <=
     // (tileH - 1) / s + 2, plus the +-1 border.
@@ -480,7 +494,7 @@ cudaError_t launch_solve32f(glu_ctx* ctx, const SolveArgs& a, const float4* pack
             const int mch = (kTY * r - 1) / a.s + 2;
             const size_t sm = sizeof(float4) * size_t(mcw + 2) * (mch + 2);
             int per = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_solve32f, kThreads, sm);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_solve32f<MODE>, kThreads, sm);
             const long slots = long(max(per, 1)) * nsm;
             const long tiles = tilesX * ((a.H + kTY * r - 1) / (kTY * r));
             const float cost = float((tiles + slots - 1) / slots) * (float(r) + kStageCost);
@@ -502,9 +516,17 @@ cudaError_t launch_solve32f(glu_ctx* ctx, const SolveArgs& a, const float4* pack
     const int mch = (kTY * rows - 1) / a.s + 2;
     const size_t smem = sizeof(float4) * size_t(mcw + 2) * (mch + 2);  // <= 19 x 35 cells (s = 2)
     dim3 grid(unsigned(tilesX), (a.H + kTY * rows - 1) / (kTY * rows));
-    k_solve32f<<<grid, kThreads, smem, ctx->stream>>>(a, packed, forceFallback, nanFlag, rows);
+    k_solve32f<MODE><<<grid, kThreads, smem, ctx->stream>>>(a, packed, forceFallback, nanFlag, rows);
     ++ctx->launches;
     return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_solve32f(glu_ctx* ctx, const SolveArgs& a, const float4* packed,
+                            int forceFallback, const unsigned* nanFlag) {
+    return a.mode == GLU_MODE_GNU ? launch_f<GLU_MODE_GNU>(ctx, a, packed, forceFallback, nanFlag)
+                                  : launch_f<GLU_MODE_FAST>(ctx, a, packed, forceFallback, nanFlag);
 }
 
 }  // namespace glu_cu
