@@ -27,7 +27,10 @@ namespace glu_cu {
 
 namespace {
 
-constexpr int kTX = 32, kTY = 8, kThreads = kTX * kTY;
+#ifndef GLU_X_TY
+#define GLU_X_TY 4  // warps per CTA (8: 0.7 % slower)
+#endif
+constexpr int kTX = 32, kTY = GLU_X_TY, kThreads = kTX * kTY;
 constexpr int kPairs = 36;       // i < j over 9 candidates
 constexpr int kCellStride = 37;  // float4 per owner cell (592 B: bank-spread)
 constexpr int kMaxRows = 8;               // pixels per thread (rows y, y + kTY, ...): 1..8
@@ -100,7 +103,7 @@ struct PackedWindow {
 };
 
 #ifndef GLU_X_MIN_BLOCKS
-#define GLU_X_MIN_BLOCKS 4  // 64 registers: 32 warps per SM
+#define GLU_X_MIN_BLOCKS 8  // 64 registers: 32 warps per SM (8 CTAs of 4 warps)
 #endif
 
 // Offset of window candidate j (row j / 3, column j % 3) in a staged window
@@ -420,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS)
                    (pr >= 35);
     const int tj = pr - (ti * 8 - ti * (ti - 1) / 2) + ti + 1;
     const int oi = (ti / 3) * cw + ti % 3, oj = (tj / 3) * cw + tj % 3;
-    constexpr int kCellStep = kThreads / kPairs;  // 7 cells per pass; threads 252.. idle
+    constexpr int kCellStep = kThreads / kPairs;  // cells per pass (the last threads idle)
     for (int cell = int(threadIdx.x) / kPairs; cell < ncw * nch && threadIdx.x < kCellStep * kPairs;
          cell += kCellStep) {
         const int ly = cell / ncw, lx = cell - ly * ncw;
