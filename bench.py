@@ -354,6 +354,18 @@ def run_ours(args, ws, rank, local):
             "frac": xflops / (x_ms * 1e-3) / 1e12 / fp32_tflops,
             "value": nf * W_ * H_ / (nf * x_ms * 1e-3) / 1e6, "value_unit": "HR Mpix/s",
             "traffic": load_traffic().get("solve_apply_exact_c3")}
+        if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+            # the pair search's own output against the reference (one frame)
+            try:
+                import oracle
+                ref = oracle.Reference()
+                ref.set_num_threads(0)
+                want = reference_frame(ref, frames_np[0], "exact", os.cpu_count() or 1)
+                roofline["pair_search"]["parity"] = bool(
+                    want.tobytes() == xout[0].cpu().numpy().tobytes())
+                roofline["pair_search"]["parity_sample"] = "frame 0 vs oracle/_ref (exact mode)"
+            except Exception as e:  # reported, never silently replaced
+                roofline["pair_search"]["parity"] = f"error: {type(e).__name__}: {e}"
         xinstr = load_traffic().get("solve_apply_exact_c3_warp_instr")
         if xinstr:
             sms = torch.cuda.get_device_properties(local).multi_processor_count

@@ -283,6 +283,14 @@ bool trial_update_component(const ImageF32& high, ImageF32& low, ParamField& fie
     if (high.width != g.highW || high.height != g.highH || low.width != g.lowW ||
         low.height != g.lowH || errors.width != g.highW || errors.height != g.highH)
         throw std::invalid_argument("trial_update_component: shape mismatch");
+    // The reference reaches optimize_pixels (upsample.cpp:222-223) with a
+    // field of the wrong size and throws there; the host buffers below are
+    // copied by size, so check every container before any device work.
+    if (field.params.size() != high.pixelCount())
+        throw std::invalid_argument("optimize_pixels: field does not match image");
+    if (high.data.size() != 3 * high.pixelCount() || low.data.size() != 3 * low.pixelCount() ||
+        errors.e.size() != high.pixelCount())
+        throw std::invalid_argument("trial_update_component: shape mismatch");
     const glu_grid cg = cgrid(g);
     const glu_config cc = ccfg(cfg);
     int accepted = 0;

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdint>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -69,6 +70,15 @@ int check_grid(const glu_grid* g) {
 
 size_t npx_of(const glu_grid* g) { return size_t(g->highW) * g->highH; }
 size_t lown_of(const glu_grid* g) { return size_t(g->lowW) * g->lowH; }
+
+// Records and floats are read / written as 4-byte words (the vector apply
+// peels any head that is not 16-byte aligned, launch_apply).
+int check_apply_alignment(const void* field, const void* target, const void* out) {
+    if ((reinterpret_cast<uintptr_t>(field) | reinterpret_cast<uintptr_t>(target) |
+         reinterpret_cast<uintptr_t>(out)) % 4 != 0)
+        return einval("apply_field: buffers must be 4-byte aligned");
+    return GLU_OK;
+}
 
 int check_mode(int mode) {
     if (mode < 0 || mode > 2) return einval("unknown mode (expected fast|exact|gnu)");
@@ -193,7 +203,8 @@ int glu_ctx_create(int device, glu_ctx** out) {
         return fail_cuda(e, "stream");
     }
     c->stream = c->own;
-    e = cudaMalloc(&c->d_counters, 8 * sizeof(unsigned long long));
+    e = cudaEventCreateWithFlags(&c->switchEv, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_counters, 8 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMemset(c->d_counters, 0, 8 * sizeof(unsigned long long));
     if (e != cudaSuccess) {
         cudaStreamDestroy(c->own);
@@ -215,6 +226,7 @@ int glu_ctx_destroy(glu_ctx* ctx) {
     cudaFree(ctx->d_counters);
     for (cudaEvent_t ev : ctx->ev)
         if (ev) cudaEventDestroy(ev);
+    if (ctx->switchEv) cudaEventDestroy(ctx->switchEv);
     if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
     if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
     cudaStreamDestroy(ctx->own);
@@ -224,7 +236,15 @@ int glu_ctx_destroy(glu_ctx* ctx) {
 
 int glu_ctx_set_stream(glu_ctx* ctx, void* s) {
     if (!ctx) return einval("ctx must not be null");
-    ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own;
+    cudaStream_t next = s ? static_cast<cudaStream_t>(s) : ctx->own;
+    if (next != ctx->stream) {
+        // The scratch slots and counters are shared by every stream this
+        // context is bound to: order the new stream after everything already
+        // issued on the old one.
+        GLU_CUDA(cudaEventRecord(ctx->switchEv, ctx->stream), "stream switch");
+        GLU_CUDA(cudaStreamWaitEvent(next, ctx->switchEv, 0), "stream switch");
+        ctx->stream = next;
+    }
     return GLU_OK;
 }
 
@@ -343,6 +363,7 @@ int glu_cu_apply_field(glu_ctx* ctx, const glu_pixel_params* field, const glu_gr
     if (!ctx) return einval("ctx must not be null");
     GLU_TRY(check_grid(g));
     if (channels != 1 && channels != 3) return einval("apply_field: channels must be 1 or 3");
+    GLU_TRY(check_apply_alignment(field, lowTarget, out));
     GLU_CUDA(launch_apply(ctx, field, npx_of(g), lowTarget, lown_of(g), channels, clampOutput, out),
              "apply_field");
     return GLU_OK;
@@ -356,6 +377,7 @@ int glu_cu_apply_field_band(glu_ctx* ctx, const glu_pixel_params* bandField, siz
     if (channels != 1 && channels != 3) return einval("apply_field: channels must be 1 or 3");
     if (bandPixels > npx_of(g)) return einval("apply_field: band exceeds the grid");
     if (bandPixels == 0) return GLU_OK;
+    GLU_TRY(check_apply_alignment(bandField, lowTarget, out));
     GLU_CUDA(launch_apply(ctx, bandField, bandPixels, lowTarget, lown_of(g), channels,
                           clampOutput, out),
              "apply_field");

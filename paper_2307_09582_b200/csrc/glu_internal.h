@@ -29,6 +29,10 @@ struct glu_ctx {
     // Copy streams + events of the host frame pipeline (created lazily).
     cudaStream_t h2d = nullptr, d2h = nullptr;
     cudaEvent_t ev[8] = {};
+    // Recorded on the previous stream when glu_ctx_set_stream switches
+    // streams: the new stream waits on it, so work issued on different
+    // streams never overlaps on the shared scratch slots / counters.
+    cudaEvent_t switchEv = nullptr;
 };
 
 namespace glu_cu {

@@ -341,13 +341,15 @@ __device__ int run_trial(const TrialState& t, const TrialBuffers& b, TrialSmem<N
     }
     GLU_PHASE(4)
     const double e1 = BlockReduce(sm.tmp.reduce).Sum(part);
-    // Identical per-pixel errors give identical sequential sums: accept.
+    // Identical per-pixel errors give identical sequential sums: accept --
+    // unless the sum is NaN (a NaN error in the set), where the reference's
+    // `e1 <= e0` is false: the sequential re-check below then rejects.
     const bool anyChanged = __syncthreads_or(changed);
     if (tid == 0) {
         const double s0 = sm.e0;
         // |parallel - sequential| <= 2 * gamma_na * sum for non-negative terms.
         const double bound = 4.0 * (double(na) + 64.0) * 0x1.0p-53 * (s0 + e1);
-        if (!anyChanged || e1 + bound < s0)
+        if ((!anyChanged && s0 == s0) || e1 + bound < s0)
             sm.verdict = 1;
         else if (e1 > s0 + bound)
             sm.verdict = 0;
@@ -870,7 +872,7 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
             e1 += red[1][k];
         }
         const double bound = 4.0 * (double(na) + 64.0) * 0x1.0p-53 * (s0 + e1);
-        verdict = (!anyChangedCta || e1 + bound < s0) ? 1 : (e1 > s0 + bound ? 0 : -1);
+        verdict = ((!anyChangedCta && s0 == s0) || e1 + bound < s0) ? 1 : (e1 > s0 + bound ? 0 : -1);
     } else {
         if (tid == 0) {
             double s0 = 0, e1 = 0;
@@ -893,7 +895,7 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
                 anyChanged |= xred[r][2] != 0.0;
             }
             const double bound = 4.0 * (double(na) + 64.0) * 0x1.0p-53 * (s0 + e1);
-            if (!anyChanged || e1 + bound < s0)
+            if ((!anyChanged && s0 == s0) || e1 + bound < s0)
                 sm.verdict = 1;
             else if (e1 > s0 + bound)
                 sm.verdict = 0;
@@ -1228,7 +1230,8 @@ __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
     TrialState t, TrialBuffers big, char* ctaBufs, const uint32_t* off, const uint32_t* px,
     const uint32_t* ids, int ncomp, const int4* boxes, const int* sufTop, unsigned long long* pred,
     int* queue, int* qHead, int* qTail, int* finished, int reach, int spec, int* specState,
-    uint32_t* specSnap, int* specQ, int* specTail, const uint32_t* parkOff, uint32_t* parkBuf) {
+    uint32_t* specSnap, int* specQ, int* specTail, const uint32_t* parkOff, uint32_t* parkBuf,
+    uint32_t parkCap) {
     __shared__ TrialSmem<kSchedThreads> sm;
     __shared__ int sIdx, sMode, sUse;
     extern __shared__ __align__(16) char dyn[];
@@ -1284,7 +1287,7 @@ __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
                     for (int k = 0; k < kWin; ++k) {
                         const int j = cand[k];
                         if (got < 0 && j >= 0 && ld_relaxed(specState + j) == 7 &&
-                            parkOff[j + 1] > parkOff[j] && parkOff[j + 1] <= kParkWords &&
+                            parkOff[j + 1] > parkOff[j] && parkOff[j + 1] <= parkCap &&
                             atomicCAS(specState + j, 7, 1) == 7)
                             got = j;
                     }
@@ -1601,7 +1604,10 @@ void trace_end(glu_ctx* ctx, unsigned long long* trace, const int4* boxes, size_
 int run_sched(glu_ctx* ctx, const TrialState& t, const JointScratch& js, const glu_grid& g,
               const glu_config& cfg, const uint32_t* off, const uint32_t* px,
               const uint32_t* ids, size_t n, bool spec) {
-    const int grid = sched_grid(ctx, k_trial_sched);
+    // No more CTAs than trials (each CTA owns 1.44 MB of private buffers; a
+    // small problem needs neither the whole machine nor ~210 MB of them).
+    const int grid = std::min(sched_grid(ctx, k_trial_sched),
+                              int((std::max<size_t>(n, 1) + kCS - 1) / kCS) * kCS);
     const size_t per = size_t(kCtaCells) * 16 + size_t(kCtaPixels) * 20;
     char* ctaBufs = static_cast<char*>(scratch(ctx, S_SCHED, per * grid));
     // boxes (int4) | pred (u64: accepted << 32 | unfinished) | counters (16) | sufTop |
@@ -1634,6 +1640,7 @@ int run_sched(glu_ctx* ctx, const TrialState& t, const JointScratch& js, const g
     k_trial_seed<<<blocks_for(n, 256), 256, 0, st>>>(pred, int(n), queue, qTail);
     ctx->launches += 4;
     uint32_t* parkBuf = nullptr;
+    uint32_t parkCap = 0;
     if (spec) {
         size_t tb = 0;
         cub::DeviceScan::ExclusiveSum(nullptr, tb, parkOff, parkOff, int(n) + 1, st);
@@ -1649,9 +1656,15 @@ int run_sched(glu_ctx* ctx, const TrialState& t, const JointScratch& js, const g
         e = cub::DeviceScan::ExclusiveSum(temp + wBytes, tb, w, parkOff, int(n) + 1, st);
         if (e != cudaSuccess) return fail_cuda(e, "trial schedule");
         ctx->launches += 2;
-        // fixed arena, no host round trip: records past its end are simply
-        // not speculated (C4 needs ~280 MB, C2 ~60 MB)
-        parkBuf = static_cast<uint32_t*>(scratch(ctx, S_PARK, size_t(kParkWords) * 4));
+        // arena sized on the host without a round trip: n times the largest
+        // record an on-chip trial can park (k_park_words: 3 + 5 words per
+        // affected pixel of the h-dilated box, <= kSW cells and <= the image,
+        // + 4 per replaced cell, <= kSQ), capped at kParkWords; records past
+        // its end are simply not speculated (C4 needs ~280 MB, C2 ~60 MB)
+        const size_t maxRec = 3 + 5 * std::min(size_t(kSW) * g.scale * g.scale,
+                                               size_t(g.highW) * g.highH) + 4 * size_t(kSQ);
+        parkCap = uint32_t(std::min(size_t(kParkWords), n * maxRec));
+        parkBuf = static_cast<uint32_t*>(scratch(ctx, S_PARK, size_t(parkCap) * 4));
         if (!parkBuf) return GLU_ENOMEM;
     }
     TrialState ts = t;
@@ -1660,7 +1673,7 @@ int run_sched(glu_ctx* ctx, const TrialState& t, const JointScratch& js, const g
     void* args[] = {&ts,    &big,      &ctaBufs, &off,       &px,       &ids,
                     &nc,    &boxes,    &sufTop,  &pred,      &queue,    &qHead,
                     &qTail, &finished, &rch,     &sp,        &specState, &specSnap,
-                    &specQ, &specTail, &parkOff, &parkBuf};
+                    &specQ, &specTail, &parkOff, &parkBuf, &parkCap};
 #ifdef GLU_SCHED_TRACE
     unsigned long long* trace = trace_begin(ctx, n);
 #endif

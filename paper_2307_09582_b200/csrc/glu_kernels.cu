@@ -5,6 +5,8 @@
 // PixelParams, row-major.  All selection maths is bit-compatible with the
 // reference's double-precision expressions (glu_math.cuh).
 #include <cuda_runtime.h>
+#include <algorithm>
+#include <cstdint>
 
 #include "glu_internal.h"
 #include "glu_math.cuh"
@@ -188,6 +190,20 @@ __global__ void __launch_bounds__(256) k_apply(const glu_pixel_params* __restric
             apply_px<C>(f[0], f[1], __uint_as_float(f[2]), lowT, lowN, clamp != 0, out + C * p);
         }
     }
+}
+
+// One pixel per thread: the pixels before the first 16-byte aligned record
+// of a band slice (k_apply / k_apply3v read the field as uint4 and write
+// float4), or a whole slice whose field and output cannot both be aligned.
+template <int C>
+__global__ void __launch_bounds__(256) k_apply_scalar(const glu_pixel_params* __restrict__ field,
+                                                      size_t npx, const float* __restrict__ lowT,
+                                                      unsigned lowN, int clamp,
+                                                      float* __restrict__ out) {
+    const size_t p = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= npx) return;
+    const unsigned* f = reinterpret_cast<const unsigned*>(field + p);
+    apply_px<C>(f[0], f[1], __uint_as_float(f[2]), lowT, lowN, clamp != 0, out + C * p);
 }
 
 // RGB apply with the LR target repacked as float4 cells: one 16 B gather per
@@ -384,6 +400,30 @@ cudaError_t launch_solve_list(glu_ctx* ctx, const SolveArgs& a, const uint32_t* 
 
 cudaError_t launch_apply(glu_ctx* ctx, const glu_pixel_params* field, size_t npx,
                          const float* lowT, size_t lowN, int channels, int clamp, float* out) {
+    if (npx == 0) return cudaSuccess;
+    // The vector kernels need field + p and out + channels * p 16-byte aligned
+    // at p = 0 (mod 4).  A row-band slice of a field (glu_cu_apply_field_band)
+    // may start mid-quad: peel the head pixels up to the first aligned record
+    // (12 B records: field + head is aligned for exactly one head in 0..3),
+    // or run everything per pixel when the output cannot be aligned with it.
+    const uintptr_t fa = reinterpret_cast<uintptr_t>(field);
+    size_t head = 0;
+    while (head < 4 && (fa + 12 * head) % 16 != 0) ++head;
+    const bool aligned = head < 4 && (reinterpret_cast<uintptr_t>(out + channels * head) % 16) == 0;
+    if (!aligned || head > 0) {
+        const size_t n = aligned ? std::min(head, npx) : npx;
+        if (channels == 1)
+            k_apply_scalar<1><<<blocks_for(n, 256), 256, 0, ctx->stream>>>(field, n, lowT,
+                                                                          unsigned(lowN), clamp, out);
+        else
+            k_apply_scalar<3><<<blocks_for(n, 256), 256, 0, ctx->stream>>>(field, n, lowT,
+                                                                          unsigned(lowN), clamp, out);
+        ++ctx->launches;
+        if (!aligned || n == npx) return cudaGetLastError();
+        field += n;
+        out += channels * n;
+        npx -= n;
+    }
     const unsigned blocks = blocks_for((npx + 3) / 4, 256);
 #ifndef GLU_APPLY_V4
 #define GLU_APPLY_V4 1

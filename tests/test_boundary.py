@@ -123,3 +123,22 @@ def test_product_never_imports_the_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "glu_oracle" not in txt and "libglu_ref" not in txt, f
+
+
+def test_cpp_dropin_validation_without_gpu(tmp_path):
+    """Host-side validation of the drop-in C++ API (tests/cpp/
+    dropin_validation_test.cpp): the reference's std::invalid_argument texts,
+    thrown before any device work -- including a field of the wrong size in
+    trial_update_component, which must not reach the size-based host copy."""
+    import subprocess
+    from paper_2307_09582_b200 import build
+    if not os.path.exists(build.CPP_SO):
+        build.build()
+    lib = os.path.dirname(build.CPP_SO)
+    exe = tmp_path / "dropin_validation_test"
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I" + os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "dropin_validation_test.cpp"),
+                    "-L" + lib, "-lglu", "-lglu_cuda", "-Wl,-rpath," + lib, "-o", str(exe)],
+                   check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr

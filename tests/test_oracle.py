@@ -212,3 +212,26 @@ def test_oracle_vs_reference_nonfinite(oracle, reference, S):
             want = reference.optimize_field(img, low, s, S, EPS_DEFAULT, m)
             got = oracle.optimize_field(img, low, s, S, EPS_DEFAULT, m)
             assert same(got, want), (s, m)
+
+
+def nan_joint_scene():
+    """tests/test_robustness_gpu.py's joint input: NaN channels on 40 guide
+    pixels, so many trials see a NaN error in their affected set."""
+    from paper_2307_09582_b200 import workloads
+    img = workloads.scene(256, 192, 91)
+    rng = np.random.default_rng(3)
+    ys, xs = rng.integers(0, 192, 40), rng.integers(0, 256, 40)
+    img[ys, xs, rng.integers(0, 3, 40)] = np.nan
+    return img
+
+
+@pytest.mark.parametrize("mode", ["fast", "exact", "gnu"])
+def test_oracle_vs_reference_joint_nan_guide(oracle, reference, mode):
+    # NaN <= NaN is false in jointopt.cpp:167: such trials are rejected
+    img = nan_joint_scene()
+    a = oracle.joint_optimize(img, 8, mode=mode)
+    b = reference.joint_optimize(img, 8, mode=mode)
+    assert (a["iterations"], a["accepted"], a["rejected"]) == \
+        (b["iterations"], b["accepted"], b["rejected"])
+    for k in ("low", "field", "errors"):
+        assert same(a[k], b[k]), k
