@@ -259,9 +259,42 @@ GLU_HD Pick pick64(int mode, const float* ip, Cands c, int n, double eps) {
     return pick_fast64(ip, c, n, eps);
 }
 
+// NaN results with the reference host's bits.  x86-64 SSE returns the first
+// NaN operand of an operation (quieted), or the default NaN (sign set,
+// 0xffc00000 as a float) when an invalid operation has no NaN operand; the GPU
+// returns a canonical 0x7fffffff instead.  The reference's compiled loops
+// evaluate reconstruct_pixel as (la * w) + (lb * (1 - w)) and pixel_error as
+// s + (t - r)^2, channel by channel (objdump of apply_field / error_map in
+// the reference build), so the first NaN in that order is the result.  Only
+// reached when the result is NaN.
+#ifdef __CUDA_ARCH__
+__device__ __forceinline__ float quiet_nan_of(float x) {
+    return __uint_as_float(__float_as_uint(x) | 0x00400000u);
+}
+__device__ __noinline__ float host_nan_lerp(float w, float la, float lb) {
+    if (la != la) return quiet_nan_of(la);
+    if (w != w) return quiet_nan_of(w);
+    if (lb != lb) return quiet_nan_of(lb);
+    return __uint_as_float(0xffc00000u);  // 0 * inf or inf - inf
+}
+__device__ __noinline__ float host_nan_error(const float* t, const float* r) {
+    for (int c = 0; c < 3; ++c) {
+        if (t[c] != t[c]) return quiet_nan_of(t[c]);
+        if (r[c] != r[c]) return quiet_nan_of(r[c]);
+        if (t[c] == r[c] && (t[c] - t[c]) != 0.0f) return __uint_as_float(0xffc00000u);  // inf - inf
+    }
+    return __uint_as_float(0xffc00000u);
+}
+#endif
+
 // reconstruct_pixel, one channel (upsample.hpp:54-65): float maths, no FMA.
 GLU_HD float lerp_clamp(float w, float la, float lb, bool clampOutput) {
     float v = w * la + (1.0f - w) * lb;
+#ifdef __CUDA_ARCH__
+    // a NaN passes the reference's clamp unchanged; returned before it, since
+    // nvcc lowers the clamp to a NaN-canonicalising FMNMX
+    if (v != v) return host_nan_lerp(w, la, lb);
+#endif
     if (clampOutput) v = v < 0.0f ? 0.0f : (v > 1.0f ? 1.0f : v);
     return v;
 }
@@ -273,7 +306,11 @@ GLU_HD float pixel_error(const float* t, const float* r) {
         const double d = double(t[c]) - double(r[c]);
         s += d * d;
     }
-    return float(dsqrt(s));
+    float e = float(dsqrt(s));
+#ifdef __CUDA_ARCH__
+    if (e != e) e = host_nan_error(t, r);
+#endif
+    return e;
 }
 
 }  // namespace glu_cu

@@ -88,3 +88,25 @@ def test_one_context_many_streams(glu):
     torch.cuda.synchronize()
     for k, (p, e) in enumerate(got):
         assert torch.equal(p, want[k % 4][0]) and torch.equal(e, want[k % 4][1]), k
+
+
+@pytest.mark.parametrize("clamp", [True, False])
+def test_nonfinite_apply_and_error_map_bits_match_reference(glu, reference, clamp):
+    """NaN / inf guide pixels reach the LR image, the reconstruction and the
+    error map: NaN results must carry the reference host's bits (first NaN
+    operand quieted, or the x86 default NaN), not the GPU's canonical NaN."""
+    from test_oracle import nonfinite_scene
+    img = nonfinite_scene()
+    for s in (4, 8):
+        high = torch.from_numpy(img).cuda()
+        low, grid = glu.grid_downsample(high, s)
+        field = glu.optimize_field(high, low, grid)
+        P = _host_params(field.params)
+        want = reference.apply_field(P, s, low.cpu().numpy(), clamp)
+        got = glu.apply_field(field, low, clampOutput=clamp)
+        assert got.cpu().numpy().tobytes() == want.tobytes(), (s, clamp)
+        e_want = reference.error_map(img, want)
+        assert glu.error_map(high, got).cpu().numpy().tobytes() == e_want.tobytes(), s
+        if clamp:
+            se = glu.self_error_map(high, field, low).cpu().numpy()
+            assert se.tobytes() == e_want.tobytes(), s
