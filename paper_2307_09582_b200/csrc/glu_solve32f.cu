@@ -33,7 +33,11 @@
 // |channel|) in shared memory once and solves 1-8 rows of pixels per thread;
 // the rare paths (close calls, the double path) are out of line with scalar
 // arguments, so the scans stay in registers.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
 
 #include "glu_internal.h"
 #include "glu_math.cuh"
@@ -222,36 +226,51 @@ __device__ __noinline__ float weight_fast_ieee(float ip0, float ip1, float ip2, 
     return float(dB / (dA + dB + eps));
 }
 
-// The tile's staged candidate cells (shared memory).
+// ---- the kernel ---------------------------------------------------------------
+//
+// A CTA solves a tile of kTX = 32 columns x tileH = kTY * rows rows; warp ty
+// owns the tile's rows [ty * rows, (ty + 1) * rows), one pixel per thread per
+// row.  Before the rows are solved the CTA stages in shared memory:
+//   * the tile's guide pixels (tileH x 96 floats), loaded by one TMA
+//     (cp.async.bulk.tensor.2d, completion on an mbarrier) when the image rows
+//     are 16-byte aligned, else by the threads;
+//   * the candidate cells of the tile's owner cells +- 1 (the packed LR image)
+//     at a pitch of P cells (a compile-time constant for the common scales, so
+//     every candidate's offset is an immediate), with .w replaced by what the
+//     epilogue needs from a winning cell: its LR index (params) or the
+//     1-channel target value (the video path's fused apply);
+//   * the tile's largest |channel| (k_pack_low's .w) for the rounding floor F.
+
+enum Out { kOutParams = 0, kOutApply1 = 1, kOutGeneric = 2 };
+
 struct FTile {
-    const float4* wcells;  // owner cells of the tile +- 1, cw per row
+    const float4* wcells;  // staged cells, pitch P (or cw when P = 0)
     int cw, ocx0, ocy0;
 };
 
+template <int P>
+__device__ __forceinline__ int pitch_of(const FTile& t) { return P > 0 ? P : t.cw; }
+
 // MODE: GLU_MODE_FAST, or GLU_MODE_GNU (stage A only: b = a, w = 1;
-// upsample.cpp:93-104).
-template <int MODE>
+// upsample.cpp:93-104).  `swin` = the owner cell's window (top-left candidate),
+// `wM` = the tile's largest |channel|.
+template <int MODE, int OUT, int P>
 __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* packed, const FTile& t,
-                                            int forceFallback, int x, int y, float ip0, float ip1,
+                                            const float4* swin, float wM, int forceFallback,
+                                            size_t p, int cx, int cy, float ip0, float ip1,
                                             float ip2) {
-    const int cw = t.cw;
-    const size_t p = size_t(y) * a.W + x;
-    const int cx = div_s(x, a), cy = div_s(y, a);
-    const float4* swin = t.wcells + (cy - t.ocy0) * cw + (cx - t.ocx0);
+    const int cw = pitch_of<P>(t);
 
     // ---- stage A: a = first argmin |I_j - I_p| (compared as squares) -------
     // Each candidate's q_j as a key with its index in the low 4 mantissa bits
     // (<= 15 ulp = 30u): K1a (smallest) gives a = the first argmin of the fp32
     // distances up to keys within 30u of each other, and K2a (second
     // smallest) screens for the near ties that need the exact check below.
-    // (q_j is recomputed where it is needed again, by the same instruction
-    // sequence: kept live across the stages it spills.)
     const unsigned kmask = 0xfffffff0u | (unsigned(a.W) >> 31);  // opaque: a register
-    float K1a = kInf, K2a = kInf, pa = 0.0f, mw = 0.0f;
+    float K1a = kInf, K2a = kInf, pa = 0.0f;
 #pragma unroll
     for (int j = 0; j < 9; ++j) {
         const float4 v = swin[woff(j, cw)];
-        mw = fmaxf(mw, v.w);
         const float d0 = v.x - ip0, d1 = v.y - ip1, d2 = v.z - ip2;
         const float qq = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmul_rn(d0, d0)));
         unsigned kb;
@@ -285,6 +304,7 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
         }
     }
     int jb = ja;
+    float4 cb = ca;
     float w = 0.0f;
     bool wExact = false;  // w settled in double (close-set path)
     if (MODE == GLU_MODE_FAST && ok && !exactA) {
@@ -314,11 +334,11 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
         }
         jb = int(__float_as_uint(K1) & 15u);
         // the winner's upper bound: K1 + 2 G q_b / s_b^2 + F
-        const float4 cb = swin[woff(jb, cw)];
+        cb = swin[woff(jb, cw)];
         const float qb = __fmaf_rn(cb.z - ip2, cb.z - ip2,
                                    __fmaf_rn(cb.y - ip1, cb.y - ip1, __fmul_rn(cb.x - ip0, cb.x - ip0)));
         const float sb = __fadd_rn(at, fast_sqrt(qb));
-        const float m = fmaxf(mw, fmaxf(fabsf(ip0), fmaxf(fabsf(ip1), fabsf(ip2))));
+        const float m = fmaxf(wM, fmaxf(fabsf(ip0), fmaxf(fabsf(ip1), fabsf(ip2))));
         const float F = kF * __fmaf_rn(m, m, eps);
         const float lim = K1 + __fmaf_rn(2.0f * G * qb, rcp_approx(__fmul_rn(sb, sb)), F);
         if (!(K1 < kInf)) {
@@ -330,62 +350,63 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
             jb = c.jb;
             wExact = c.wExact;
             w = c.w;
+            cb = swin[woff(jb, cw)];
         }
     }
-    uint32_t ia, ib;
+    // the staged .w of the winning cells: LR indices, or the 1-channel target
+    float wa = ca.w, wb = cb.w;
     if (ok) {
-        const int ra = (ja * 11) >> 5, rb = (jb * 11) >> 5;
-        ia = uint32_t(cy - 1 + ra) * uint32_t(a.lw) + uint32_t(cx - 1 + ja - 3 * ra);
-        ib = uint32_t(cy - 1 + rb) * uint32_t(a.lw) + uint32_t(cx - 1 + jb - 3 * rb);
         if (MODE == GLU_MODE_GNU) {
             w = 1.0f;
         } else if (!wExact) {
-            const float4 cb = swin[woff(jb, cw)];
             bool wok = false;
-#ifndef GLU_F_LEAN_W
-#define GLU_F_LEAN_W 1
-#endif
-#if GLU_F_LEAN_W
             w = weight_fast_lean(ip0, ip1, ip2, ca, cb, a.eps, &wok);
-#else
-            const float ip[3] = {ip0, ip1, ip2};
-            const float a3[3] = {ca.x, ca.y, ca.z}, b3[3] = {cb.x, cb.y, cb.z};
-            w = weight_fast_verified(ip, a3, b3, a.eps, &wok);
-#endif
             if (!wok) w = weight_fast_ieee(ip0, ip1, ip2, ca, cb, a.eps);
         }
     } else {
         const uint3 r =
             solve_double_fast<MODE>(packed, a.lw, a.lh, a.eps, a.fallbacks, cx, cy, ip0, ip1, ip2);
-        ia = r.x;
-        ib = r.y;
         w = __uint_as_float(r.z);
+        if (OUT == kOutApply1) {
+            wa = __ldg(a.lowT + r.x);
+            wb = __ldg(a.lowT + r.y);
+        } else {
+            wa = __uint_as_float(r.x);
+            wb = __uint_as_float(r.y);
+        }
     }
-    if (a.params) {
+    if (OUT == kOutApply1) {  // the video path: 1-channel matte, no params
+        a.out[p] = lerp_clamp(w, wa, wb, a.clamp != 0);
+        return;
+    }
+    const uint32_t ia = __float_as_uint(wa), ib = __float_as_uint(wb);
+    if (OUT == kOutParams || a.params) {
         unsigned* o = reinterpret_cast<unsigned*>(a.params + p);
         o[0] = ia;
         o[1] = ib;
         o[2] = __float_as_uint(w);
     }
-    if (a.lowT) {
-        const bool clamp = a.clamp != 0;
-        if (a.channels == 1) {  // the video path's matte target
-            a.out[p] = lerp_clamp(w, __ldg(a.lowT + ia), __ldg(a.lowT + ib), clamp);
-        } else {
+    if (OUT == kOutGeneric) {
+        if (a.lowT) {
+            const bool clamp = a.clamp != 0;
+            if (a.channels == 1) {
+                a.out[p] = lerp_clamp(w, __ldg(a.lowT + ia), __ldg(a.lowT + ib), clamp);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+                    a.out[3 * p + k] = lerp_clamp(w, __ldg(a.lowT + 3 * size_t(ia) + k),
+                                                  __ldg(a.lowT + 3 * size_t(ib) + k), clamp);
+            }
+        }
+        if (a.errOut) {  // pixel_error of the clamped self reconstruction (jointopt.cpp:190)
+            float r[3];
 #pragma unroll
             for (int k = 0; k < 3; ++k)
-                a.out[3 * p + k] = lerp_clamp(w, __ldg(a.lowT + 3 * size_t(ia) + k),
-                                              __ldg(a.lowT + 3 * size_t(ib) + k), clamp);
+                r[k] = lerp_clamp(w, __ldg(a.low + 3 * size_t(ia) + k),
+                                  __ldg(a.low + 3 * size_t(ib) + k), true);
+            const float ipx[3] = {ip0, ip1, ip2};
+            a.errOut[p] = pixel_error(ipx, r);
         }
-    }
-    if (a.errOut) {  // pixel_error of the clamped self reconstruction (jointopt.cpp:190)
-        float r[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k)
-            r[k] = lerp_clamp(w, __ldg(a.low + 3 * size_t(ia) + k), __ldg(a.low + 3 * size_t(ib) + k),
-                              true);
-        const float ipx[3] = {ip0, ip1, ip2};
-        a.errOut[p] = pixel_error(ipx, r);
     }
 }
 
@@ -393,80 +414,103 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
 #define GLU_F_MIN_BLOCKS 8  // 64 registers: 32 warps per SM (8 CTAs of 4 warps)
 #endif
 
-template <int MODE>
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+// Dynamic shared memory: [guide: tileH x 96 floats][cells: P x (nch + 2)].
+// `tmap` is a 2-D tensor map of the guide (3 W floats x H rows, box 96 x
+// tileH) when useTma != 0.
+template <int MODE, int OUT, int P>
 __global__ void __launch_bounds__(kThreads, GLU_F_MIN_BLOCKS)
-    k_solve32f(SolveArgs a, const float4* packed, int forceFallback, const unsigned* nanFlag,
-               int rows) {
-    extern __shared__ float4 wcells[];  // the tile's candidate cells (owner cells +- 1)
+    k_solve32f(const __grid_constant__ CUtensorMap tmap, SolveArgs a, const float4* packed,
+               int forceFallback, const unsigned* nanFlag, int rows, int useTma) {
+    extern __shared__ __align__(1024) float smem[];
+    __shared__ __align__(8) unsigned long long bar;
+    __shared__ float warpMax[kTY];
+    const int tileH = kTY * rows;
+    float* gtile = smem;                                                  // tileH x 96
+    float4* wcells = reinterpret_cast<float4*>(smem + size_t(tileH) * 96);
+    const int tx = threadIdx.x % kTX, ty = threadIdx.x / kTX;
+    const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * tileH;
+    if (useTma && threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)),
+                     "r"(unsigned(tileH * 96 * 4))
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(gtile)),
+            "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(3 * x0), "r"(y0), "r"(smem_u32(&bar))
+            : "memory");
+    }
     forceFallback |= int(__ldg(nanFlag));
     const int pw = a.lw + 2;  // h = 1
-    const int tileH = kTY * rows;
-    const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * tileH;
     const int ocx0 = div_s(x0, a), ocy0 = div_s(y0, a);
     const int ncw = div_s(min(x0 + kTX - 1, a.W - 1), a) - ocx0 + 1;
     const int nch = div_s(min(y0 + tileH - 1, a.H - 1), a) - ocy0 + 1;
-    const int cw = ncw + 2;
-#ifndef GLU_F_CPASYNC
-#define GLU_F_CPASYNC 1
-#endif
-    const int x = x0 + (threadIdx.x % kTX), yb = y0 + (threadIdx.x / kTX);
-    const bool xin = x < a.W;
-#if GLU_F_CPASYNC
-    // Each thread's guide colour for row k + 1 is copied global -> shared by
-    // cp.async (LDGSTS, no registers held) while it solves row k; row 0's is
-    // requested before the staging barrier.  Only the issuing thread reads
-    // its slot, so cp.async.wait_group alone orders the copy and the read.
-    __shared__ float gbuf[2][3 * kThreads];
-    auto fetch = [&](int k) {
-        const int y = yb + k * kTY;
-        if (xin && y < a.H) {
-            const float* g = a.high + 3 * (size_t(y) * a.W + x);
-            float* d = &gbuf[k & 1][3 * threadIdx.x];
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                                 static_cast<unsigned>(__cvta_generic_to_shared(d + c))),
-                             "l"(g + c));
-        }
-        asm volatile("cp.async.commit_group;");
-    };
-    fetch(0);
-#else
-    // the first pixel's guide colour is requested before the staging barrier
-    float g0 = 0.0f, g1 = 0.0f, g2 = 0.0f;
-    if (xin && yb < a.H) {
-        const float* g = a.high + 3 * (size_t(yb) * a.W + x);
-        g0 = __ldg(g);
-        g1 = __ldg(g + 1);
-        g2 = __ldg(g + 2);
-    }
-#endif
+    const int cw = P > 0 ? P : ncw + 2;
     // packed cell (c - 1) of the LR grid is at padded index c
-    for (int k = threadIdx.x; k < cw * (nch + 2); k += kThreads)
-        wcells[k] = __ldg(packed + size_t(ocy0 + k / cw) * pw + (ocx0 + k % cw));
+    float m = 0.0f;
+    for (int k = threadIdx.x; k < cw * (nch + 2); k += kThreads) {
+        const int r = k / cw, c = k - r * cw;
+        if (c < ncw + 2) {
+            float4 v = __ldg(packed + size_t(ocy0 + r) * pw + (ocx0 + c));
+            m = fmaxf(m, v.w);
+            const int lx = ocx0 + c - 1, ly = ocy0 + r - 1;
+            const bool in = lx >= 0 && ly >= 0 && lx < a.lw && ly < a.lh;
+            const unsigned li = in ? unsigned(ly) * unsigned(a.lw) + unsigned(lx) : 0u;
+            v.w = OUT == kOutApply1 ? (in ? __ldg(a.lowT + li) : 0.0f) : __uint_as_float(li);
+            wcells[k] = v;
+        }
+    }
+    if (!useTma) {  // the guide rows are not 16-byte aligned: staged by the threads
+        for (int k = threadIdx.x; k < tileH * 96; k += kThreads) {
+            const int r = k / 96, c = k - r * 96;
+            const int y = y0 + r;
+            gtile[k] = (y < a.H && x0 * 3 + c < a.W * 3)
+                           ? __ldg(a.high + 3 * (size_t(y) * a.W + x0) + c)
+                           : 0.0f;
+        }
+    }
+    // the tile's largest |channel| (a NaN .w counts as +inf: every pixel then
+    // settles its close calls in double)
+    m = m == m ? m : kInf;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (tx == 0) warpMax[ty] = m;
     __syncthreads();
+    float wM = warpMax[0];
+#pragma unroll
+    for (int k = 1; k < kTY; ++k) wM = fmaxf(wM, warpMax[k]);
+    if (useTma) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n"
+            "W:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+            "@!p bra W;\n}" ::"r"(smem_u32(&bar))
+            : "memory");
+    }
     const FTile t{wcells, cw, ocx0, ocy0};
+    const int x = x0 + tx;
+    if (x >= a.W) return;
+    const int cx = div_s(x, a);
+    const int r0 = ty * rows;
+    const float* g = gtile + r0 * 96 + 3 * tx;
+    size_t p = size_t(y0 + r0) * a.W + x;
+    int cy = -1;
+    const float4* swin = nullptr;
 #pragma unroll 1
-    for (int k = 0; k < rows; ++k) {
-        const int y = yb + k * kTY;
-#if GLU_F_CPASYNC
-        if (k + 1 < rows) {
-            fetch(k + 1);
-            asm volatile("cp.async.wait_group 1;" ::: "memory");
-        } else {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
+    for (int k = 0; k < rows; ++k, g += 96, p += a.W) {
+        const int y = y0 + r0 + k;
+        if (y >= a.H) break;
+        const int ncy = div_s(y, a);
+        if (ncy != cy) {
+            cy = ncy;
+            swin = wcells + (cy - ocy0) * cw + (cx - ocx0);
         }
-        const float* gb = &gbuf[k & 1][3 * threadIdx.x];
-        const float g0 = gb[0], g1 = gb[1], g2 = gb[2];
-#else
-        if (k > 0 && xin && y < a.H) {
-            const float* g = a.high + 3 * (size_t(y) * a.W + x);
-            g0 = __ldg(g);
-            g1 = __ldg(g + 1);
-            g2 = __ldg(g + 2);
-        }
-#endif
-        if (xin && y < a.H) solve_pixel<MODE>(a, packed, t, forceFallback, x, y, g0, g1, g2);
+        solve_pixel<MODE, OUT, P>(a, packed, t, swin, wM, forceFallback, p, cx, cy, g[0], g[1], g[2]);
     }
 }
 
@@ -478,26 +522,46 @@ bool solve32f_supported(int mode, int S) {
 
 namespace {
 
-template <int MODE>
-cudaError_t launch_f(glu_ctx* ctx, const SolveArgs& a, const float4* packed, int forceFallback,
-                     const unsigned* nanFlag) {
-    // Rows per thread: as k_solve32x -- the count minimising waves x (rows +
-    // staging cost).  Cells a tile touches: ncw <= (kTX - 1) / s + 2, nch <=
-    // (tileH - 1) / s + 2, plus the +-1 border.
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }();
+    return fn;
+}
+
+// Cells a tile touches: ncw <= (kTX - 1) / s + 2 (plus the +-1 border).
+int max_pitch(int s) { return (kTX - 1) / s + 4; }
+
+template <int MODE, int OUT, int P>
+cudaError_t launch_fp(glu_ctx* ctx, const SolveArgs& a, const float4* packed, int forceFallback,
+                      const unsigned* nanFlag) {
+    // Rows per thread: the count minimising waves x (rows + staging cost),
+    // as k_solve32x.
     int dev = 0;
     cudaGetDevice(&dev);
-    const int mcw = (kTX - 1) / a.s + 2;
+    const int pitch = P > 0 ? P : max_pitch(a.s);
     const long tilesX = (a.W + kTX - 1) / kTX;
-    thread_local int memo[5] = {-1, 0, 0, 0, 1};  // device, s, W, H -> rows
-    if (memo[0] != dev || memo[1] != a.s || memo[2] != a.W || memo[3] != a.H) {
+    auto smem_of = [&](int r) {
+        const int mch = (kTY * r - 1) / a.s + 2;
+        return sizeof(float) * size_t(kTY * r) * 96 + sizeof(float4) * size_t(pitch) * (mch + 2);
+    };
+    thread_local int memo[6] = {-1, 0, 0, 0, -1, 1};  // device, s, W, H, MODE/OUT/P -> rows
+    const int key = (MODE * 4 + OUT) * 64 + P;
+    if (memo[0] != dev || memo[1] != a.s || memo[2] != a.W || memo[3] != a.H || memo[4] != key) {
         int nsm = 148, rows = 1;
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         float best = -1.0f;
         for (int r = 1; r <= kMaxRows; ++r) {
-            const int mch = (kTY * r - 1) / a.s + 2;
-            const size_t sm = sizeof(float4) * size_t(mcw + 2) * (mch + 2);
             int per = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_solve32f<MODE>, kThreads, sm);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_solve32f<MODE, OUT, P>, kThreads,
+                                                          smem_of(r));
             const long slots = long(max(per, 1)) * nsm;
             const long tiles = tilesX * ((a.H + kTY * r - 1) / (kTY * r));
             const float cost = float((tiles + slots - 1) / slots) * (float(r) + kStageCost);
@@ -510,18 +574,64 @@ cudaError_t launch_f(glu_ctx* ctx, const SolveArgs& a, const float4* packed, int
         memo[1] = a.s;
         memo[2] = a.W;
         memo[3] = a.H;
-        memo[4] = rows;
+        memo[4] = key;
+        memo[5] = rows;
     }
 #ifndef GLU_F_ROWS
 #define GLU_F_ROWS 0  // 0: picked per launch (A/B builds force a count)
 #endif
-    const int rows = GLU_F_ROWS > 0 ? GLU_F_ROWS : memo[4];
-    const int mch = (kTY * rows - 1) / a.s + 2;
-    const size_t smem = sizeof(float4) * size_t(mcw + 2) * (mch + 2);  // <= 19 x 35 cells (s = 2)
-    dim3 grid(unsigned(tilesX), (a.H + kTY * rows - 1) / (kTY * rows));
-    k_solve32f<MODE><<<grid, kThreads, smem, ctx->stream>>>(a, packed, forceFallback, nanFlag, rows);
+    const int rows = GLU_F_ROWS > 0 ? GLU_F_ROWS : memo[5];
+    const int tileH = kTY * rows;
+    // TMA needs 16-byte aligned rows (3 W floats) and base; else the threads stage the guide.
+    CUtensorMap tmap{};
+    int useTma = 0;
+#ifndef GLU_F_TMA
+#define GLU_F_TMA 1
+#endif
+    if (GLU_F_TMA && a.W % 4 == 0 && (reinterpret_cast<uintptr_t>(a.high) & 15u) == 0) {
+        if (auto enc = tensor_map_encoder()) {
+            const cuuint64_t dims[2] = {cuuint64_t(3) * a.W, cuuint64_t(a.H)};
+            const cuuint64_t strides[1] = {cuuint64_t(12) * a.W};
+            const cuuint32_t box[2] = {96u, cuuint32_t(tileH)};
+            const cuuint32_t estr[2] = {1u, 1u};
+            useTma = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a.high), dims,
+                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+        }
+    }
+    const size_t smem = smem_of(rows);
+    if (smem > 48 * 1024) {
+        const cudaError_t e = cudaFuncSetAttribute(
+            k_solve32f<MODE, OUT, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+    }
+    dim3 grid(unsigned(tilesX), (a.H + tileH - 1) / tileH);
+    k_solve32f<MODE, OUT, P><<<grid, kThreads, smem, ctx->stream>>>(tmap, a, packed, forceFallback,
+                                                                    nanFlag, rows, useTma);
     ++ctx->launches;
     return cudaGetLastError();
+}
+
+template <int MODE, int OUT>
+cudaError_t launch_fo(glu_ctx* ctx, const SolveArgs& a, const float4* packed, int forceFallback,
+                      const unsigned* nanFlag) {
+    switch (max_pitch(a.s)) {  // s = 8 (C3, C2): 7; s = 16 (C4): 5; s >= 32: 4
+        case 4: return launch_fp<MODE, OUT, 4>(ctx, a, packed, forceFallback, nanFlag);
+        case 5: return launch_fp<MODE, OUT, 5>(ctx, a, packed, forceFallback, nanFlag);
+        case 7: return launch_fp<MODE, OUT, 7>(ctx, a, packed, forceFallback, nanFlag);
+        default: return launch_fp<MODE, OUT, 0>(ctx, a, packed, forceFallback, nanFlag);
+    }
+}
+
+template <int MODE>
+cudaError_t launch_f(glu_ctx* ctx, const SolveArgs& a, const float4* packed, int forceFallback,
+                     const unsigned* nanFlag) {
+    if (a.params && !a.lowT && !a.errOut)
+        return launch_fo<MODE, kOutParams>(ctx, a, packed, forceFallback, nanFlag);
+    if (!a.params && a.lowT && a.channels == 1 && !a.errOut)
+        return launch_fo<MODE, kOutApply1>(ctx, a, packed, forceFallback, nanFlag);
+    return launch_fo<MODE, kOutGeneric>(ctx, a, packed, forceFallback, nanFlag);
 }
 
 }  // namespace
