@@ -290,8 +290,8 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
     const float m1 = __fmaf_rn(ea2, ea2, __fmaf_rn(ea1, ea1, __fmul_rn(ea0, ea0)));  // q_a
     const bool exactA = ca.x == ip0 && ca.y == ip1 && ca.z == ip2;
     // NaN inputs and underflow-sized distances go to the exact path.
-    bool ok = !forceFallback && K1a < kInf && ip0 == ip0 && ip1 == ip1 && ip2 == ip2 &&
-              (m1 >= 1e-27f || exactA);
+    // (a NaN guide channel makes every q_j and key NaN: K1a stays +inf)
+    bool ok = !forceFallback && K1a < kInf && (m1 >= 1e-27f || exactA);
     // any other candidate within (1 + 32u) q_a has a key within K1a (1 + 128u)
     if (ok && K2a <= __fmaf_rn(K1a, 128.0f * kU, K1a) + 2e-36f) {
         const float lim = __fmaf_rn(m1, kCA * kU, m1) + 1e-36f;
@@ -496,19 +496,20 @@ __global__ void __launch_bounds__(kThreads, GLU_F_MIN_BLOCKS)
     const int x = x0 + tx;
     if (x >= a.W) return;
     const int cx = div_s(x, a);
-    const int r0 = ty * rows;
-    const float* g = gtile + r0 * 96 + 3 * tx;
-    size_t p = size_t(y0 + r0) * a.W + x;
-    int cy = -1;
-    const float4* swin = nullptr;
+    const int yr = y0 + ty * rows;
+    const int yEnd = min(yr + rows, a.H);
+    const float* g = gtile + (ty * rows) * 96 + 3 * tx;
+    size_t p = size_t(yr) * a.W + x;
+    // owner-cell row of the current row, advanced when y reaches yNext
+    int cy = div_s(yr, a);
+    int yNext = (cy + 1) * a.s;
+    const float4* swin = wcells + (cy - ocy0) * cw + (cx - ocx0);
 #pragma unroll 1
-    for (int k = 0; k < rows; ++k, g += 96, p += a.W) {
-        const int y = y0 + r0 + k;
-        if (y >= a.H) break;
-        const int ncy = div_s(y, a);
-        if (ncy != cy) {
-            cy = ncy;
-            swin = wcells + (cy - ocy0) * cw + (cx - ocx0);
+    for (int y = yr; y < yEnd; ++y, g += 96, p += a.W) {
+        if (y == yNext) {
+            ++cy;
+            yNext += a.s;
+            swin += cw;
         }
         solve_pixel<MODE, OUT, P>(a, packed, t, swin, wM, forceFallback, p, cx, cy, g[0], g[1], g[2]);
     }
