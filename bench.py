@@ -45,6 +45,8 @@ def parse():
     p.add_argument("--frames", type=int, default=FRAMES)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--c5-targets", type=int, default=64)
+    p.add_argument("--no-c5", action="store_true")
     return p.parse_args()
 
 
@@ -144,6 +146,36 @@ def load_traffic():
     return {}
 
 
+def capture_of(key: str, kernel_ms: float, probe_tflops: float, nominal_tflops: float) -> dict:
+    """What the committed ncu capture `key` (profiles/traffic.json) says about a
+    kernel: DRAM bytes, executed warp instructions and executed FP32 / FP64
+    flops per launch, with the live kernel time turned into executed TFLOP/s.
+    `stale` is true when the kernel's sources changed since the capture."""
+    import hashlib
+    t = load_traffic()
+    out = {"traffic": t.get(key), "warp_instr": t.get(key + "_warp_instr")}
+    src = t.get(key + "_src")
+    if src:
+        h = hashlib.sha256()
+        try:
+            for f in src["files"]:
+                with open(os.path.join(ROOT, f), "rb") as fh:
+                    h.update(fh.read())
+            out["stale"] = h.hexdigest()[:16] != src["sha256"]
+        except OSError:
+            out["stale"] = None
+    else:
+        out["stale"] = None  # no source hash recorded with this capture
+    f32 = t.get(key + "_fp32_flop_executed")
+    if f32:
+        tf = f32 / (kernel_ms * 1e-3) / 1e12
+        out["executed_fp32"] = {"flop_per_launch": f32, "tflops": tf,
+                                "frac_of_probe": tf / probe_tflops,
+                                "frac_of_nominal": tf / nominal_tflops,
+                                "fp64_flop_per_launch": t.get(key + "_fp64_flop_executed")}
+    return out
+
+
 # ---- CPU reference timing (oracle/_ref = the reference compiled from its sources) -
 
 def reference_frame(ref, frame: np.ndarray, mode: str, threads: int) -> np.ndarray:
@@ -178,6 +210,111 @@ def cpu_reference_sample(frames: np.ndarray, mode: str, budget_s: float, gpu_out
                       f"oracle/_ref: grid_downsample + optimize_pixels on {threads} row bands "
                       f"+ apply_field",
             "parity_vs_gpu": bool(parity) if gpu_out is not None else None}
+
+
+# ---- C5: upsample-only editing at 8K over HR row bands (configs[4]) -----------------
+
+C5_W, C5_H, C5_S, C5_SEED = 7680, 4320, 16, 4
+
+
+def run_c5(args, ws, rank, dist, hbm_gbs):
+    """BASELINE.json configs[4] beside the headline: the C4 joint field of the
+    8K scene (7680x4320, s = 16) applied to `args.c5_targets` RGB edits of its
+    LR image (channel_mix(M_k), seeds 1005 + k).  Each rank keeps its HR row
+    band of the field (strong scaling: total work fixed).  Two loops:
+      * black-box edits: rank 0 holds each edited target and broadcasts it (NCCL,
+        double-buffered against the previous target's apply), every rank applies
+        it to its band (glu_cu_apply_field_band);
+      * fused edits: the operator is the reference's SimOperator, so every rank
+        runs it on its copy of the LR image inside the packing step of the band
+        apply (glu_cu_apply_operator_field_band) -- nothing to broadcast.
+    Times are CUDA events on the apply stream, max over ranks."""
+    import torch
+    import paper_2307_09582_b200 as glu
+    from paper_2307_09582_b200 import banded, workloads
+    G = glu.glu
+    high = torch.from_numpy(workloads.scene(C5_W, C5_H, C5_SEED, 0)).cuda()
+    r = glu.joint_optimize(high, C5_S)
+    grid, low = r.field.grid, r.low
+    y0, y1 = banded.band_rows(grid, 3, ws, rank)
+    band = r.field.params[y0:y1].contiguous()
+    del high, r
+    torch.cuda.empty_cache()
+    nt = args.c5_targets
+    ops = [G.channel_mix_op(workloads.mix_op(1005 + k).M.reshape(9)) for k in range(nt)]
+    targets = [G.apply_operator(op, low) for op in ops] if rank == 0 else None
+    outs = [torch.empty((y1 - y0, C5_W, 3), dtype=torch.float32, device="cuda")
+            for _ in range(2)]
+    kk = {"k": 0}
+
+    def app(p, g, t, c):
+        o = outs[kk["k"] % 2]
+        kk["k"] += 1
+        return G.apply_field_band(p, g, t, c, out=o)
+
+    def loop_bcast():
+        if ws == 1:
+            for k in range(nt):
+                G.apply_field_band(band, grid, targets[k], out=outs[k % 2])
+        else:
+            banded.run_banded_apply(band, grid, targets, nt, 3, apply=app)
+
+    def loop_fused():
+        for k in range(nt):
+            G.apply_operator_field_band(band, grid, ops[k], low, out=outs[k % 2])
+
+    def timed(fn):
+        fn()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    ms_b = timed(loop_bcast)
+    ms_f = timed(loop_fused)
+    # one band apply launch pair (pack + apply) per target, timed alone
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(nt)]
+    for k in range(nt):
+        ev[k][0].record()
+        G.apply_operator_field_band(band, grid, ops[k], low, out=outs[k % 2])
+        ev[k][1].record()
+    torch.cuda.synchronize()
+    k_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+    band_px = (y1 - y0) * C5_W
+    nbytes = band_px * 24 + grid.lowW * grid.lowH * 12
+    parity = None
+    if rank == 0:
+        a = G.apply_operator_field_band(band, grid, ops[0], low)
+        b = G.apply_field_band(band, grid, targets[0])
+        parity = bool(torch.equal(a, b))
+    total_px = C5_W * C5_H * nt
+    return {
+        "workload": f"C5 (configs[4]): C4 joint field of the 7680x4320 s=16 scene, {nt} RGB "
+                    f"channel-mix edits of its 480x270 LR image, HR row bands over {ws} GPU(s)",
+        "metric": "HR Mpix/s (apply of every edit to the whole 8K frame)",
+        "value": total_px / (ms_b * 1e-3) / 1e6, "unit": "HR Mpix/s", "n_gpus": ws,
+        "scaling": "strong", "ms_per_pass": ms_b,
+        "broadcast_bytes_per_target": grid.lowW * grid.lowH * 12 if ws > 1 else 0,
+        "fused_operator": {"value": total_px / (ms_f * 1e-3) / 1e6, "ms_per_pass": ms_f,
+                           "api": "glu_cu_apply_operator_field_band (no broadcast)"},
+        "apply_kernel": {"kernel": "k_op_pack_target4 + k_apply3v", "ms_mean": k_ms,
+                         "algorithmic_bytes_per_launch": nbytes,
+                         "hbm_gbs": nbytes / (k_ms * 1e-3) / 1e9,
+                         "hbm_frac": nbytes / (k_ms * 1e-3) / 1e9 / hbm_gbs if hbm_gbs else None,
+                         "peak": "MEASURED_PEAKS.json hbm_gbs (of measured)"},
+        "parity_fused_vs_broadcast": parity,
+    }
 
 
 # ---- arms ---------------------------------------------------------------------------
@@ -306,10 +443,20 @@ def run_ours(args, ws, rank, local):
     flops, nbytes = algorithmic_work(W_, H_, SCALE, 3, args.mode, 1)
     k_ms = statistics.mean(kernel_ms)
     achieved = flops / (k_ms * 1e-3) / 1e12
-    traffic = load_traffic().get("solve_apply_fast_c3")
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    clocks = clk.summary()
+    max_mhz = clocks.get("sm_max_mhz") or 1965
+    nominal = 2 * 128 * sms * max_mhz * 1e6 / 1e12  # FFMA = 2 flops, 128 lanes / SM
+    key = {"fast": "solve_apply_fast_c3", "exact": "solve_apply_exact_c3",
+           "gnu": "solve_apply_gnu_c3"}[args.mode]
+    cap = capture_of(key, k_ms, fp32_tflops, nominal)
     roofline = {
         "bound": "fp32", "achieved": achieved, "peak": fp32_tflops, "unit": "TFLOP/s",
-        "frac": achieved / fp32_tflops, "traffic": traffic,
+        "frac": achieved / fp32_tflops, "traffic": cap["traffic"],
+        "basis": "algorithmic flops (the reference's fp64 expressions, SURVEY 8(a)) per "
+                 "launch / mean CUDA-event launch time; peak = FFMA probe in this run",
+        "peak_nominal": nominal, "frac_of_nominal": achieved / nominal,
+        "executed_fp32": cap.get("executed_fp32"), "capture_stale": cap["stale"],
         "kernel": {"fast": "k_solve32f", "gnu": "k_solve32<3,Gnu>",
                    "exact": "k_solve32x"}[args.mode] + " (fused optimize_field + 1-ch apply_field)"
                   " with its k_frame_prep launch (downsample + matte + LR packing, ~2 % of kernel_ms)",
@@ -319,16 +466,15 @@ def run_ours(args, ws, rank, local):
         "hbm_achieved_gbs": nbytes / (k_ms * 1e-3) / 1e9,
         "peak_source": f"FFMA probe in this run ({fp32_mhz:.0f} MHz implied)",
     }
-    winstr = load_traffic().get("solve_apply_fast_c3_warp_instr") if args.mode == "fast" else None
+    winstr = cap["warp_instr"]
     if winstr:
         # The kernel is instruction-issue bound: the floor of its executed
         # instruction stream (ncu count per launch, profiles/) at 4 warp
         # instructions / cycle / SM, at the clock the FFMA probe measured.
-        sms = torch.cuda.get_device_properties(local).multi_processor_count
         floor_ms = winstr / (4 * sms * fp32_mhz * 1e6) * 1e3
         roofline["issue_bound"] = {
             "warp_instr_per_launch": winstr, "floor_ms": floor_ms,
-            "frac": floor_ms / k_ms, "source": "profiles/r01_ncu_solve32f.md (ncu --set full)"}
+            "frac": floor_ms / k_ms, "source": f"profiles/traffic.json[{key}] (ncu --set full)"}
     if args.mode == "fast":
         # The north star's pair search ("every LR candidate pair (i, j)") is
         # the reference's Exact mode: the same frames through the same entry
@@ -346,14 +492,20 @@ def run_ours(args, ws, rank, local):
         x_ms = statistics.mean(xev[k][f][0].elapsed_time(xev[k][f][1]) for k in range(3)
                                for f in range(nf))
         xflops, _ = algorithmic_work(W_, H_, SCALE, 3, "exact", 1)
+        xcap = capture_of("solve_apply_exact_c3", x_ms, fp32_tflops, nominal)
+        xach = xflops / (x_ms * 1e-3) / 1e12
         roofline["pair_search"] = {
             "mode": "exact", "kernel": "k_solve32x (fused optimize_field + 1-ch apply_field) "
             "with its k_frame_prep launch", "kernel_ms": x_ms,
             "algorithmic_flops_per_launch": xflops,
-            "achieved": xflops / (x_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
-            "frac": xflops / (x_ms * 1e-3) / 1e12 / fp32_tflops,
+            "achieved": xach, "unit": "TFLOP/s",
+            "frac": xach / fp32_tflops, "frac_of_nominal": xach / nominal,
+            "basis": "algorithmic-equivalent (REFORMULATED: the kernel hoists D' = D / sqrt(|D|^2"
+                     " + eps) per owner cell and executes far fewer flops than the reference's "
+                     "1,755 per pixel; see executed_fp32 for utilisation)",
+            "executed_fp32": xcap.get("executed_fp32"), "capture_stale": xcap["stale"],
             "value": nf * W_ * H_ / (nf * x_ms * 1e-3) / 1e6, "value_unit": "HR Mpix/s",
-            "traffic": load_traffic().get("solve_apply_exact_c3")}
+            "traffic": xcap["traffic"]}
         if rank == 0 and ws == 1 and not args.no_cpu_baseline:
             # the pair search's own output against the reference (one frame)
             try:
@@ -366,13 +518,12 @@ def run_ours(args, ws, rank, local):
                 roofline["pair_search"]["parity_sample"] = "frame 0 vs oracle/_ref (exact mode)"
             except Exception as e:  # reported, never silently replaced
                 roofline["pair_search"]["parity"] = f"error: {type(e).__name__}: {e}"
-        xinstr = load_traffic().get("solve_apply_exact_c3_warp_instr")
+        xinstr = xcap["warp_instr"]
         if xinstr:
-            sms = torch.cuda.get_device_properties(local).multi_processor_count
             xfloor = xinstr / (4 * sms * fp32_mhz * 1e6) * 1e3
             roofline["pair_search"]["issue_bound"] = {
                 "warp_instr_per_launch": xinstr, "floor_ms": xfloor, "frac": xfloor / x_ms,
-                "source": "profiles/r01_ncu_solve32x_exact.md (ncu --set full)"}
+                "source": "profiles/traffic.json[solve_apply_exact_c3] (ncu --set full)"}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             hbm = json.load(fh)["hbm_gbs"]
@@ -380,6 +531,21 @@ def run_ours(args, ws, rank, local):
         roofline["hbm_peak_gbs"] = hbm
     except Exception:
         pass
+
+    hbm_gbs = None
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            hbm_gbs = json.load(fh)["hbm_gbs"]
+    except Exception:
+        pass
+    c5 = None
+    if not args.no_c5:
+        del frames
+        torch.cuda.empty_cache()
+        try:
+            c5 = run_c5(args, ws, rank, dist, hbm_gbs)
+        except Exception as e:  # reported, never silently replaced
+            c5 = {"error": f"{type(e).__name__}: {e}"}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -409,7 +575,8 @@ def run_ours(args, ws, rank, local):
             "gpu_launches": launches,
             "roofline": roofline,
             "cpu_baseline": cpu,
-            "clocks": clk.summary(),
+            "clocks": clocks,
+            "c5": c5,
         }
         print(json.dumps(line), flush=True)
     if dist:

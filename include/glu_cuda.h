@@ -219,6 +219,34 @@ int glu_cu_op_color(glu_ctx* ctx, const float* in, size_t n, const double* M3x3,
 /* 1-channel matte: out = 1 / (1 + exp(-10 (Y - 0.5))), Y = BT.601 luma. */
 int glu_cu_op_matte(glu_ctx* ctx, const float* in, size_t n, float* out);
 
+/* The reference's black-box operator stand-ins (glu::SimOperator,
+ * simop.hpp:11-26): kind, gain (ScalarGain), gamma (Gamma), row-major 3x3
+ * mix (ChannelMix).  Every output channel is clamp01 of the reference's
+ * double expression (simop.cpp:16-41). */
+enum glu_sim_kind { GLU_OP_IDENTITY = 0, GLU_OP_GAIN = 1, GLU_OP_MIX = 2, GLU_OP_GRAY = 3,
+                    GLU_OP_GAMMA = 4, GLU_OP_INVERT = 5 };
+typedef struct glu_sim_operator {
+    int kind;
+    double gain;
+    double gamma;
+    double mix[9];
+} glu_sim_operator;
+/* apply_operator (simop.cpp:120-132) on n RGB pixels (LR targets). */
+int glu_cu_apply_operator(glu_ctx* ctx, const glu_sim_operator* op, const float* in, size_t n,
+                          float* out);
+/* The edit loop's "edit T-down, then upsample" in one pass over the HR field:
+ * apply_field(field, apply_operator(op, lowIn), clampOutput) -- the operator
+ * runs once per LR cell inside the target packing, the HR pass is the RGB
+ * apply (out: W*H*3 floats). */
+int glu_cu_apply_operator_field(glu_ctx* ctx, const glu_pixel_params* field, const glu_grid* grid,
+                                const glu_sim_operator* op, const float* lowIn, int clampOutput,
+                                float* out);
+/* The same over a row band of the field (multi-GPU C5, as glu_cu_apply_field_band). */
+int glu_cu_apply_operator_field_band(glu_ctx* ctx, const glu_pixel_params* bandField,
+                                     size_t bandPixels, const glu_grid* grid,
+                                     const glu_sim_operator* op, const float* lowIn,
+                                     int clampOutput, float* out);
+
 /* Batched per-pixel selection (optimize_pixel_{fast,exact,gnu},
  * upsample.cpp:178-192): instance k has pixel colour ip[3k..], counts[k]
  * candidates starting at offsets[k] in candIdx/candRgb. */

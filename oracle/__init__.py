@@ -233,6 +233,21 @@ class Reference(_Common):
         w = np.array([out[2]], np.uint32).view(np.float32)[0]
         return int(out[0]), int(out[1]), float(w)
 
+    def apply_operator(self, kind: int, img, gain=1.0, gamma=1.0, mix=None) -> np.ndarray:
+        """apply_operator (simop.cpp:120-132) with the reference's operator
+        constructors (kind: 0 identity, 1 gain, 2 mix, 3 gray, 4 gamma, 5 invert)."""
+        L = self.lib
+        f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+        L.glu_r_apply_operator.argtypes = [C.c_int, C.c_double, C.c_double, f64p, _f32p, C.c_int,
+                                           C.c_int, _f32p]
+        img = _f32(img)
+        m = np.ascontiguousarray(np.eye(3) if mix is None else mix, np.float64).reshape(9)
+        out = np.zeros_like(img)
+        if L.glu_r_apply_operator(int(kind), float(gain), float(gamma), m, img, img.shape[1],
+                                  img.shape[0], out):
+            raise ValueError("apply_operator: invalid operator")
+        return out
+
     def set_num_threads(self, n: int) -> None:
         self.lib.glu_r_set_num_threads(n)
 

@@ -6,6 +6,7 @@
 // It is used (1) to generate the golden vectors in tests/golden/ that pin
 // oracle/glu_oracle.c, and (2) as the CPU baseline ("kind": "reference") timed
 // by bench.py.  Nothing in the product links it.
+#include <array>
 #include <cstdio>
 #include <cstring>
 #include <span>
@@ -57,6 +58,32 @@ int guarded(F&& f) {
 extern "C" {
 
 void glu_r_set_num_threads(int n) { set_num_threads(n); }
+
+// apply_operator (simop.cpp:120-132) with an operator built by the
+// reference's own constructors: kind 0 identity, 1 gain, 2 mix, 3 gray,
+// 4 gamma, 5 invert.
+int glu_r_apply_operator(int kind, double gain, double gamma, const double* mix, const float* in,
+                         int w, int h, float* out) {
+    return guarded([&] {
+        SimOperator op;
+        switch (kind) {
+            case 0: op = identity_op(); break;
+            case 1: op = scalar_gain_op(gain); break;
+            case 2: {
+                std::array<double, 9> m{};
+                for (int i = 0; i < 9; ++i) m[i] = mix[i];
+                op = channel_mix_op(m);
+                break;
+            }
+            case 3: op = grayscale_op(); break;
+            case 4: op = gamma_op(gamma); break;
+            case 5: op = invert_op(); break;
+            default: throw std::invalid_argument("kind");
+        }
+        const ImageF32 r = apply_operator(op, wrap(in, w, h));
+        std::memcpy(out, r.data.data(), r.data.size() * sizeof(float));
+    });
+}
 int glu_r_num_threads() { return num_threads(); }
 
 // Synthetic generators of the reference (synth.cpp), used to build the same

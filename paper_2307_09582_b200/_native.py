@@ -36,6 +36,11 @@ class GluJointStats(C.Structure):
                 ("trialsRejected", C.c_int), ("components", C.c_int)]
 
 
+class GluSimOperator(C.Structure):
+    _fields_ = [("kind", C.c_int), ("gain", C.c_double), ("gamma", C.c_double),
+                ("mix", C.c_double * 9)]
+
+
 class GluError(RuntimeError):
     """A CUDA / runtime failure reported by the C-ABI (GLU_ECUDA / GLU_ENOMEM)."""
 
@@ -104,6 +109,9 @@ SIGNATURES: dict[str, tuple] = {
     "glu_cu_ssim": (I, [P, P, P, I, I, C.POINTER(D)]),
     "glu_cu_op_color": (I, [P, P, SZ, P, P, D, P]),
     "glu_cu_op_matte": (I, [P, P, SZ, P]),
+    "glu_cu_apply_operator": (I, [P, C.POINTER(GluSimOperator), P, SZ, P]),
+    "glu_cu_apply_operator_field": (I, [P, P, GP, C.POINTER(GluSimOperator), P, I, P]),
+    "glu_cu_apply_operator_field_band": (I, [P, P, SZ, GP, C.POINTER(GluSimOperator), P, I, P]),
     "glu_cu_optimize_pixel_batch": (I, [P, P, P, P, P, SZ, D, I, P]),
     "glu_cu_pair_eval": (I, [P, P, P, P, P, SZ, D, P, P, P]),
     "glu_h_grid_downsample": (I, [P, P, GP, P]),

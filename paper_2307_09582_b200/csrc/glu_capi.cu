@@ -713,6 +713,59 @@ int glu_cu_op_color(glu_ctx* ctx, const float* in, size_t n, const double* M,
     return GLU_OK;
 }
 
+namespace {
+// The reference's constructors' checks (simop.cpp:44-87).
+int check_sim_operator(const glu_sim_operator* op) {
+    if (!op) return einval("operator must not be null");
+    if (op->kind < GLU_OP_IDENTITY || op->kind > GLU_OP_INVERT) return einval("unknown operator");
+    if (op->kind == GLU_OP_GAIN && !(op->gain >= 0))
+        return einval("scalar_gain_op: gain must be >= 0");
+    if (op->kind == GLU_OP_GAMMA && !(op->gamma > 0))
+        return einval("gamma_op: gamma must be > 0");
+    return GLU_OK;
+}
+}  // namespace
+
+int glu_cu_apply_operator(glu_ctx* ctx, const glu_sim_operator* op, const float* in, size_t n,
+                          float* out) {
+    if (!ctx) return einval("ctx must not be null");
+    GLU_TRY(check_sim_operator(op));
+    if (n == 0) return GLU_OK;
+    GLU_CUDA(launch_apply_operator(ctx, *op, in, n, out), "apply_operator");
+    return GLU_OK;
+}
+
+int glu_cu_apply_operator_field(glu_ctx* ctx, const glu_pixel_params* field, const glu_grid* g,
+                                const glu_sim_operator* op, const float* lowIn, int clampOutput,
+                                float* out) {
+    if (!ctx) return einval("ctx must not be null");
+    GLU_TRY(check_grid(g));
+    GLU_TRY(check_sim_operator(op));
+    if ((reinterpret_cast<uintptr_t>(field) | reinterpret_cast<uintptr_t>(out)) % 16 != 0)
+        return einval("apply_operator_field: field and out must be 16-byte aligned");
+    GLU_CUDA(launch_apply_operator_field(ctx, field, npx_of(g), *op, lowIn, lown_of(g),
+                                         clampOutput, out),
+             "apply_operator_field");
+    return GLU_OK;
+}
+
+int glu_cu_apply_operator_field_band(glu_ctx* ctx, const glu_pixel_params* bandField,
+                                     size_t bandPixels, const glu_grid* g,
+                                     const glu_sim_operator* op, const float* lowIn,
+                                     int clampOutput, float* out) {
+    if (!ctx) return einval("ctx must not be null");
+    GLU_TRY(check_grid(g));
+    GLU_TRY(check_sim_operator(op));
+    if (bandPixels > npx_of(g)) return einval("apply_field: band exceeds the grid");
+    if ((reinterpret_cast<uintptr_t>(bandField) | reinterpret_cast<uintptr_t>(out)) % 16 != 0)
+        return einval("apply_operator_field: field and out must be 16-byte aligned");
+    if (bandPixels == 0) return GLU_OK;
+    GLU_CUDA(launch_apply_operator_field(ctx, bandField, bandPixels, *op, lowIn, lown_of(g),
+                                         clampOutput, out),
+             "apply_operator_field");
+    return GLU_OK;
+}
+
 int glu_cu_op_matte(glu_ctx* ctx, const float* in, size_t n, float* out) {
     if (!ctx) return einval("ctx must not be null");
     if (n == 0) return GLU_OK;

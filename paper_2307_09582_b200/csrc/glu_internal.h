@@ -96,6 +96,12 @@ cudaError_t launch_self_error(glu_ctx* ctx, const float* high, const glu_pixel_p
 cudaError_t launch_op_color(glu_ctx* ctx, const float* in, size_t n, const double* M,
                             const double* bias, double gammaExp, float* out);
 cudaError_t launch_op_matte(glu_ctx* ctx, const float* in, size_t n, float* out);
+cudaError_t launch_apply_operator(glu_ctx* ctx, const glu_sim_operator& op, const float* in,
+                                  size_t n, float* out);
+// k_op_pack_target4 + k_apply3v (field and out 16-byte aligned).
+cudaError_t launch_apply_operator_field(glu_ctx* ctx, const glu_pixel_params* field, size_t npx,
+                                        const glu_sim_operator& op, const float* lowIn,
+                                        size_t lowN, int clamp, float* out);
 cudaError_t launch_ffma_probe(glu_ctx* ctx, float* sink, int iters, int blocks, int threads);
 cudaError_t launch_pixel_batch(glu_ctx* ctx, const float* ip, const uint32_t* offsets,
                                const uint32_t* candIdx, const float* candRgb, size_t count,

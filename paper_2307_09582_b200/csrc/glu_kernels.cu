@@ -284,6 +284,7 @@ struct ColorOp {
     double m[9];
     double b[3];
     double gammaExp;
+    int hasBias;
 };
 
 // gamma (simop.cpp:33-36, clamp01 11-13) then channel mix (22-27) + bias.
@@ -294,9 +295,58 @@ __global__ void k_op_color(const float* __restrict__ in, size_t n, ColorOp op,
     float v[3] = {in[3 * i], in[3 * i + 1], in[3 * i + 2]};
     if (op.gammaExp > 0)
         for (int c = 0; c < 3; ++c) v[c] = clamp01d(pow(double(v[c]), op.gammaExp));
-    for (int r = 0; r < 3; ++r)
-        out[3 * i + r] = clamp01d(op.m[3 * r] * v[0] + op.m[3 * r + 1] * v[1] +
-                                  op.m[3 * r + 2] * v[2] + op.b[r]);
+    for (int r = 0; r < 3; ++r) {
+        double y = op.m[3 * r] * v[0] + op.m[3 * r + 1] * v[1] + op.m[3 * r + 2] * v[2];
+        if (op.hasBias) y += op.b[r];  // (no bias: -0.0 stays -0.0, as channel_mix)
+        out[3 * i + r] = clamp01d(y);
+    }
+}
+
+// SimOperator::apply (simop.cpp:16-41): each channel clamp01 of the double
+// expression, in the reference's operation order (no contraction).
+__device__ __forceinline__ void sim_apply(const glu_sim_operator& op, const float* v, float* o) {
+    switch (op.kind) {
+        case GLU_OP_GAIN:
+            for (int c = 0; c < 3; ++c) o[c] = clamp01d(op.gain * v[c]);
+            return;
+        case GLU_OP_MIX:
+            for (int r = 0; r < 3; ++r)
+                o[r] = clamp01d(op.mix[r * 3] * v[0] + op.mix[r * 3 + 1] * v[1] +
+                                op.mix[r * 3 + 2] * v[2]);
+            return;
+        case GLU_OP_GRAY: {
+            const float g = clamp01d(0.299 * v[0] + 0.587 * v[1] + 0.114 * v[2]);
+            o[0] = o[1] = o[2] = g;
+            return;
+        }
+        case GLU_OP_GAMMA:
+            for (int c = 0; c < 3; ++c) o[c] = clamp01d(pow(double(v[c]), op.gamma));
+            return;
+        case GLU_OP_INVERT:
+            for (int c = 0; c < 3; ++c) o[c] = clamp01d(1.0 - v[c]);
+            return;
+        default:
+            for (int c = 0; c < 3; ++c) o[c] = v[c];
+    }
+}
+
+__global__ void k_apply_operator(const float* __restrict__ in, size_t n, glu_sim_operator op,
+                                 float* __restrict__ out) {
+    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float v[3] = {in[3 * i], in[3 * i + 1], in[3 * i + 2]};
+    sim_apply(op, v, out + 3 * i);
+}
+
+// The operator fused into k_pack_target4: T = op(lowIn) as float4 cells.
+__global__ void k_op_pack_target4(const float* __restrict__ in, unsigned n, glu_sim_operator op,
+                                  float4* __restrict__ t4) {
+    const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float v[3] = {in[3 * size_t(i)], in[3 * size_t(i) + 1], in[3 * size_t(i) + 2]};
+    float o[3];
+    sim_apply(op, v, o);
+    t4[i] = make_float4(o[0], o[1], o[2], 0.0f);
 }
 
 __global__ void k_op_matte(const float* __restrict__ in, size_t n, float* __restrict__ out) {
@@ -463,8 +513,30 @@ cudaError_t launch_op_color(glu_ctx* ctx, const float* in, size_t n, const doubl
     ColorOp op{};
     for (int i = 0; i < 9; ++i) op.m[i] = M ? M[i] : (i % 4 == 0 ? 1.0 : 0.0);
     for (int i = 0; i < 3; ++i) op.b[i] = bias ? bias[i] : 0.0;
+    op.hasBias = bias != nullptr;
     op.gammaExp = gammaExp;
     k_op_color<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(in, n, op, out);
+    ++ctx->launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_apply_operator(glu_ctx* ctx, const glu_sim_operator& op, const float* in,
+                                  size_t n, float* out) {
+    k_apply_operator<<<blocks_for(n, 256), 256, 0, ctx->stream>>>(in, n, op, out);
+    ++ctx->launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_apply_operator_field(glu_ctx* ctx, const glu_pixel_params* field, size_t npx,
+                                        const glu_sim_operator& op, const float* lowIn,
+                                        size_t lowN, int clamp, float* out) {
+    if (npx == 0) return cudaSuccess;
+    float4* t4 = static_cast<float4*>(scratch(ctx, S_TARGET4, lowN * sizeof(float4)));
+    if (!t4) return cudaErrorMemoryAllocation;
+    k_op_pack_target4<<<blocks_for(lowN, 256), 256, 0, ctx->stream>>>(lowIn, unsigned(lowN), op, t4);
+    ++ctx->launches;
+    k_apply3v<<<blocks_for((npx + 3) / 4, 256), 256, 0, ctx->stream>>>(field, npx, t4,
+                                                                      unsigned(lowN), clamp, out);
     ++ctx->launches;
     return cudaGetLastError();
 }

@@ -542,6 +542,137 @@ def op_matte(low: torch.Tensor) -> torch.Tensor:
     return out
 
 
+# ---- SimOperator (simop.hpp:11-37): the reference's black-box operator stand-ins ----
+
+class SimOperator:
+    """glu::SimOperator (simop.hpp:11-26): a pointwise colour operator, applied
+    on the device (glu_cu_apply_operator) with the reference's double
+    expressions and clamp01 (simop.cpp:16-41)."""
+
+    class Kind(enum.IntEnum):
+        Identity = 0
+        ScalarGain = 1
+        ChannelMix = 2
+        Grayscale = 3
+        Gamma = 4
+        Invert = 5
+
+    def __init__(self, kind: "SimOperator.Kind" = Kind.Identity, gain: float = 1.0,
+                 gamma: float = 1.0, mix=(1, 0, 0, 0, 1, 0, 0, 0, 1), name: str = "identity"):
+        self.kind, self.gain, self.gamma = SimOperator.Kind(kind), float(gain), float(gamma)
+        self.mix = tuple(float(v) for v in np.asarray(mix, np.float64).reshape(9))
+        self.name = name
+
+    def linear(self) -> bool:
+        K = SimOperator.Kind
+        return self.kind in (K.Identity, K.ScalarGain, K.ChannelMix, K.Grayscale)
+
+    def c(self) -> N.GluSimOperator:
+        return N.GluSimOperator(int(self.kind), self.gain, self.gamma, (C.c_double * 9)(*self.mix))
+
+
+def identity_op() -> SimOperator:
+    return SimOperator()
+
+
+def scalar_gain_op(gain: float) -> SimOperator:
+    if not gain >= 0:
+        raise ValueError("scalar_gain_op: gain must be >= 0")
+    return SimOperator(SimOperator.Kind.ScalarGain, gain=gain, name=f"gain({gain:g})")
+
+
+def channel_mix_op(m) -> SimOperator:
+    return SimOperator(SimOperator.Kind.ChannelMix, mix=m, name="mix")
+
+
+def grayscale_op() -> SimOperator:
+    return SimOperator(SimOperator.Kind.Grayscale, name="gray")
+
+
+def gamma_op(gamma: float) -> SimOperator:
+    if not gamma > 0:
+        raise ValueError("gamma_op: gamma must be > 0")
+    return SimOperator(SimOperator.Kind.Gamma, gamma=gamma, name=f"gamma({gamma:g})")
+
+
+def invert_op() -> SimOperator:
+    return SimOperator(SimOperator.Kind.Invert, name="invert")
+
+
+def parse_operator(text: str) -> SimOperator:
+    """identity | gain:<c> | gamma:<g> | gray | invert | mix:m00,...,m22 (simop.cpp:89-118)."""
+    if text == "identity":
+        return identity_op()
+    if text == "gray":
+        return grayscale_op()
+    if text == "invert":
+        return invert_op()
+    head, sep, rest = text.partition(":")
+    if sep:
+        if head == "gain":
+            return scalar_gain_op(float(rest))
+        if head == "gamma":
+            return gamma_op(float(rest))
+        if head == "mix":
+            vals = rest.split(",")
+            if len(vals) < 9:
+                raise ValueError("mix needs 9 comma-separated values")
+            if len(vals) > 9:
+                raise ValueError("mix needs exactly 9 values")
+            return channel_mix_op([float(v) for v in vals])
+    raise ValueError("unknown operator: " + text)
+
+
+def apply_operator(op: SimOperator, img: torch.Tensor) -> torch.Tensor:
+    """apply_operator (simop.cpp:120-132) on a device RGB image."""
+    img = _image(img, "apply_operator")
+    out = torch.empty_like(img)
+    ctx = context(img.device.index)
+    N.check(N.lib().glu_cu_apply_operator(ctx.handle, C.byref(op.c()), _ptr(img),
+                                          img.shape[0] * img.shape[1], _ptr(out)))
+    return out
+
+
+def apply_operator_field(field: ParamField, op: SimOperator, lowIn: torch.Tensor,
+                         clampOutput: bool = True, out: torch.Tensor | None = None
+                         ) -> torch.Tensor:
+    """apply_field(field, apply_operator(op, lowIn)) in one pass over the HR
+    field: the edit loop's "operator on T-down, then upsample"
+    (glu_cu_apply_operator_field)."""
+    g = field.grid
+    lowIn = _image(lowIn, "apply_operator_field")
+    if lowIn.shape[1] != g.lowW or lowIn.shape[0] != g.lowH:
+        raise ValueError("apply_field: low-res image does not match grid")
+    if out is None:
+        out = torch.empty((g.highH, g.highW, 3), dtype=torch.float32, device=lowIn.device)
+    ctx = context(lowIn.device.index)
+    N.check(N.lib().glu_cu_apply_operator_field(ctx.handle, _ptr(field.params), C.byref(g.c()),
+                                                C.byref(op.c()), _ptr(lowIn),
+                                                int(bool(clampOutput)), _ptr(out)))
+    return out
+
+
+def apply_operator_field_band(bandParams: torch.Tensor, grid: GridSpec, op: SimOperator,
+                              lowIn: torch.Tensor, clampOutput: bool = True,
+                              out: torch.Tensor | None = None) -> torch.Tensor:
+    """apply_operator_field over a (rows, W, 3) int32 row band of a field of
+    `grid` (multi-GPU C5); returns (rows, W, 3)."""
+    lowIn = _image(lowIn, "apply_operator_field")
+    if lowIn.shape[1] != grid.lowW or lowIn.shape[0] != grid.lowH:
+        raise ValueError("apply_field: low-res image does not match grid")
+    if bandParams.dim() != 3 or bandParams.shape[1] != grid.highW or bandParams.shape[2] != 3:
+        raise ValueError("apply_field: band does not match grid")
+    bandParams = bandParams.contiguous()
+    rows = bandParams.shape[0]
+    if out is None:
+        out = torch.empty((rows, grid.highW, 3), dtype=torch.float32, device=lowIn.device)
+    ctx = context(lowIn.device.index)
+    N.check(N.lib().glu_cu_apply_operator_field_band(
+        ctx.handle, _ptr(bandParams), rows * grid.highW, C.byref(grid.c()), C.byref(op.c()),
+        _ptr(lowIn), int(bool(clampOutput)), _ptr(out)))
+    return out
+
+
 # ---- frame pipeline (BASELINE.json configs[2]) -----------------------------------
 
 TARGET_OPS = {"identity": 0, "matte": 1}

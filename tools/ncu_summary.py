@@ -1,7 +1,8 @@
 """Summarise ncu outputs into profiles/ (tracked).
 
   python tools/ncu_summary.py launches <launches.csv> <out.md>
-  python tools/ncu_summary.py kernel <report.ncu-rep> <out.md> [--traffic-key KEY]
+  python tools/ncu_summary.py kernel <report.ncu-rep> <out.md> [--traffic-key KEY] [--id N]
+                                    [--sources a.cu,b.cuh]
 
 `launches`: per-kernel launch count, total / mean device time and share of the
 captured launches (ncu's launch list is cold-cache and serialised: compare
@@ -61,13 +62,17 @@ WANT = [
 ]
 
 
-def kernel(rep: str, out: str, traffic_key: str | None) -> None:
+def kernel(rep: str, out: str, traffic_key: str | None, kid: int = 0,
+           sources: list[str] | None = None) -> None:
+    """Summarise result `kid` (0-based, ncu's ID) of the report."""
     det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(det)))
     hdr = rows[0]
     im, iu, iv, ik = (hdr.index("Metric Name"), hdr.index("Metric Unit"),
                       hdr.index("Metric Value"), hdr.index("Kernel Name"))
+    iid = hdr.index("ID")
+    rows = [hdr] + [r for r in rows[1:] if r[iid] == str(kid)]
     kname = short(rows[1][ik]) if len(rows) > 1 else "?"
     vals = {}
     for r in rows[1:]:
@@ -76,7 +81,7 @@ def kernel(rep: str, out: str, traffic_key: str | None) -> None:
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rr = list(csv.reader(io.StringIO(raw)))
-    rawd = dict(zip(rr[0], rr[2])) if len(rr) > 2 else {}
+    rawd = dict(zip(rr[0], rr[2 + kid])) if len(rr) > 2 + kid else {}
     units = dict(zip(rr[0], rr[1])) if len(rr) > 1 else {}
 
     def rawval(name):
@@ -90,7 +95,20 @@ def kernel(rep: str, out: str, traffic_key: str | None) -> None:
     dram_r, dram_w = rawval("dram__bytes_read.sum"), rawval("dram__bytes_write.sum")
     sass = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"],
                           capture_output=True, text=True).stdout
-    srows = list(csv.reader(io.StringIO(sass)))
+    blocks, cur = [], None
+    for r in csv.reader(io.StringIO(sass)):
+        if r and r[0] == "Kernel Name":
+            cur = []
+            blocks.append(cur)
+        elif cur is not None:
+            cur.append(r)
+    # (the page may list a result twice in a row -- one block per source
+    # view -- so identical consecutive blocks are merged)
+    dedup = []
+    for blk in blocks:
+        if not dedup or dedup[-1][:3] != blk[:3] or len(dedup[-1]) != len(blk):
+            dedup.append(blk)
+    srows = [["Kernel Name"]] + (dedup[kid] if kid < len(dedup) else [])
     mix = collections.Counter()
     if len(srows) > 2:
         h2 = srows[1]
@@ -121,12 +139,38 @@ def kernel(rep: str, out: str, traffic_key: str | None) -> None:
             lines.append(f"| {op} | {n} | {100 * n / tot:.1f}% |")
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
+    # executed floating-point work per launch (thread-level, predicated on):
+    # FFMA = 2 flops (the north-star's hardware FP32 FLOP/s)
+    cyc = rawval("smsp__cycles_elapsed.avg") or rawval("smsp__cycles_elapsed.max")
+
+    def thread_ops(op):
+        v = rawval(f"smsp__sass_thread_inst_executed_op_{op}_pred_on.sum.per_cycle_elapsed")
+        return v * cyc if v is not None and cyc else None
+
+    f32 = [thread_ops(o) for o in ("ffma", "fadd", "fmul")]
+    f64 = [thread_ops(o) for o in ("dfma", "dadd", "dmul")]
+    fp32_exec = 2 * f32[0] + f32[1] + f32[2] if None not in f32 else None
+    fp64_exec = 2 * f64[0] + f64[1] + f64[2] if None not in f64 else None
+    if fp32_exec is not None:
+        extra = [f"| executed FP32 flop (2 FFMA + FADD + FMUL, thread-level) | {fp32_exec:.4g} |",
+                 f"| executed FP64 flop (2 DFMA + DADD + DMUL) | {fp64_exec:.4g} |"]
+        lines[4:4] = extra
+        open(out, "w").write("\n".join(lines) + "\n")
     if traffic_key and dram_r is not None:
+        import hashlib
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         d = json.load(open(tp)) if os.path.exists(tp) else {}
         d[traffic_key] = dram_r + dram_w
         if tot:  # executed warp instructions per launch (bench.py's issue bound)
             d[traffic_key + "_warp_instr"] = tot
+        if fp32_exec is not None:
+            d[traffic_key + "_fp32_flop_executed"] = fp32_exec
+            d[traffic_key + "_fp64_flop_executed"] = fp64_exec
+        if sources:  # bench.py flags the numbers stale when these files change
+            h = hashlib.sha256()
+            for f in sources:
+                h.update(open(os.path.join(ROOT, f), "rb").read())
+            d[traffic_key + "_src"] = {"files": sources, "sha256": h.hexdigest()[:16]}
         json.dump(d, open(tp, "w"), indent=1)
 
 
@@ -135,4 +179,7 @@ if __name__ == "__main__":
         launches(sys.argv[2], sys.argv[3])
     else:
         key = sys.argv[sys.argv.index("--traffic-key") + 1] if "--traffic-key" in sys.argv else None
-        kernel(sys.argv[2], sys.argv[3], key)
+        kid = int(sys.argv[sys.argv.index("--id") + 1]) if "--id" in sys.argv else 0
+        srcs = (sys.argv[sys.argv.index("--sources") + 1].split(",")
+                if "--sources" in sys.argv else None)
+        kernel(sys.argv[2], sys.argv[3], key, kid, srcs)
