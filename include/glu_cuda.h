@@ -274,6 +274,31 @@ typedef struct glu_trial_log {
     uint32_t cellCapacity, pixelCapacity;
 } glu_trial_log;
 
+/* ---- banded joint loop (SURVEY §8(e), C4 over HR row bands) -------------- *
+ * A rank owns the LR rows [r0, r1) of the grid and the HR rows of their
+ * footprints; paper_2307_09582_b200/bands.py runs the loop of
+ * jointopt.cpp:182-206 over bands (downsample + solve per band, band CCL with a
+ * seam merge, trials owned by the band of their first pixel in rounds, change
+ * logs exchanged between rounds).  Buffers are full-size (global indices);
+ * only the band (and its halo rows) is ever written or read. */
+/* grid_downsample (grid.cpp:41-52) of the LR rows [r0, r1) into `low` (the full
+ * LR buffer); reads only the HR rows of the band. */
+int glu_cu_downsample_band(glu_ctx* ctx, const float* high, const glu_grid* grid, int r0, int r1,
+                           float* low);
+/* joint_optimize's initial optimize_field + self error map (jointopt.cpp:187-190)
+ * for the LR rows [r0, r1): `low` must hold LR rows [r0 - h, r1 + h) (h = S / 2,
+ * the solve's halo).  Writes field / errors for the band's HR rows; the rows of
+ * the h LR rows around the band are used as scratch (refreshed by the caller's
+ * halo exchange). */
+int glu_cu_solve_band(glu_ctx* ctx, const float* high, const float* low, const glu_grid* grid,
+                      const glu_config* cfg, int mode, int r0, int r1, glu_pixel_params* field,
+                      float* errors);
+/* Host: the round of each component of a sweep for a banded schedule: owners[i]
+ * = the rank running trial i; round(i) = max over earlier components j within
+ * Chebyshev `reach` of i of round(j) (same owner) or round(j) + 1 (other owner). */
+int glu_trial_rounds(const int32_t* boxes, size_t count, int reach, const int32_t* owners,
+                     int32_t* rounds);
+
 /* Cell bounding boxes {x0, y0, x1, y1} of components (device, 4 int32 each). */
 int glu_cu_component_boxes(glu_ctx* ctx, const uint32_t* compOffsets,
                            const uint32_t* compPixels, size_t count, const glu_grid* grid,

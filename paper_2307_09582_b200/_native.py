@@ -110,6 +110,9 @@ SIGNATURES: dict[str, tuple] = {
     "glu_cu_op_color": (I, [P, P, SZ, P, P, D, P]),
     "glu_cu_op_matte": (I, [P, P, SZ, P]),
     "glu_cu_apply_operator": (I, [P, C.POINTER(GluSimOperator), P, SZ, P]),
+    "glu_cu_downsample_band": (I, [P, P, GP, I, I, P]),
+    "glu_cu_solve_band": (I, [P, P, P, GP, CP, I, I, I, P, P]),
+    "glu_trial_rounds": (I, [P, SZ, I, P, P]),
     "glu_cu_apply_operator_field": (I, [P, P, GP, C.POINTER(GluSimOperator), P, I, P]),
     "glu_cu_apply_operator_field_band": (I, [P, P, SZ, GP, C.POINTER(GluSimOperator), P, I, P]),
     "glu_cu_optimize_pixel_batch": (I, [P, P, P, P, P, SZ, D, I, P]),

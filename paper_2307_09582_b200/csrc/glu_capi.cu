@@ -682,6 +682,83 @@ int glu_trial_levels(const int32_t* boxes, size_t n, int reach, int32_t* levels)
     return GLU_OK;
 }
 
+int glu_trial_rounds(const int32_t* boxes, size_t n, int reach, const int32_t* owners,
+                     int32_t* rounds) {
+    if ((n && (!boxes || !owners || !rounds)) || reach < 0)
+        return einval("glu_trial_rounds: bad arguments");
+    // the bins of glu_trial_levels
+    constexpr int kBin = 16;
+    int maxX = 0, maxY = 0;
+    for (size_t i = 0; i < n; ++i) {
+        maxX = std::max(maxX, boxes[4 * i + 2]);
+        maxY = std::max(maxY, boxes[4 * i + 3]);
+    }
+    const int bw = maxX / kBin + 1, bh = maxY / kBin + 1;
+    std::vector<std::vector<uint32_t>> bins(size_t(bw) * bh);
+    for (size_t i = 0; i < n; ++i) {
+        const int32_t* b = boxes + 4 * i;
+        const int x0 = std::max(0, b[0] - reach), y0 = std::max(0, b[1] - reach);
+        const int x1 = b[2] + reach, y1 = b[3] + reach;
+        int r = 0;
+        for (int by = y0 / kBin; by <= std::min(bh - 1, y1 / kBin); ++by)
+            for (int bx = x0 / kBin; bx <= std::min(bw - 1, x1 / kBin); ++bx)
+                for (uint32_t j : bins[size_t(by) * bw + bx]) {
+                    const int32_t* c = boxes + 4 * size_t(j);
+                    const int dx = std::max(0, std::max(c[0] - b[2], b[0] - c[2]));
+                    const int dy = std::max(0, std::max(c[1] - b[3], b[1] - c[3]));
+                    if (std::max(dx, dy) <= reach)
+                        r = std::max(r, rounds[j] + (owners[j] != owners[i] ? 1 : 0));
+                }
+        rounds[i] = r;
+        for (int by = b[1] / kBin; by <= b[3] / kBin; ++by)
+            for (int bx = b[0] / kBin; bx <= b[2] / kBin; ++bx)
+                bins[size_t(by) * bw + bx].push_back(uint32_t(i));
+    }
+    return GLU_OK;
+}
+
+int glu_cu_downsample_band(glu_ctx* ctx, const float* high, const glu_grid* g, int r0, int r1,
+                           float* low) {
+    if (!ctx) return einval("ctx must not be null");
+    GLU_TRY(check_grid(g));
+    if (r0 < 0 || r1 > g->lowH || r0 > r1) return einval("band: LR rows out of range");
+    if (r0 == r1) return GLU_OK;
+    // the band's sample pixels min(cy s + s/2, H - 1) lie in its HR rows
+    const int y0 = r0 * g->scale, y1 = std::min(r1 * g->scale, g->highH);
+    GLU_CUDA(launch_grid_downsample(ctx, high + size_t(y0) * g->highW * 3, g->highW, y1 - y0,
+                                    g->scale, g->lowW, r1 - r0, low + size_t(r0) * g->lowW * 3),
+             "downsample_band");
+    return GLU_OK;
+}
+
+int glu_cu_solve_band(glu_ctx* ctx, const float* high, const float* low, const glu_grid* g,
+                      const glu_config* cfg, int mode, int r0, int r1, glu_pixel_params* field,
+                      float* errors) {
+    if (!ctx) return einval("ctx must not be null");
+    GLU_TRY(glu_config_validate(cfg));
+    GLU_TRY(check_grid(g));
+    GLU_TRY(check_mode(mode));
+    if (r0 < 0 || r1 > g->lowH || r0 > r1) return einval("band: LR rows out of range");
+    if (r0 == r1) return GLU_OK;
+    // The band plus its h-row LR halo as a sub-image: its owned rows see the
+    // same (unclipped) windows as in the full grid; stored indices are
+    // rebased to the full grid (idxBase); the halo rows' outputs are scratch.
+    const int h = cfg->windowSide / 2;
+    const int ls = std::max(0, r0 - h), le = std::min(g->lowH, r1 + h);
+    const int y0 = ls * g->scale, y1 = std::min(le * g->scale, g->highH);
+    glu_grid sub = *g;
+    sub.highH = y1 - y0;
+    sub.lowH = le - ls;
+    const size_t off = size_t(y0) * g->highW;
+    SolveArgs a = solve_args(high + 3 * off, low + size_t(ls) * g->lowW * 3, &sub, cfg, mode);
+    a.params = field + off;
+    a.errOut = errors + off;
+    a.idxBase = unsigned(ls) * unsigned(g->lowW);
+    a.fallbacks = ctx->d_counters;
+    GLU_CUDA(launch_solve(ctx, a), "solve_band");
+    return GLU_OK;
+}
+
 int glu_cu_run_trials(glu_ctx* ctx, const float* high, float* low, glu_pixel_params* field,
                       float* errors, const glu_grid* g, const glu_config* cfg, int mode,
                       const uint32_t* off, const uint32_t* px, const uint32_t* ids, size_t n,

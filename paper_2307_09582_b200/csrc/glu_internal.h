@@ -63,6 +63,9 @@ struct SolveArgs {
     unsigned sdiv;  // ceil(2^32 / s) when W, H < 2^16 (x / s = umulhi(x, sdiv)), else 0
     float epsf;     // (float)eps for the fp32 filter
     float* errOut;  // optional: self reconstruction error per pixel (k_self_error fused)
+    // Added to the stored LR indices: a row band solved as a sub-image whose
+    // LR rows start at global row r (idxBase = r * lowW of the full grid).
+    unsigned idxBase;
 };
 
 // Launchers (return cudaError_t of the launch).

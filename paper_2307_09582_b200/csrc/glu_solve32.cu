@@ -291,8 +291,8 @@ __global__ void __launch_bounds__(kThreads, GLU_SOLVE_MIN_BLOCKS)
     }
     if (a.params) {
         unsigned* o = reinterpret_cast<unsigned*>(a.params + p);
-        o[0] = ia;
-        o[1] = ib;
+        o[0] = ia + a.idxBase;
+        o[1] = ib + a.idxBase;
         o[2] = __float_as_uint(w);
     }
     if (a.lowT) {

@@ -362,8 +362,8 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
     }
     if (a.params) {
         unsigned* o = reinterpret_cast<unsigned*>(a.params + p);
-        o[0] = ia;
-        o[1] = ib;
+        o[0] = ia + a.idxBase;
+        o[1] = ib + a.idxBase;
         o[2] = __float_as_uint(w);
     }
     if (a.lowT) {

@@ -175,3 +175,85 @@ def test_two_rank_banded_apply_matches_full_apply():
         assert p.exitcode == 0
     res = dict(q.get(timeout=10) for _ in range(2))
     assert res == {0: True, 1: True}
+
+
+def _bands_comm_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2307_09582_b200 import bands
+        comm = bands.DistBandComm()
+        # variable-length all-gather (change logs, CSR lists, LR rows)
+        mine = torch.arange(3 * (rank + 2), dtype=torch.int32).reshape(-1, 3) + 100 * rank
+        got = comm.all_gather([mine])[0]
+        shapes = [tuple(t.shape) for t in got]
+        firsts = [int(t[0, 0]) for t in got]
+        sums = comm.all_reduce_sum([[rank + 1, 5]])
+        # halo rows of params / errors between neighbouring bands (send / recv)
+        H, W = 32, 8
+        st = bands.BandState(rank, sharding.row_bands(H, 4, 3, world)[rank],
+                             torch.zeros(1), torch.full((H, W, 3), rank, dtype=torch.int32),
+                             torch.full((H, W), float(rank)))
+        comm.exchange_rows([st], [(0, 1, 12, 16), (1, 0, 16, 20)])
+        ok = (bool(torch.all(st.params[12:16] == 0)) and bool(torch.all(st.params[16:20] == 1))
+              and bool(torch.all(st.errors[12:20] == torch.tensor([0.0] * 4 + [1.0] * 4)[:, None])))
+        q.put((rank, shapes, firsts, sums, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_band_comm():
+    """bands.DistBandComm over gloo: variable-size all-gather, sum all-reduce and
+    the neighbour halo exchange of params / errors rows."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bands_comm_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    for _ in range(2):
+        rank, shapes, firsts, sums, ok = q.get(timeout=10)
+        assert shapes == [(2, 3), (3, 3)] and firsts == [0, 100] and sums == [3, 10] and ok
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_seam_merge_matches_full_find_large_error(world):
+    """bands._merge (the seam union-find and the global component list) on band
+    CCL results equals find_large_error on the whole map (jointopt.cpp:9-46):
+    the band CCL is the oracle's here (test stand-in for the kernel); the merge
+    is the product code."""
+    import numpy as np
+
+    import oracle
+    from paper_2307_09582_b200 import bands
+    from paper_2307_09582_b200.glu import GridSpec
+    ora = oracle.Oracle()
+    rng = np.random.default_rng(world)
+    H, W, s = 96, 70, 4
+    e = (rng.random((H, W)) < 0.45).astype(np.float32)   # percolating blobs cross seams
+    e[:, 33] = 1.0                                         # a column through every seam
+    g = GridSpec.create(W, H, s)
+    bl = sharding.row_bands(H, s, 3, world)
+    parts, states = [], []
+    for b in bl:
+        y0, y1 = b.hr_rows
+        mask, comps = ora.find_large_error(e[y0:y1], 0.5)
+        lab = np.full((y1 - y0, W), -1, np.int64)
+        for c in comps:
+            lab.reshape(-1)[c.astype(np.int64)] = int(c[0]) + y0 * W
+        off = np.zeros(len(comps) + 1, np.int64)
+        off[1:] = np.cumsum([len(c) for c in comps])
+        px = (np.concatenate(comps).astype(np.int64) if comps else np.zeros(0, np.int64)) + y0 * W
+        parts.append((torch.from_numpy(np.stack([lab[0], lab[-1]])), torch.from_numpy(off),
+                      torch.from_numpy(px)))
+        states.append(bands.BandState(b.rank, b, torch.zeros(1), torch.zeros(1, dtype=torch.int32),
+                                      torch.zeros(1)))
+    comm = bands.LocalBandComm(world)
+    off, px = bands._merge(states, g, comm, parts)[0]
+    _, want = ora.find_large_error(e, 0.5)
+    got = [px[off[k]:off[k + 1]].numpy().astype(np.uint32) for k in range(off.numel() - 1)]
+    assert len(got) == len(want)
+    assert all(a.tobytes() == b.tobytes() for a, b in zip(got, want))
