@@ -47,6 +47,7 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--c5-targets", type=int, default=64)
     p.add_argument("--no-c5", action="store_true")
+    p.add_argument("--no-c4", action="store_true")
     return p.parse_args()
 
 
@@ -317,6 +318,62 @@ def run_c5(args, ws, rank, dist, hbm_gbs):
     }
 
 
+# ---- C4: joint optimisation at 8K over HR row bands (configs[3]) ---------------------
+
+def run_c4(args, ws, rank, dist):
+    """BASELINE.json configs[3]: joint_optimize of the 7680x4320 scene at s = 16.
+    One rank: the device-resident loop (glu_cu_joint_optimize).  Under torchrun:
+    paper_2307_09582_b200.bands (one HR row band per rank; NCCL all-gathers /
+    send-recv between the phases), checked against the one-GPU result on every
+    rank's band.  Times: CUDA events, max over ranks, best of `reps`."""
+    import torch
+    import paper_2307_09582_b200 as glu
+    from paper_2307_09582_b200 import bands, workloads
+    cfg = workloads.CONFIGS[4]
+    high = torch.from_numpy(workloads.scene(cfg["W"], cfg["H"], 4, 0)).cuda()
+
+    def timed(fn, reps=3):
+        best, out = None, None
+        for _ in range(reps + 1):
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            out = fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            if dist:
+                t = torch.tensor([ms], device="cuda")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                ms = float(t.item())
+            best = ms if best is None else min(best, ms)
+        return best, out
+
+    ms1, ref = timed(lambda: glu.joint_optimize(high, cfg["scale"]))
+    line = {"workload": "C4 (configs[3]): joint_optimize 7680x4320, s=16, fast mode",
+            "unit": "HR Mpix/s", "n_gpus": ws, "scaling": "strong",
+            "single_gpu_ms": ms1, "iterations": ref.iterations,
+            "accepted": ref.trialsAccepted, "rejected": ref.trialsRejected}
+    if ws == 1:
+        line.update(value=cfg["W"] * cfg["H"] / (ms1 * 1e-3) / 1e6, ms=ms1,
+                    path="glu_cu_joint_optimize (one device)")
+        return line
+    msb, (st, _, stats) = timed(lambda: bands.joint_optimize_banded(high, cfg["scale"]))
+    y0, y1 = st.band.hr_rows
+    ok = torch.equal(st.params[y0:y1], ref.field.params[y0:y1]) and \
+        torch.equal(st.errors[y0:y1], ref.errors[y0:y1]) and torch.equal(st.low, ref.low) and \
+        (stats["accepted"], stats["rejected"]) == (ref.trialsAccepted, ref.trialsRejected)
+    t = torch.tensor([1 if ok else 0], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    line.update(value=cfg["W"] * cfg["H"] / (msb * 1e-3) / 1e6, ms=msb,
+                path=f"bands.joint_optimize_banded ({ws} HR row bands)",
+                rounds_per_sweep=stats["rounds"], replicated_sweeps=stats["replicated_sweeps"],
+                parity_vs_single_gpu=bool(t.item()))
+    return line
+
+
 # ---- arms ---------------------------------------------------------------------------
 
 def run_reference(args, ws, rank):
@@ -547,6 +604,14 @@ def run_ours(args, ws, rank, local):
         except Exception as e:  # reported, never silently replaced
             c5 = {"error": f"{type(e).__name__}: {e}"}
 
+    c4 = None
+    if not args.no_c4:
+        torch.cuda.empty_cache()
+        try:
+            c4 = run_c4(args, ws, rank, dist)
+        except Exception as e:  # reported, never silently replaced
+            c4 = {"error": f"{type(e).__name__}: {e}"}
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
@@ -577,6 +642,7 @@ def run_ours(args, ws, rank, local):
             "cpu_baseline": cpu,
             "clocks": clocks,
             "c5": c5,
+            "c4": c4,
         }
         print(json.dumps(line), flush=True)
     if dist:
