@@ -16,9 +16,12 @@
 // per-pair bound, and sends the remaining ties between differently coloured
 // pairs to the reference's exact double-precision path.  The stored weight is
 // recomputed in double in the reference's order.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <cassert>
+#include <cstdint>
 
 #include "glu_internal.h"
 #include "glu_math.cuh"
@@ -224,30 +227,22 @@ __device__ __noinline__ uint3 solve_double(const float4* packed, int lw, int lh,
 
 // The tile's staged candidate cells and pair table (shared memory).
 struct XTile {
-    const float4* wcells;  // candidate cells of the tile's owner cells (+- 1), cw per row
-    const float4* table;   // kCellStride float4 per owner cell: D' of its 36 pairs
-    int cw, ncw, ocx0, ocy0;
-#ifdef GLU_X_DEBUG
-    int nrow, nwin, ntab;  // owner-cell rows, staged cells, table float4s (bounds checks)
-#endif
+    const float4* wcells;  // candidate cells of the tile's owner cells (+- 1), pitch cw;
+                           // .w = the cell's LR index, or its 1-channel target value
+    int cw;
 };
 
-// One HR pixel (x, y) with guide colour (ip0, ip1, ip2): the pair search,
-// tie recovery, weight and the fused epilogues.
+enum Out { kOutParams = 0, kOutApply1 = 1, kOutGeneric = 2 };
+
+// One HR pixel with guide colour (ip0, ip1, ip2): the pair search, tie
+// recovery, weight and the fused epilogues.  `swin` = its owner cell's window
+// (top-left candidate) in the staged cells, `tab` = the cell's pair table.
+template <int OUT, int P>
 __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* packed, const XTile& t,
-                                            int forceFallback, int x, int y, float ip0, float ip1,
-                                            float ip2) {
-    const int cw = t.cw;
-    const size_t p = size_t(y) * a.W + x;
-    const int cx = div_s(x, a), cy = div_s(y, a);
-    // the window in shared memory: candidate j is swin[(j / 3) * cw + j % 3]
-    const float4* swin = t.wcells + (cy - t.ocy0) * cw + (cx - t.ocx0);
-    const float4* tab = t.table + ((cy - t.ocy0) * t.ncw + (cx - t.ocx0)) * kCellStride;
-#ifdef GLU_X_DEBUG  // bounds of the staged window / table (debug builds)
-    assert(cy >= t.ocy0 && cx >= t.ocx0 && cx - t.ocx0 < t.ncw && cy - t.ocy0 + 2 < t.nrow + 2);
-    assert((cy - t.ocy0 + 2) * cw + (cx - t.ocx0) + 2 < t.nwin);
-    assert(((cy - t.ocy0) * t.ncw + (cx - t.ocx0) + 1) * kCellStride <= t.ntab);
-#endif
+                                            const float4* swin, const float4* tab,
+                                            int forceFallback, size_t p, int cx, int cy, float ip0,
+                                            float ip1, float ip2) {
+    const int cw = P > 0 ? P : t.cw;
 
     // j-outer scan: pair (i, j) needs only e_j = I_j - I_p and q_j = |e_j|^2
     // (D'_ij = D_ij / sqrt(den) comes from the cell's table: obj = q_j -
@@ -299,8 +294,8 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
         bj = K1 != k1in ? j : bj;
     }
     int bi = int(__float_as_uint(K1) & 15u);
-    bool ok = !forceFallback && K1 < kInf && ip0 == ip0 && ip1 == ip1 && ip2 == ip2 &&
-              (qmin >= 1e-27f || qmin == 0.0f);
+    // (a NaN guide channel makes every key NaN: K1 stays +inf)
+    bool ok = !forceFallback && K1 < kInf && (qmin >= 1e-27f || qmin == 0.0f);
     // An exact colour match I_j0 == I_p: the pairs (i, j0) have objective 0
     // in double (w = 0, v = 0) and every other pair a positive one (a
     // non-matching colour has a nonzero double distance, even where its fp32
@@ -330,9 +325,6 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
         const float qb = __fmaf_rn(eb2, eb2, __fmaf_rn(eb1, eb1, __fmul_rn(eb0, eb0)));
         const float lim = K1 + __fmaf_rn(kT, qb, 2e-36f);
         if (K2 <= lim) {
-#ifdef GLU_X_COUNT_RECHECK
-            if (a.fallbacks) atomicAdd(a.fallbacks + 1, 1ull);
-#endif
             const ClosePick c =
                 resolve_close(swin, tab, cw, ip0, ip1, ip2, lim, kmask, bi, bj, a.eps, a.fallbacks);
             ok = c.ok;
@@ -345,76 +337,118 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
     // (the pair's colours are re-read here rather than kept live across the
     // out-of-line call, which would spill them on every pixel)
     const float4 ci = swin[woff(bi, cw)], cj = swin[woff(bj, cw)];
-    uint32_t ia, ib;
-    float w;
+    float w, wa = ci.w, wb = cj.w;
     if (ok) {
-        const int ri = (bi * 11) >> 5, rj = (bj * 11) >> 5;
-        ia = uint32_t(cy - 1 + ri) * uint32_t(a.lw) + uint32_t(cx - 1 + bi - 3 * ri);
-        ib = uint32_t(cy - 1 + rj) * uint32_t(a.lw) + uint32_t(cx - 1 + bj - 3 * rj);
         const float ip[3] = {ip0, ip1, ip2};
         const float a3[3] = {ci.x, ci.y, ci.z}, b3[3] = {cj.x, cj.y, cj.z};
         w = wSet ? wClose : weight_exact64_f(ip, a3, b3, a.eps);
     } else {
         const uint3 r = solve_double(packed, a.lw, a.lh, a.eps, a.fallbacks, cx, cy, ip0, ip1, ip2);
-        ia = r.x;
-        ib = r.y;
         w = __uint_as_float(r.z);
+        if (OUT == kOutApply1) {
+            wa = __ldg(a.lowT + r.x);
+            wb = __ldg(a.lowT + r.y);
+        } else {
+            wa = __uint_as_float(r.x);
+            wb = __uint_as_float(r.y);
+        }
     }
-    if (a.params) {
+    if (OUT == kOutApply1) {  // the video path: 1-channel matte, no params
+        a.out[p] = lerp_clamp(w, wa, wb, a.clamp != 0);
+        return;
+    }
+    const uint32_t ia = __float_as_uint(wa), ib = __float_as_uint(wb);
+    if (OUT == kOutParams || a.params) {
         unsigned* o = reinterpret_cast<unsigned*>(a.params + p);
         o[0] = ia + a.idxBase;
         o[1] = ib + a.idxBase;
         o[2] = __float_as_uint(w);
     }
-    if (a.lowT) {
-        const bool clamp = a.clamp != 0;
-        if (a.channels == 1) {
-            a.out[p] = lerp_clamp(w, __ldg(a.lowT + ia), __ldg(a.lowT + ib), clamp);
-        } else {
+    if (OUT == kOutGeneric) {
+        if (a.lowT) {
+            const bool clamp = a.clamp != 0;
+            if (a.channels == 1) {
+                a.out[p] = lerp_clamp(w, __ldg(a.lowT + ia), __ldg(a.lowT + ib), clamp);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+                    a.out[3 * p + k] = lerp_clamp(w, __ldg(a.lowT + 3 * size_t(ia) + k),
+                                                  __ldg(a.lowT + 3 * size_t(ib) + k), clamp);
+            }
+        }
+        if (a.errOut) {  // pixel_error of the clamped self reconstruction (jointopt.cpp:190)
+            float r[3];
 #pragma unroll
             for (int k = 0; k < 3; ++k)
-                a.out[3 * p + k] = lerp_clamp(w, __ldg(a.lowT + 3 * size_t(ia) + k),
-                                              __ldg(a.lowT + 3 * size_t(ib) + k), clamp);
+                r[k] = lerp_clamp(w, __ldg(a.low + 3 * size_t(ia) + k),
+                                  __ldg(a.low + 3 * size_t(ib) + k), true);
+            const float ipx[3] = {ip0, ip1, ip2};
+            a.errOut[p] = pixel_error(ipx, r);
         }
-    }
-    if (a.errOut) {  // pixel_error of the clamped self reconstruction (jointopt.cpp:190)
-        float r[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k)
-            r[k] = lerp_clamp(w, __ldg(a.low + 3 * size_t(ia) + k), __ldg(a.low + 3 * size_t(ib) + k),
-                              true);
-        const float ipx[3] = {ip0, ip1, ip2};
-        a.errOut[p] = pixel_error(ipx, r);
     }
 }
 
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+// A CTA solves a tile of kTX = 32 columns x tileH = kTY * rows rows; warp ty
+// owns rows [ty * rows, (ty + 1) * rows).  Dynamic shared memory: [guide:
+// tileH x 96 floats, one TMA (cp.async.bulk.tensor.2d) when useTma][pair
+// table: maxCells x kCellStride][candidate cells: pitch x (mch + 2)].
+template <int OUT, int P>
 __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS)
-    k_solve32x(SolveArgs a, const float4* packed, int forceFallback, const unsigned* nanFlag,
-               int maxCells, int maxWin, int rows) {
-    extern __shared__ float4 smem[];
-    float4* table = smem;                         // maxCells * kCellStride
-    float4* wcells = smem + maxCells * kCellStride;  // the tile's candidate cells
+    k_solve32x(const __grid_constant__ CUtensorMap tmap, SolveArgs a, const float4* packed,
+               int forceFallback, const unsigned* nanFlag, int maxCells, int rows, int useTma) {
+    extern __shared__ __align__(1024) float xsm[];
+    __shared__ __align__(8) unsigned long long bar;
+    const int tileH = kTY * rows;
+    float* gtile = xsm;
+    float4* table = reinterpret_cast<float4*>(xsm + size_t(tileH) * 96);
+    float4* wcells = table + maxCells * kCellStride;
+    const int tx = threadIdx.x % kTX, ty = threadIdx.x / kTX;
+    const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * tileH;
+    if (useTma && threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)),
+                     "r"(unsigned(tileH * 96 * 4))
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(gtile)),
+            "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(3 * x0), "r"(y0), "r"(smem_u32(&bar))
+            : "memory");
+    }
     forceFallback |= int(__ldg(nanFlag));
     const int pw = a.lw + 2;  // h = 1
-    const int tileH = kTY * rows;  // a CTA solves a kTX x tileH tile
-    const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * tileH;
     const int ocx0 = div_s(x0, a), ocy0 = div_s(y0, a);
     const int ncw = div_s(min(x0 + kTX - 1, a.W - 1), a) - ocx0 + 1;
     const int nch = div_s(min(y0 + tileH - 1, a.H - 1), a) - ocy0 + 1;
     const float eps = a.epsf;
-    const int cw = ncw + 2;
-    // the first pixel's guide colour is requested before the staging barriers
-    const int x = x0 + (threadIdx.x % kTX), yb = y0 + (threadIdx.x / kTX);
-    const bool xin = x < a.W;
-    float g0 = 0.0f, g1 = 0.0f, g2 = 0.0f;
-    if (xin && yb < a.H) {
-        const float* g = a.high + 3 * (size_t(yb) * a.W + x);
-        g0 = __ldg(g);
-        g1 = __ldg(g + 1);
-        g2 = __ldg(g + 2);
+    const int cw = P > 0 ? P : ncw + 2;
+    // packed cell (c - 1) of the LR grid is at padded index c; .w becomes what
+    // the epilogue reads from a winning cell
+    for (int k = threadIdx.x; k < cw * (nch + 2); k += kThreads) {
+        const int r = k / cw, c = k - r * cw;
+        if (c < ncw + 2) {
+            float4 v = __ldg(packed + size_t(ocy0 + r) * pw + (ocx0 + c));
+            const int lx = ocx0 + c - 1, ly = ocy0 + r - 1;
+            const bool in = lx >= 0 && ly >= 0 && lx < a.lw && ly < a.lh;
+            const unsigned li = in ? unsigned(ly) * unsigned(a.lw) + unsigned(lx) : 0u;
+            v.w = OUT == kOutApply1 ? (in ? __ldg(a.lowT + li) : 0.0f) : __uint_as_float(li);
+            wcells[k] = v;
+        }
     }
-    for (int k = threadIdx.x; k < cw * (nch + 2); k += kThreads)
-        wcells[k] = __ldg(packed + size_t(ocy0 + k / cw) * pw + (ocx0 + k % cw));
+    if (!useTma) {  // the guide rows are not 16-byte aligned: staged by the threads
+        for (int k = threadIdx.x; k < tileH * 96; k += kThreads) {
+            const int r = k / 96, c = k - r * 96;
+            const int y = y0 + r;
+            gtile[k] = (y < a.H && x0 * 3 + c < a.W * 3)
+                           ? __ldg(a.high + 3 * (size_t(y) * a.W + x0) + c)
+                           : 0.0f;
+        }
+    }
     __syncthreads();
     // thread t builds pair pr = t % 36 for cells t / 36, t / 36 + 7, ... (the
     // pair decode is paid once per thread)
@@ -436,56 +470,86 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS)
         table[cell * kCellStride + pr] = make_float4(d0 * r, d1 * r, d2 * r, 0.0f);
     }
     __syncthreads();
-
-#ifdef GLU_X_DEBUG
-    assert(ncw * nch <= maxCells && cw * (nch + 2) <= maxWin);
-    const XTile t{wcells, table, cw, ncw, ocx0, ocy0, nch, cw * (nch + 2), maxCells * kCellStride};
-#else
-    const XTile t{wcells, table, cw, ncw, ocx0, ocy0};
-#endif
+    if (useTma) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n"
+            "W:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+            "@!p bra W;\n}" ::"r"(smem_u32(&bar))
+            : "memory");
+    }
+    const XTile t{wcells, cw};
+    const int x = x0 + tx;
+    if (x >= a.W) return;
+    const int cx = div_s(x, a);
+    const int yr = y0 + ty * rows;
+    const int yEnd = min(yr + rows, a.H);
+    const float* g = gtile + (ty * rows) * 96 + 3 * tx;
+    size_t p = size_t(yr) * a.W + x;
+    // owner-cell row of the current row, advanced when y reaches yNext
+    int cy = div_s(yr, a);
+    int yNext = (cy + 1) * a.s;
+    const float4* swin = wcells + (cy - ocy0) * cw + (cx - ocx0);
+    const float4* tab = table + ((cy - ocy0) * ncw + (cx - ocx0)) * kCellStride;
 #pragma unroll 1
-    for (int k = 0; k < rows; ++k) {
-        const int y = yb + k * kTY;
-        if (k > 0 && xin && y < a.H) {  // (prefetching one scan ahead measured slower)
-            const float* g = a.high + 3 * (size_t(y) * a.W + x);
-            g0 = __ldg(g);
-            g1 = __ldg(g + 1);
-            g2 = __ldg(g + 2);
+    for (int y = yr; y < yEnd; ++y, g += 96, p += a.W) {
+        if (y == yNext) {
+            ++cy;
+            yNext += a.s;
+            swin += cw;
+            tab += ncw * kCellStride;
         }
-        const float ip0 = g0, ip1 = g1, ip2 = g2;
-        if (xin && y < a.H) solve_pixel(a, packed, t, forceFallback, x, y, ip0, ip1, ip2);
+        solve_pixel<OUT, P>(a, packed, t, swin, tab, forceFallback, p, cx, cy, g[0], g[1], g[2]);
     }
 }
 
-}  // namespace
-
-bool solve32x_supported(int mode, int S, int s) {
-    return mode == GLU_MODE_EXACT && S == 3 && s >= 3;
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }();
+    return fn;
 }
 
-cudaError_t launch_solve32x(glu_ctx* ctx, const SolveArgs& a, const float4* packed,
-                            int forceFallback, const unsigned* nanFlag) {
+int max_pitch(int s) { return (kTX - 1) / s + 4; }
+
+template <int OUT, int P>
+cudaError_t launch_xp(glu_ctx* ctx, const SolveArgs& a, const float4* packed, int forceFallback,
+                      const unsigned* nanFlag) {
     // Rows per thread: more rows amortise a tile's staging (cells, pair
-    // table, two barriers) over more pixels, fewer rows give more tiles and a
-    // smaller partial last wave.  Pick the count minimising waves x (rows +
-    // staging cost) among those whose tile fits kSmemCap.  Owner cells a tile
-    // can touch: ncw <= (kTX - 1) / s + 2, nch <= (tileH - 1) / s + 2.
+    // table, guide, two barriers) over more pixels, fewer rows give more
+    // tiles and a smaller partial last wave.  Pick the count minimising waves
+    // x (rows + staging cost) among those whose tile fits kSmemCap.  Owner
+    // cells a tile can touch: ncw <= (kTX - 1) / s + 2, nch <= (tileH - 1) / s + 2.
     int dev = 0;
     cudaGetDevice(&dev);
     const int mcw = (kTX - 1) / a.s + 2;
+    const int pitch = P > 0 ? P : max_pitch(a.s);
     const long tilesX = (a.W + kTX - 1) / kTX;
-    thread_local int memo[5] = {-1, 0, 0, 0, 1};  // device, s, W, H -> rows
-    if (memo[0] != dev || memo[1] != a.s || memo[2] != a.W || memo[3] != a.H) {
+    auto smem_of = [&](int r) {
+        const int mch = (kTY * r - 1) / a.s + 2;
+        return sizeof(float) * size_t(kTY * r) * 96 +
+               sizeof(float4) * (size_t(mcw * mch) * kCellStride + size_t(pitch) * (mch + 2));
+    };
+    thread_local int memo[6] = {-1, 0, 0, 0, -1, 1};  // device, s, W, H, key -> rows
+    const int key = OUT * 64 + P;
+    if (memo[0] != dev || memo[1] != a.s || memo[2] != a.W || memo[3] != a.H || memo[4] != key) {
         int nsm = 148, rows = 1;
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         float best = -1.0f;
         for (int r = 1; r <= kMaxRows; ++r) {
-            const int mch = (kTY * r - 1) / a.s + 2;
-            const size_t sm =
-                sizeof(float4) * (size_t(mcw * mch) * kCellStride + (mcw + 2) * (mch + 2));
+            const size_t sm = smem_of(r);
             if (r > 1 && sm > kSmemCap) break;
+            cudaFuncSetAttribute(k_solve32x<OUT, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(sm));
             int per = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_solve32x, kThreads, sm);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_solve32x<OUT, P>, kThreads, sm);
             const long slots = long(max(per, 1)) * nsm;
             const long tiles = tilesX * ((a.H + kTY * r - 1) / (kTY * r));
             const float cost = float((tiles + slots - 1) / slots) * (float(r) + kStageCost);
@@ -498,19 +562,62 @@ cudaError_t launch_solve32x(glu_ctx* ctx, const SolveArgs& a, const float4* pack
         memo[1] = a.s;
         memo[2] = a.W;
         memo[3] = a.H;
-        memo[4] = rows;
+        memo[4] = key;
+        memo[5] = rows;
     }
-    const int rows = memo[4];
-    const int mch = (kTY * rows - 1) / a.s + 2;
+    const int rows = memo[5];
+    const int tileH = kTY * rows;
+    const int mch = (tileH - 1) / a.s + 2;
     const int maxCells = mcw * mch;
-    const size_t smem = sizeof(float4) * (size_t(maxCells) * kCellStride + (mcw + 2) * (mch + 2));
-    if (smem > 48 * 1024)  // one row per thread at s = 3: 12 x 4 cells fit in 48 KB
-        cudaFuncSetAttribute(k_solve32x, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    dim3 grid(unsigned(tilesX), (a.H + kTY * rows - 1) / (kTY * rows));
-    k_solve32x<<<grid, kThreads, smem, ctx->stream>>>(a, packed, forceFallback, nanFlag, maxCells,
-                                                        (mcw + 2) * (mch + 2), rows);
+    CUtensorMap tmap{};
+    int useTma = 0;
+    if (a.W % 4 == 0 && (reinterpret_cast<uintptr_t>(a.high) & 15u) == 0) {
+        if (auto enc = tensor_map_encoder()) {
+            const cuuint64_t dims[2] = {cuuint64_t(3) * a.W, cuuint64_t(a.H)};
+            const cuuint64_t strides[1] = {cuuint64_t(12) * a.W};
+            const cuuint32_t box[2] = {96u, cuuint32_t(tileH)};
+            const cuuint32_t estr[2] = {1u, 1u};
+            useTma = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a.high), dims,
+                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+        }
+    }
+    const size_t smem = smem_of(rows);
+    cudaError_t e = cudaFuncSetAttribute(k_solve32x<OUT, P>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    dim3 grid(unsigned(tilesX), (a.H + tileH - 1) / tileH);
+    k_solve32x<OUT, P><<<grid, kThreads, smem, ctx->stream>>>(tmap, a, packed, forceFallback,
+                                                              nanFlag, maxCells, rows, useTma);
     ++ctx->launches;
     return cudaGetLastError();
+}
+
+template <int OUT>
+cudaError_t launch_xo(glu_ctx* ctx, const SolveArgs& a, const float4* packed, int forceFallback,
+                      const unsigned* nanFlag) {
+    switch (max_pitch(a.s)) {  // s = 8: 7; s = 16: 5; s >= 32: 4
+        case 4: return launch_xp<OUT, 4>(ctx, a, packed, forceFallback, nanFlag);
+        case 5: return launch_xp<OUT, 5>(ctx, a, packed, forceFallback, nanFlag);
+        case 7: return launch_xp<OUT, 7>(ctx, a, packed, forceFallback, nanFlag);
+        default: return launch_xp<OUT, 0>(ctx, a, packed, forceFallback, nanFlag);
+    }
+}
+
+}  // namespace
+
+bool solve32x_supported(int mode, int S, int s) {
+    return mode == GLU_MODE_EXACT && S == 3 && s >= 3;
+}
+
+cudaError_t launch_solve32x(glu_ctx* ctx, const SolveArgs& a, const float4* packed,
+                            int forceFallback, const unsigned* nanFlag) {
+    if (a.params && !a.lowT && !a.errOut)
+        return launch_xo<kOutParams>(ctx, a, packed, forceFallback, nanFlag);
+    if (!a.params && a.lowT && a.channels == 1 && !a.errOut)
+        return launch_xo<kOutApply1>(ctx, a, packed, forceFallback, nanFlag);
+    return launch_xo<kOutGeneric>(ctx, a, packed, forceFallback, nanFlag);
 }
 
 }  // namespace glu_cu
