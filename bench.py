@@ -418,11 +418,19 @@ def run_ours(args, ws, rank, local):
     import paper_2307_09582_b200 as glu
     from paper_2307_09582_b200 import glu as G
 
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(local % torch.cuda.device_count())
+    local = local % torch.cuda.device_count()
     dist = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # GLU_BENCH_BACKEND=gloo: a functional check of the multi-rank path with
+        # several ranks on one GPU (NCCL refuses two ranks per device); the
+        # measured runs use NCCL
+        backend = os.environ.get("GLU_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     mode = glu.mode_from_name(args.mode)
     nf = args.frames
     frames_np = make_frames(rank, nf)

@@ -203,29 +203,41 @@ def _ctx(t: torch.Tensor):
 
 
 def _band_components(st: BandState, grid: GridSpec, tau: float):
-    """Band-local find_large_error (glu_cu_find_large_error) made global: the
-    labels (smallest pixel index, -1 outside the mask) of the band's first and
-    last HR rows, the band CSR offsets and the pixels as global indices."""
+    """Band-local find_large_error (glu_cu_find_large_error, the sparse
+    variant the joint loop uses) made global: the labels (first pixel, -1
+    outside the mask) of the band's first and last HR rows, the band CSR
+    offsets and the pixels as global indices."""
     y0, y1 = st.band.hr_rows
     W, hb = grid.highW, y1 - y0
     dev = st.errors.device
-    label = torch.empty((hb, W), dtype=torch.int32, device=dev)
     n = C.c_size_t()
     off, px = C.c_void_p(), C.c_void_p()
     ctx = _ctx(st.errors)
     N.check(N.lib().glu_cu_find_large_error(ctx.handle, _ptr(st.errors[y0:y1]), W, hb,
-                                            float(tau), C.c_void_p(0), _ptr(label), C.byref(n),
+                                            float(tau), C.c_void_p(0), C.c_void_p(0), C.byref(n),
                                             C.byref(off), C.byref(px)))
     offsets = torch.zeros(n.value + 1, dtype=torch.int32, device=dev)
     pixels = torch.empty(0, dtype=torch.int32, device=dev)
+    m = 0
     if n.value:
         N.check(N.lib().glu_cu_copy(ctx.handle, _ptr(offsets), off, (n.value + 1) * 4))
-        pixels = torch.empty(int(offsets[-1].item()), dtype=torch.int32, device=dev)
-        N.check(N.lib().glu_cu_copy(ctx.handle, _ptr(pixels), px, pixels.numel() * 4))
+        m = int(offsets[-1].item())
+        pixels = torch.empty(m, dtype=torch.int32, device=dev)
+        N.check(N.lib().glu_cu_copy(ctx.handle, _ptr(pixels), px, m * 4))
     base = y0 * W
-    edge = torch.stack([label[0], label[hb - 1]]).to(torch.int64)
-    edge = torch.where(edge >= 0, edge + base, edge)
-    return edge, offsets.to(torch.int64), pixels.to(torch.int64) + base
+    offsets, pixels = offsets.to(torch.int64), pixels.to(torch.int64)
+    edge = torch.full((2, W), -1, dtype=torch.int64, device=dev)
+    if m:
+        # each pixel's label (its component's first pixel), scattered into
+        # the band's first and last rows
+        comp = torch.repeat_interleave(torch.arange(n.value, device=dev), torch.diff(offsets),
+                                       output_size=m)
+        lab = pixels[offsets[:-1]][comp] + base
+        top = pixels < W
+        edge[0, pixels[top]] = lab[top]
+        bot = pixels >= (hb - 1) * W
+        edge[1, pixels[bot] - (hb - 1) * W] = lab[bot]
+    return edge, offsets, pixels + base
 
 
 def _merge(states, grid: GridSpec, comm, parts):
@@ -257,47 +269,53 @@ def _merge(states, grid: GridSpec, comm, parts):
                 ru, rv = find(u), find(v)
                 if ru != rv:
                     parent[max(ru, rv)] = min(ru, rv)
-        bpix = pixs[k]
-        if not any(find(x) != x for x in parent):
-            # no component crosses a seam: the band lists in band order are the
-            # global list in first-pixel order
-            pixels = torch.cat(list(bpix)) if bpix else torch.zeros(0, dtype=torch.int64)
-            lens = []
-            for o in offs[k]:
-                lens.append(torch.diff(o))
-            sizes = torch.cat(lens) if lens else torch.zeros(0, dtype=torch.int64)
-        else:
+        bpix = list(pixs[k])
+        boff = list(offs[k])
+        # every band component in band order: global first pixel, start, size
+        # (the band lists concatenated are the global list in first-pixel
+        # order when nothing merges)
+        shift, starts, sizes_l = 0, [], []
+        for o in boff:
+            starts.append(o[:-1] + shift)
+            sizes_l.append(torch.diff(o))
+            shift += int(o[-1]) if o.numel() else 0
+        allpix = torch.cat(bpix) if bpix else torch.zeros(0, dtype=torch.int64)
+        start = torch.cat(starts) if starts else torch.zeros(0, dtype=torch.int64)
+        sizes = torch.cat(sizes_l) if sizes_l else torch.zeros(0, dtype=torch.int64)
+        pixels = allpix
+        if parent:
             member = {}
             for x in list(parent):
                 r = find(x)
                 member[x] = r
                 member[r] = r  # (a root is never a key of `parent`)
-            chunks, sizes_l = [], []
-            pending: dict[int, list] = {}
-            for b, o in enumerate(offs[k]):
-                on = o.cpu().numpy()
-                px = bpix[b]
-                if on.size <= 1:
-                    continue
-                firsts = px[o[:-1].to(px.device)].cpu().numpy()
-                for c in range(on.size - 1):
-                    seg = px[int(on[c]):int(on[c + 1])]
-                    r = member.get(int(firsts[c]))
-                    if r is None:
-                        chunks.append(seg)
-                        sizes_l.append(seg.numel())
-                    else:
-                        pending.setdefault(r, []).append(seg)
-                        if r == int(firsts[c]):
-                            chunks.append(r)   # placeholder: filled once every part is seen
-                            sizes_l.append(None)
-            for i, c in enumerate(chunks):
-                if isinstance(c, int):
-                    merged = torch.sort(torch.cat(pending[c])).values
-                    chunks[i] = merged
-                    sizes_l[i] = merged.numel()
+            # the few components that merge: the root keeps its place with the
+            # group's pixels re-sorted, the other members are dropped; the
+            # lists between them are copied as whole slices
+            firsts = allpix[start.to(allpix.device)].cpu().numpy() if start.numel() else []
+            special = [c for c, f in enumerate(firsts.tolist()) if f in member]
+            start_h, size_h = start.tolist(), sizes.tolist()
+            groups: dict[int, list] = {}
+            for c in special:
+                groups.setdefault(member[int(firsts[c])], []).append(c)
+            chunks, new_sizes, prev = [], [], 0
+            for c in special:
+                chunks.append(allpix[start_h[prev] if prev < len(start_h) else 0:start_h[c]]
+                              if c > prev else allpix[0:0])
+                new_sizes.append(sizes[prev:c])
+                root = member[int(firsts[c])]
+                if int(firsts[c]) == root:
+                    merged = torch.sort(torch.cat([allpix[start_h[m]:start_h[m] + size_h[m]]
+                                                   for m in groups[root]])).values
+                    chunks.append(merged)
+                    new_sizes.append(torch.tensor([merged.numel()], dtype=torch.int64,
+                                                  device=sizes.device))
+                prev = c + 1
+            if prev < len(start_h):
+                chunks.append(allpix[start_h[prev]:])
+                new_sizes.append(sizes[prev:])
             pixels = torch.cat(chunks)
-            sizes = torch.tensor(sizes_l, dtype=torch.int64)
+            sizes = torch.cat(new_sizes)
         off = torch.zeros(sizes.numel() + 1, dtype=torch.int32, device=dev)
         if sizes.numel():
             off[1:] = torch.cumsum(sizes.to(dev), 0).to(torch.int32)

@@ -459,7 +459,7 @@ __device__ int run_trial(const TrialState& t, const TrialBuffers& b, TrialSmem<N
 constexpr int kSQ = 2048;  // cells of the component's box
 constexpr int kSW = 4096;  // cells of the box dilated by 2h
 constexpr int kSC = 2048;  // pixels of the component
-constexpr int kSS = 512;   // successors found by the early scan (= the CTA size)
+constexpr int kSS = kSchedThreads > 512 ? kSchedThreads : 512;  // successors found by the early scan (>= the CTA size)
 constexpr uint32_t kParkWords = 128u << 20;  // speculative-record arena (512 MB)
 constexpr size_t kTrialSmemBytes = size_t(kSQ) * 8 + size_t(kSW) * 16 + size_t(kSC) * 16 +
                                    size_t(kSW + 1) * 4 + size_t(kSW) * 4 + size_t(kSQ) * 4 +
