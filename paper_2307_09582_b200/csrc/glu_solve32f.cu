@@ -241,7 +241,10 @@ __device__ __noinline__ float weight_fast_ieee(float ip0, float ip1, float ip2, 
 //     1-channel target value (the video path's fused apply);
 //   * the tile's largest |channel| (k_pack_low's .w) for the rounding floor F.
 
-enum Out { kOutParams = 0, kOutApply1 = 1, kOutGeneric = 2 };
+// kOutParamsErr: the joint loop's initial solve (params + the self error map,
+// jointopt.cpp:187-190) -- the reconstruction uses the winning cells' staged
+// colours (the LR image itself) instead of gathering them again.
+enum Out { kOutParams = 0, kOutApply1 = 1, kOutGeneric = 2, kOutParamsErr = 3 };
 
 struct FTile {
     const float4* wcells;  // staged cells, pitch P (or cw when P = 0)
@@ -355,6 +358,7 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
     }
     // the staged .w of the winning cells: LR indices, or the 1-channel target
     float wa = ca.w, wb = cb.w;
+    float4 la = ca, lb = cb;  // the winning cells' LR colours (kOutParamsErr)
     if (ok) {
         if (MODE == GLU_MODE_GNU) {
             w = 1.0f;
@@ -373,6 +377,12 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
         } else {
             wa = __uint_as_float(r.x);
             wb = __uint_as_float(r.y);
+            if (OUT == kOutParamsErr) {
+                const float* pa = a.low + 3 * size_t(r.x);
+                const float* pb = a.low + 3 * size_t(r.y);
+                la = make_float4(pa[0], pa[1], pa[2], 0.0f);
+                lb = make_float4(pb[0], pb[1], pb[2], 0.0f);
+            }
         }
     }
     if (OUT == kOutApply1) {  // the video path: 1-channel matte, no params
@@ -380,11 +390,17 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
         return;
     }
     const uint32_t ia = __float_as_uint(wa), ib = __float_as_uint(wb);
-    if (OUT == kOutParams || a.params) {
+    if (OUT == kOutParams || OUT == kOutParamsErr || a.params) {
         unsigned* o = reinterpret_cast<unsigned*>(a.params + p);
         o[0] = ia + a.idxBase;
         o[1] = ib + a.idxBase;
         o[2] = __float_as_uint(w);
+    }
+    if (OUT == kOutParamsErr) {  // pixel_error of the clamped self reconstruction
+        const float r[3] = {lerp_clamp(w, la.x, lb.x, true), lerp_clamp(w, la.y, lb.y, true),
+                            lerp_clamp(w, la.z, lb.z, true)};
+        const float ipx[3] = {ip0, ip1, ip2};
+        a.errOut[p] = pixel_error(ipx, r);
     }
     if (OUT == kOutGeneric) {
         if (a.lowT) {
@@ -630,6 +646,8 @@ cudaError_t launch_f(glu_ctx* ctx, const SolveArgs& a, const float4* packed, int
                      const unsigned* nanFlag) {
     if (a.params && !a.lowT && !a.errOut)
         return launch_fo<MODE, kOutParams>(ctx, a, packed, forceFallback, nanFlag);
+    if (a.params && !a.lowT && a.errOut)
+        return launch_fo<MODE, kOutParamsErr>(ctx, a, packed, forceFallback, nanFlag);
     if (!a.params && a.lowT && a.channels == 1 && !a.errOut)
         return launch_fo<MODE, kOutApply1>(ctx, a, packed, forceFallback, nanFlag);
     return launch_fo<MODE, kOutGeneric>(ctx, a, packed, forceFallback, nanFlag);
