@@ -503,10 +503,13 @@ struct TrialGeom {
         dy0 = max(0, b.y - h);
         dw = min(lw - 1, b.z + h) - dx0 + 1;
         dh = min(lh - 1, b.w + h) - dy0 + 1;
-        vx0 = max(0, b.x - 2 * h);
-        vy0 = max(0, b.y - 2 * h);
-        vw = min(lw - 1, b.z + 2 * h) - vx0 + 1;
-        vh = min(lh - 1, b.w + 2 * h) - vy0 + 1;
+        // V is NOT clipped to the grid: cells outside it are staged as +inf
+        // (like the packed LR image's border), so a pixel's 3 x 3 window is
+        // always inside V and needs no bounds checks
+        vx0 = b.x - 2 * h;
+        vy0 = b.y - 2 * h;
+        vw = b.z - b.x + 1 + 4 * h;
+        vh = b.w - b.y + 1 + 4 * h;
         full = (dx0 + dw) * s <= W && (dy0 + dh) * s <= H && lw < 65536 && lh < 65536;
         sh = (s & (s - 1)) == 0 ? __ffs(s) - 1 : -1;
     }
@@ -643,8 +646,13 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
     const int nv = g.vw * g.vh, nq = g.qw * g.qh, nd = g.dw * g.dh;
     for (int k = tid; k < nv; k += NT) {
         const int y = g.vy0 + k / g.vw, x = g.vx0 + k % g.vw;
-        const float* src = t.low + 3 * (size_t(y) * t.lw + x);
-        ss.win[k] = make_float4(src[0], src[1], src[2], max_abs3(src[0], src[1], src[2]));
+        if (x >= 0 && y >= 0 && x < t.lw && y < t.lh) {
+            const float* src = t.low + 3 * (size_t(y) * t.lw + x);
+            ss.win[k] = make_float4(src[0], src[1], src[2], max_abs3(src[0], src[1], src[2]));
+        } else {
+            ss.win[k] = make_float4(__int_as_float(0x7f800000), __int_as_float(0x7f800000),
+                                    __int_as_float(0x7f800000), 0.0f);
+        }
     }
     for (uint32_t i = tid; i < n; i += NT) {
         const uint32_t p = comp[i];
@@ -781,15 +789,11 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
         float4 c_dbg[9];
 #endif
         if (t.S == 3) {
+            // the window inside V (off-grid cells are the staged +inf cells)
+            const float4* wv = ss.win + (cy - 1 - g.vy0) * g.vw + (cx - 1 - g.vx0);
             float4 c[9];
 #pragma unroll
-            for (int k = 0; k < 9; ++k) {
-                const int gx = cx - 1 + k % 3, gy = cy - 1 + k / 3;
-                c[k] = make_float4(__int_as_float(0x7f800000), __int_as_float(0x7f800000),
-                                   __int_as_float(0x7f800000), 0.0f);
-                if (gx >= 0 && gy >= 0 && gx < t.lw && gy < t.lh)
-                    c[k] = ss.win[(gy - g.vy0) * g.vw + (gx - g.vx0)];
-            }
+            for (int k = 0; k < 9; ++k) c[k] = wv[(k / 3) * g.vw + k % 3];
             const Filter32Result fr =
                 t.mode == GLU_MODE_EXACT
                     ? filter32x_pixel(c, ip, float(t.eps), t.eps)
