@@ -227,6 +227,9 @@ int glu_ctx_destroy(glu_ctx* ctx) {
     for (cudaEvent_t ev : ctx->ev)
         if (ev) cudaEventDestroy(ev);
     if (ctx->switchEv) cudaEventDestroy(ctx->switchEv);
+    for (cudaEvent_t ev : ctx->pev)
+        if (ev) cudaEventDestroy(ev);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
     if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
     if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
     cudaStreamDestroy(ctx->own);
@@ -527,6 +530,59 @@ int frame_kernels(glu_ctx* ctx, const float* frame, const glu_grid* g, const glu
     return GLU_OK;
 }
 
+// Device frames (all resident at the call): frame k's k_frame_prep runs on a
+// side stream into buffer set k % 2 while frame k - 1 is solved on the
+// context stream (the prep is a small grid: it fills the solve's last wave).
+// Prep k waits for solve k - 2 (its buffers); solve k waits for prep k.
+int frames_pipelined(glu_ctx* ctx, const float* frames, int count, const glu_grid* g,
+                     const glu_config* cfg, int mode, int targetOp, float* out,
+                     glu_pixel_params* paramsOut) {
+    const size_t n = npx_of(g), ln = lown_of(g);
+    const bool matte = targetOp == GLU_TARGET_MATTE;
+    const int ch = matte ? 1 : 3;
+    const int h = cfg->windowSide / 2;
+    const size_t cells = size_t(g->lowW + 2 * h) * (g->lowH + 2 * h);
+    // per buffer set: low (3 ln floats) | matte (ln) | packed (cells float4) | nanFlag
+    const size_t setBytes = ((ln * 16 + 255) & ~size_t(255)) + cells * 16 + 256;
+    char* base = static_cast<char*>(scratch(ctx, S_SPARE2, 2 * setBytes));
+    if (!base) return GLU_ENOMEM;
+    if (!ctx->side) {
+        GLU_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking), "stream");
+        for (cudaEvent_t& ev : ctx->pev)
+            GLU_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+    }
+    cudaEvent_t* prepped = ctx->pev;     // [2]
+    cudaEvent_t* solved = ctx->pev + 2;  // [2]
+    cudaEvent_t entry = ctx->pev[4];
+    // the side stream starts after everything already issued on the context stream
+    GLU_CUDA(cudaEventRecord(entry, ctx->stream), "pipeline");
+    GLU_CUDA(cudaStreamWaitEvent(ctx->side, entry, 0), "pipeline");
+    for (int k = 0; k < count; ++k) {
+        const int b = k & 1;
+        char* set = base + b * setBytes;
+        float* low = reinterpret_cast<float*>(set);
+        float* tgt = low + 3 * ln;
+        float4* packed = reinterpret_cast<float4*>(set + ((ln * 16 + 255) & ~size_t(255)));
+        unsigned* nanFlag = reinterpret_cast<unsigned*>(packed + cells);
+        SolveArgs a = solve_args(frames + size_t(k) * n * 3, low, g, cfg, mode);
+        a.params = paramsOut ? paramsOut + size_t(k) * n : nullptr;
+        a.lowT = matte ? tgt : low;
+        a.channels = ch;
+        a.clamp = 1;
+        a.out = out + size_t(k) * n * ch;
+        a.fallbacks = ctx->d_counters;
+        if (k >= 2) GLU_CUDA(cudaStreamWaitEvent(ctx->side, solved[b], 0), "pipeline");
+        GLU_CUDA(launch_frame_prep(ctx, ctx->side, a, low, matte ? tgt : nullptr, packed, nanFlag),
+                 "upsample_frames");
+        GLU_CUDA(cudaEventRecord(prepped[b], ctx->side), "pipeline");
+        GLU_CUDA(cudaStreamWaitEvent(ctx->stream, prepped[b], 0), "pipeline");
+        GLU_CUDA(launch_prepped_solve32(ctx, a, packed, ctx->solver == 2, nanFlag),
+                 "upsample_frames");
+        GLU_CUDA(cudaEventRecord(solved[b], ctx->stream), "pipeline");
+    }
+    return GLU_OK;
+}
+
 int check_frames(glu_ctx* ctx, int count, const glu_grid* g, const glu_config* cfg, int mode,
                  int targetOp) {
     if (!ctx) return einval("ctx must not be null");
@@ -549,6 +605,8 @@ int glu_cu_upsample_frames(glu_ctx* ctx, const float* frames, int count, const g
     GLU_TRY(check_frames(ctx, count, g, cfg, mode, targetOp));
     const size_t n = npx_of(g), ln = lown_of(g);
     const int ch = targetOp == GLU_TARGET_MATTE ? 1 : 3;
+    if (count > 1 && ctx->solver != 1 && solve32_supported(mode, cfg->windowSide, g->scale))
+        return frames_pipelined(ctx, frames, count, g, cfg, mode, targetOp, out, paramsOut);
     float* low = dev<float>(ctx, S_LOW, ln * 3);
     float* tgt = dev<float>(ctx, S_AUX, ln);
     if (!low || !tgt) return GLU_ENOMEM;

@@ -29,6 +29,10 @@ struct glu_ctx {
     // Copy streams + events of the host frame pipeline (created lazily).
     cudaStream_t h2d = nullptr, d2h = nullptr;
     cudaEvent_t ev[8] = {};
+    // Side stream + events of the device frame pipeline (created lazily):
+    // frame k + 1's preparation overlaps frame k's solve.
+    cudaStream_t side = nullptr;
+    cudaEvent_t pev[5] = {};
     // Recorded on the previous stream when glu_ctx_set_stream switches
     // streams: the new stream waits on it, so work issued on different
     // streams never overlaps on the shared scratch slots / counters.
@@ -81,6 +85,12 @@ cudaError_t launch_solve32(glu_ctx* ctx, const SolveArgs& a, int forceFallback);
 // solve (a.lowT must already point at `low` or `matte`).
 cudaError_t launch_frame_solve32(glu_ctx* ctx, const SolveArgs& a, float* low, float* matte,
                                  int forceFallback);
+// The same split in two, for the multi-frame pipeline: k_frame_prep into the
+// given buffers on stream `st`, then the solve on ctx->stream.
+cudaError_t launch_frame_prep(glu_ctx* ctx, cudaStream_t st, const SolveArgs& a, float* low,
+                              float* matte, float4* packed, unsigned* nanFlag);
+cudaError_t launch_prepped_solve32(glu_ctx* ctx, const SolveArgs& a, const float4* packed,
+                                   int forceFallback, const unsigned* nanFlag);
 // glu_solve32f.cu: Fast, S = 3 (tile-staged, keyed closed-form stage B).
 bool solve32f_supported(int mode, int S);
 cudaError_t launch_solve32f(glu_ctx* ctx, const SolveArgs& a, const float4* packed,

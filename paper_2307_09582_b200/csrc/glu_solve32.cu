@@ -406,6 +406,24 @@ cudaError_t launch_solve32(glu_ctx* ctx, const SolveArgs& a0, int forceFallback)
     return dispatch(ctx, a, packed, forceFallback, nanFlag);
 }
 
+cudaError_t launch_frame_prep(glu_ctx* ctx, cudaStream_t st, const SolveArgs& a0, float* low,
+                              float* matte, float4* packed, unsigned* nanFlag) {
+    const SolveArgs a = prepared(a0);
+    const int h = a.S / 2;
+    const size_t cells = size_t(a.lw + 2 * h) * (a.lh + 2 * h);
+    cudaError_t e = cudaMemsetAsync(nanFlag, 0, sizeof(unsigned), st);
+    if (e != cudaSuccess) return e;
+    k_frame_prep<<<unsigned((cells + 255) / 256), 256, 0, st>>>(a.high, a.W, a.H, a.s, a.lw, a.lh,
+                                                                 h, low, packed, matte, nanFlag);
+    ++ctx->launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prepped_solve32(glu_ctx* ctx, const SolveArgs& a0, const float4* packed,
+                                   int forceFallback, const unsigned* nanFlag) {
+    return dispatch(ctx, prepared(a0), packed, forceFallback, nanFlag);
+}
+
 cudaError_t launch_frame_solve32(glu_ctx* ctx, const SolveArgs& a0, float* low, float* matte,
                                  int forceFallback) {
     const SolveArgs a = prepared(a0);
