@@ -516,6 +516,21 @@ def run_ours(args, ws, rank, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_value = ws * e2e_steps * px_step / e2e_s / 1e6
+    # the host link's own rate on the same buffers (plain pinned copies, one
+    # per direction at a time): the e2e path's roofline
+    def link_gbs(dst, src, nbytes):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(3):
+            dst.copy_(src, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        return 3 * nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    h2d_gbs = link_gbs(frames, pin_in.view(frames.shape), nf * W_ * H_ * 12)
+    d2h_gbs = link_gbs(pin_out, out, nf * W_ * H_ * 4)
+    link_floor_s = max(nf * W_ * H_ * 12 / (h2d_gbs * 1e9), nf * W_ * H_ * 4 / (d2h_gbs * 1e9))
     e2e_parity = bool(torch.equal(pin_out, out.cpu()))
 
     flops, nbytes = algorithmic_work(W_, H_, SCALE, 3, args.mode, 1)
@@ -661,6 +676,11 @@ def run_ours(args, ws, rank, local):
                     "h2d_bytes_per_step": nf * W_ * H_ * 12,
                     "d2h_bytes_per_step": nf * W_ * H_ * 4,
                     "api": "glu_h_upsample_frames (pinned host buffers)",
+                    "link_roofline": {"h2d_gbs": h2d_gbs, "d2h_gbs": d2h_gbs,
+                                      "floor_ms_per_step": link_floor_s * 1e3,
+                                      "frac": link_floor_s / (e2e_s / e2e_steps),
+                                      "basis": "pinned copies of the same bytes, one direction "
+                                               "at a time (the e2e overlaps both)"},
                     "parity_vs_device_path": e2e_parity},
             "gpu_launches": launches,
             "roofline": roofline,
