@@ -124,6 +124,64 @@ struct AboveThreshold {
     __device__ __forceinline__ bool operator()(const uint32_t& p) const { return e[p] > thr; }
 };
 
+// The selection of the mask pixels in raster order, in two passes over
+// chunks of kSelChunk pixels: k_sel_mask reads the error map once (float4
+// loads) and writes the chunk's mask as bits and its count; after an
+// exclusive scan of the counts, k_sel_write expands each chunk's bits into
+// pixel indices at the chunk's offset.  (CUB's DeviceSelect over a counting
+// iterator read the map with scalar loads: ~2.5x slower.)
+constexpr int kSelChunk = 4096, kSelThreads = 256;  // 16 pixels per thread
+constexpr int kSelWords = kSelChunk / 32;
+
+__global__ void __launch_bounds__(kSelThreads) k_sel_mask(const float* __restrict__ e, size_t npx,
+                                                          float thr, uint32_t* __restrict__ bits,
+                                                          uint32_t* __restrict__ counts) {
+    const size_t c0 = size_t(blockIdx.x) * kSelChunk;
+    const int lane = threadIdx.x & 31;
+    uint32_t cnt = 0;
+    const bool vec = (reinterpret_cast<uintptr_t>(e) & 15u) == 0;
+#pragma unroll
+    for (int k = 0; k < kSelChunk / (4 * kSelThreads); ++k) {
+        const int q = k * kSelThreads + threadIdx.x;  // quad of the chunk
+        const size_t p = c0 + 4 * size_t(q);
+        float v[4];
+        if (vec && p + 4 <= npx) {
+            const float4 f = __ldcs(reinterpret_cast<const float4*>(e + p));
+            v[0] = f.x, v[1] = f.y, v[2] = f.z, v[3] = f.w;
+        } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) v[c] = p + c < npx ? e[p + c] : thr;
+        }
+        uint32_t nib = 0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) nib |= uint32_t(v[c] > thr) << c;  // strict, NaN: no
+        cnt += __popc(nib);
+        // the word of quads 8j .. 8j + 7 (32 pixels): 8 lanes' nibbles
+        uint32_t w = nib << (4 * (lane & 7));
+        w |= __shfl_xor_sync(0xffffffffu, w, 1);
+        w |= __shfl_xor_sync(0xffffffffu, w, 2);
+        w |= __shfl_xor_sync(0xffffffffu, w, 4);
+        if ((lane & 7) == 0) bits[size_t(blockIdx.x) * kSelWords + q / 8] = w;
+    }
+    using BR = cub::BlockReduce<uint32_t, kSelThreads>;
+    __shared__ typename BR::TempStorage tmp;
+    const uint32_t total = BR(tmp).Sum(cnt);
+    if (threadIdx.x == 0) counts[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kSelWords) k_sel_write(const uint32_t* __restrict__ bits,
+                                                         const uint32_t* __restrict__ off,
+                                                         uint32_t* __restrict__ mp) {
+    using BS = cub::BlockScan<uint32_t, kSelWords>;
+    __shared__ typename BS::TempStorage tmp;
+    uint32_t w = bits[size_t(blockIdx.x) * kSelWords + threadIdx.x];
+    uint32_t pre;
+    BS(tmp).ExclusiveSum(uint32_t(__popc(w)), pre);
+    uint32_t* o = mp + off[blockIdx.x] + pre;
+    const uint32_t base = blockIdx.x * uint32_t(kSelChunk) + 32u * threadIdx.x;
+    for (; w; w &= w - 1) *o++ = base + uint32_t(__ffs(w) - 1);
+}
+
 __global__ void k_sparse_init(const uint32_t* __restrict__ mp, uint32_t m,
                               uint32_t* __restrict__ idx, uint32_t* __restrict__ parent) {
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -167,19 +225,35 @@ int ccl_sparse(glu_ctx* ctx, const float* errors, int W, int H, float thr, size_
     uint32_t* mp = static_cast<uint32_t*>(scratch(ctx, S_CCL_LIST, npx * 4 + 64));
     uint32_t* idx = static_cast<uint32_t*>(scratch(ctx, S_CCL_LABEL, npx * 4));
     if (!mp || !idx) return GLU_ENOMEM;
-    uint32_t* nsel = mp + npx;  // device counters
+    // selection: chunk masks + counts, scan, expansion (k_sel_mask / k_sel_write)
+    const size_t nch = (npx + kSelChunk - 1) / kSelChunk;
     size_t tbSel = 0;
-    const AboveThreshold pred{errors, thr};
-    thrust::counting_iterator<uint32_t> pix(0);
-    cub::DeviceSelect::If(nullptr, tbSel, pix, mp, nsel, int(npx), pred, st);
-    void* tsel = scratch(ctx, S_CCL_OFF, tbSel + 64);
-    if (!tsel) return GLU_ENOMEM;
-    cudaError_t e = cub::DeviceSelect::If(tsel, tbSel, pix, mp, nsel, int(npx), pred, st);
+    cub::DeviceScan::ExclusiveSum(nullptr, tbSel, static_cast<uint32_t*>(nullptr),
+                                  static_cast<uint32_t*>(nullptr), int(nch) + 1, st);
+    // bits (nch * kSelWords) | counts (nch + 1) | offsets (nch + 1) | scan temp
+    const size_t selWords = nch * kSelWords + 2 * (nch + 1);
+    char* sel = static_cast<char*>(scratch(ctx, S_CCL_OFF, selWords * 4 + 256 + tbSel));
+    if (!sel) return GLU_ENOMEM;
+    uint32_t* selBits = reinterpret_cast<uint32_t*>(sel);
+    uint32_t* cnts = selBits + nch * kSelWords;
+    uint32_t* coff = cnts + nch + 1;
+    void* tsel = sel + ((selWords * 4 + 255) & ~size_t(255));
+    cudaError_t e = cudaMemsetAsync(cnts + nch, 0, 4, st);
+    if (e == cudaSuccess) {
+        k_sel_mask<<<unsigned(nch), kSelThreads, 0, st>>>(errors, npx, thr, selBits, cnts);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess)
+        e = cub::DeviceScan::ExclusiveSum(tsel, tbSel, cnts, coff, int(nch) + 1, st);
+    if (e == cudaSuccess) {
+        k_sel_write<<<unsigned(nch), kSelWords, 0, st>>>(selBits, coff, mp);
+        e = cudaGetLastError();
+    }
     uint32_t m = 0;
-    if (e == cudaSuccess) e = cudaMemcpyAsync(&m, nsel, 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&m, coff + nch, 4, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return fail_cuda(e, "ccl select");
-    ctx->launches += 2;
+    ctx->launches += 4;
     // parent | isRoot | rank | keys | keys2 | vals2 (m words each)
     uint32_t* w = static_cast<uint32_t*>(scratch(ctx, S_CCL_MISC, size_t(m) * 24 + 64));
     if (!w) return GLU_ENOMEM;
