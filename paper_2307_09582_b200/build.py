@@ -7,6 +7,7 @@ Outputs (git-ignored, shipped to the GPU box with the working tree):
 """
 from __future__ import annotations
 
+import concurrent.futures
 import os
 import subprocess
 import sys
@@ -49,13 +50,17 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> None:
     hdrs += [os.path.join(INCLUDE, "glu_cuda.h")]
     srcs = [os.path.join(CSRC, f) for f in CUDA_SRCS if os.path.exists(os.path.join(CSRC, f))]
     if force or _stale(CUDA_SO, srcs + hdrs):
-        objs = []
+        objs, jobs = [], []
         for s in srcs:
             o = os.path.join(LIB, os.path.basename(s) + ".o")
             if force or _stale(o, [s] + hdrs):
-                _run([NVCC, *NVFLAGS, *(["-Xptxas", "-v"] if verbose_ptxas else []), "-c", s,
-                      "-o", o])
+                jobs.append([NVCC, *NVFLAGS, *(["-Xptxas", "-v"] if verbose_ptxas else []), "-c", s,
+                             "-o", o])
             objs.append(o)
+        # one nvcc per translation unit, in parallel
+        with concurrent.futures.ThreadPoolExecutor(max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+            for f in [ex.submit(_run, j) for j in jobs]:
+                f.result()
         _run([NVCC, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", CUDA_SO, *objs])
     api_srcs = [os.path.join(CSRC, "glu_api.cpp")]
     api_hdrs = [os.path.join(INCLUDE, "glu", f) for f in os.listdir(os.path.join(INCLUDE, "glu"))]

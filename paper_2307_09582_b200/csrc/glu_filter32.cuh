@@ -295,6 +295,8 @@ __device__ inline Filter32Result filter32k_pixel(const float4 (&c)[9], const flo
             }
         const float sb = __fadd_rn(at, f32_sqrt_approx(qb));
         const float m = fmaxf(mw, fmaxf(fabsf(ip0), fmaxf(fabsf(ip1), fabsf(ip2))));
+        // keys overflow beyond 2^29 (k_solve32f's kMaxMag): exact path
+        if (!(m < 536870912.0f)) return r;
         const float F = kF * __fmaf_rn(m, m, epsf);
         const float lim = K1 + __fmaf_rn(2.0f * G * qb, f32_rcp_approx(__fmul_rn(sb, sb)), F);
         if (K2 <= lim) {

@@ -57,6 +57,10 @@ constexpr float kCA = 32.0f;          // stage A relative margin (in u)
 constexpr float kG = 96.0f * kU;      // key offset, in u (A + B d_a)
 constexpr float kF = 5.684342e-14f;   // 2^-44
 constexpr float kInf = __builtin_huge_valf();
+// Stage B's fp32 keys stay finite while every |channel| of the pixel and its
+// tile is below 2^29 (A q_j and B d_j c_j <= 2 q_a q_j < 2^127); larger
+// values take the double path.
+constexpr float kMaxMag = 536870912.0f;
 
 __device__ __forceinline__ float rcp_approx(float x) {
     float r;
@@ -344,7 +348,7 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
         const float m = fmaxf(wM, fmaxf(fabsf(ip0), fmaxf(fabsf(ip1), fabsf(ip2))));
         const float F = kF * __fmaf_rn(m, m, eps);
         const float lim = K1 + __fmaf_rn(2.0f * G * qb, rcp_approx(__fmul_rn(sb, sb)), F);
-        if (!(K1 < kInf)) {
+        if (!(K1 < kInf) || !(m < kMaxMag)) {
             ok = false;
         } else if (K2 <= lim) {
             const CloseFast c = resolve_close_fast(swin, cw, ip0, ip1, ip2, at, b0, b1, b2, Ap, lim,

@@ -282,6 +282,12 @@ def _stress_images():
     yield "noise", rng.random((200, 320, 3), dtype=np.float32)
     yield "tiny", (rng.random((200, 320, 3)) * 1e-6).astype(np.float32)
     yield "two_level", (rng.random((200, 320, 1)) < 0.5).repeat(3, 2).astype(np.float32)
+    # magnitudes where the fp32 closed-form objective would overflow (products
+    # of two squared distances): the solve must fall back, not drop candidates
+    yield "huge", (base * 3e11).astype(np.float32)
+    spiky = base.copy()
+    spiky[rng.random((200, 320)) < 0.05] *= 1e15
+    yield "huge_spikes", spiky.astype(np.float32)
 
 
 @pytest.mark.parametrize("mode", ["fast", "gnu", "exact"])

@@ -64,6 +64,34 @@ def test_joint_with_nan_guide_pixels_matches_oracle(glu, oracle, mode):
     assert o["rejected"] > 0
 
 
+@pytest.mark.parametrize("mode", ["fast", "gnu", "exact"])
+def test_joint_with_huge_values_matches_oracle(glu, oracle, mode):
+    """Channels near 1e12: the fp32 closed-form objective of the Fast filters
+    (k_solve32f's stage B, the trials' filter32k_pixel) would overflow, so
+    those pixels must take the double path instead of losing candidates.
+    Every trial schedule against the oracle."""
+    from paper_2307_09582_b200 import workloads
+    rng = np.random.default_rng(11)
+    img = workloads.scene(160, 112, 23)
+    img[rng.random((112, 160)) < 0.03] *= 1e12
+    img = np.ascontiguousarray(img.astype(np.float32))
+    o = oracle.joint_optimize(img, 8, mode=mode)
+    ctx = glu.glu.context()
+    try:
+        for trials in (1, 0, 2):
+            ctx.set_trials(trials)
+            r = glu.joint_optimize(torch.from_numpy(img).cuda(), 8, None,
+                                   glu.mode_from_name(mode))
+            assert [r.iterations, r.trialsAccepted, r.trialsRejected] == \
+                [o["iterations"], o["accepted"], o["rejected"]], trials
+            assert r.low.cpu().numpy().tobytes() == o["low"].tobytes(), trials
+            assert _host_params(r.field.params).tobytes() == o["field"].tobytes(), trials
+            assert r.errors.cpu().numpy().tobytes() == o["errors"].tobytes(), trials
+    finally:
+        ctx.set_trials(0)
+    assert o["accepted"] + o["rejected"] > 0
+
+
 def test_one_context_many_streams(glu):
     """The per-device context's scratch (packed LR image, NaN flag, trial
     buffers) is shared by every stream it is bound to; binding a new stream
