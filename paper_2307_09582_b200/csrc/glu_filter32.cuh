@@ -358,6 +358,216 @@ __device__ inline Filter32Result filter32k_pixel(const float4 (&c)[9], const flo
     return r;
 }
 
+// ---- Fast / GNU, S = 3, reading the window from shared memory -----------------
+//
+// The trial re-solve's variant of k_solve32f's per-pixel solve (glu_solve32f.cu,
+// DESIGN.md section 3): the 3 x 3 window is read in place from the trial's
+// staged LR window (top-left cell `wv`, row pitch `pitch`; off-grid cells +inf,
+// .w = the cell's largest |channel|) instead of being copied into a register
+// array, so a, b and the winners' colours are single shared-memory loads (the
+// array version selected them with chains of FSELs).  Stage A: packed keys
+// (q_j with the index in the low 4 mantissa bits) and the exact 32u near-tie
+// check; stage B (Fast): the closed-form keys of k_solve32f; the weight by
+// weight_fast_lean.  `ok` false: the caller takes the exact double path.
+
+__device__ __forceinline__ int f32s_off(int j, int pitch) {
+    const int r = (j * 11) >> 5;  // j / 3 for j < 9
+    return r * pitch + (j - 3 * r);
+}
+
+__device__ __forceinline__ float f32s_q(float4 v, float ip0, float ip1, float ip2) {
+    const float d0 = v.x - ip0, d1 = v.y - ip1, d2 = v.z - ip2;
+    return __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmul_rn(d0, d0)));
+}
+
+__device__ __forceinline__ float f32s_max_nan(float a, float b) {  // NaN if either is NaN
+    float r;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
+
+// The stage-B key of candidate v (k_solve32f's fast_key): the packed
+// (B d_j c_j + (A - G) q_j) / s_j^2, (b0, b1, b2) = B e_a.
+__device__ __forceinline__ float f32s_key(float4 v, float ip0, float ip1, float ip2, float b0,
+                                          float b1, float b2, float at, float Ap, int j,
+                                          unsigned mask) {
+    const float e0 = v.x - ip0, e1 = v.y - ip1, e2 = v.z - ip2;
+    const float qj = __fmaf_rn(e2, e2, __fmaf_rn(e1, e1, __fmul_rn(e0, e0)));
+    const float bc = __fmaf_rn(e2, b2, __fmaf_rn(e1, b1, __fmul_rn(e0, b0)));
+    const float dj = f32_sqrt_approx(qj);
+    const float nl = __fmaf_rn(dj, bc, __fmul_rn(Ap, qj));
+    const float sj = __fadd_rn(at, dj);
+    const float t = __fmul_rn(nl, f32_rcp_approx(__fmul_rn(sj, sj)));
+    unsigned r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEC;" : "=r"(r) : "r"(__float_as_uint(t)), "r"(unsigned(j)),
+        "r"(mask));
+    return __uint_as_float(r);
+}
+
+// Stage-B close call (k_solve32f's resolve_close_fast): the candidates whose
+// key is within lim hold the reference's first argmin; all of the winner's
+// colour: the first of them, else settled in double in index order.  Returns
+// jb, or -1 (an off-grid member: the exact path), and the weight in *w when
+// settled in double (*wSet).
+__device__ __noinline__ int f32s_close(const float4* wv, int pitch, float ip0, float ip1, float ip2,
+                                       float at, float b0, float b1, float b2, float Ap, float lim,
+                                       unsigned kmask, int ja, int jb, double eps, float* w,
+                                       bool* wSet) {
+    const float4 ca = wv[f32s_off(ja, pitch)], cb = wv[f32s_off(jb, pitch)];
+    unsigned close = 0;
+    bool mixed = false;
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+        const float4 v = wv[f32s_off(j, pitch)];
+        if (f32s_key(v, ip0, ip1, ip2, b0, b1, b2, at, Ap, j, kmask) <= lim) {
+            if (!(f32s_q(v, ip0, ip1, ip2) < __builtin_huge_valf())) return -1;
+            close |= 1u << j;
+            mixed |= !(v.x == cb.x && v.y == cb.y && v.z == cb.z);
+        }
+    }
+    *wSet = false;
+    if (!mixed) return __ffs(close) - 1;  // identical colours: identical objectives
+    const float ip[3] = {ip0, ip1, ip2};
+    const float a3[3] = {ca.x, ca.y, ca.z};
+    const double dA = dist64(ip, a3);
+    double best = 0, bw = 0;
+    int bj = -1;
+    for (unsigned m = close; m; m &= m - 1) {
+        const int j = __ffs(m) - 1;
+        const float4 v = wv[f32s_off(j, pitch)];
+        const float cj[3] = {v.x, v.y, v.z};
+        const double dj = dist64(ip, cj);
+        const double wj = dj / (dA + dj + eps);
+        const double o = objective64(ip, a3, cj, wj, eps);
+        if (bj < 0 || o < best) {
+            best = o;
+            bw = wj;
+            bj = j;
+        }
+    }
+    *w = float(bw);
+    *wSet = true;
+    return bj;
+}
+
+__device__ __noinline__ float f32s_weight_ieee(float ip0, float ip1, float ip2, float4 ca,
+                                               float4 cb, double eps) {
+    const float ip[3] = {ip0, ip1, ip2};
+    const float a3[3] = {ca.x, ca.y, ca.z}, b3[3] = {cb.x, cb.y, cb.z};
+    const double dA = dist64(ip, a3), dB = dist64(ip, b3);
+    return float(dB / (dA + dB + eps));
+}
+
+template <bool GNU>
+__device__ __forceinline__ Filter32Result filter32_smem(const float4* wv, int pitch,
+                                                        const float* ip, float epsf, double eps) {
+    constexpr float kU = 5.9604645e-08f, kCA = 32.0f, kG = 96.0f * kU, kF = 5.684342e-14f;
+    constexpr float kInf = __builtin_huge_valf();
+    constexpr float kMaxMag = 536870912.0f;  // 2^29 (k_solve32f)
+    const float ip0 = ip[0], ip1 = ip[1], ip2 = ip[2];
+    const unsigned kmask = 0xfffffff0u | (__float_as_uint(epsf) >> 31);  // opaque: a register
+    Filter32Result r{false, 2, 0, 0, 1.0f};
+    // ---- stage A ----
+    float K1a = kInf, K2a = kInf, pa = 0.0f, nanq = 0.0f, mw = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+        const float4 v = wv[f32s_off(j, pitch)];
+        const float qq = f32s_q(v, ip0, ip1, ip2);
+        nanq = f32s_max_nan(nanq, qq);
+        mw = fmaxf(mw, v.w);
+        unsigned kb;
+        asm("lop3.b32 %0, %1, %2, %3, 0xEC;" : "=r"(kb) : "r"(__float_as_uint(qq)), "r"(unsigned(j)),
+            "r"(kmask));
+        const float key = __uint_as_float(kb);
+        if (j & 1)
+            f32x_track2(K1a, K2a, pa, key);
+        else if (j == 8)
+            f32x_track(K1a, K2a, key);
+        else
+            pa = key;
+    }
+    const int ja = int(__float_as_uint(K1a) & 15u);
+    const float4 ca = wv[f32s_off(ja, pitch)];
+    const float m1 = f32s_q(ca, ip0, ip1, ip2);
+    const bool exactA = ca.x == ip0 && ca.y == ip1 && ca.z == ip2;
+    // NaN colours (a NaN guide channel makes every key NaN: K1a stays +inf),
+    // underflow-sized distances: the exact path
+    if (nanq != nanq || !(K1a < kInf) || !(m1 >= 1e-27f || exactA)) return r;
+    r.why = 3;
+    // any other candidate within (1 + 32u) q_a has a key within K1a (1 + 128u)
+    if (K2a <= __fmaf_rn(K1a, 128.0f * kU, K1a) + 2e-36f) {
+        const float lim = __fmaf_rn(m1, kCA * kU, m1) + 1e-36f;
+#pragma unroll 1
+        for (int j = 0; j < 9; ++j) {
+            const float4 v = wv[f32s_off(j, pitch)];
+            if (j != ja && !(f32s_q(v, ip0, ip1, ip2) > lim) &&
+                !(v.x == ca.x && v.y == ca.y && v.z == ca.z))
+                return r;
+        }
+    }
+    r.ja = ja;
+    if (GNU) {  // b = a, w = 1 (upsample.cpp:93-104)
+        r.ok = true;
+        r.jb = ja;
+        r.w = 1.0f;
+        return r;
+    }
+    int jb = ja;
+    if (!exactA) {  // exact match I_a == I_p: b = a (the first exact zero), w = 0
+        const float eps32 = epsf;
+        const float da = f32_sqrt_approx(m1);
+        const float at = da + eps32;
+        const float A = __fadd_rn(__fmaf_rn(at, at, m1), eps32);
+        const float B = at + at;
+        const float G = kG * __fmaf_rn(B, da, A);
+        const float Ap = A - G;
+        const float b0 = B * (ca.x - ip0), b1 = B * (ca.y - ip1), b2 = B * (ca.z - ip2);
+        float K1 = kInf, K2 = kInf, pend = 0.0f;
+#pragma unroll
+        for (int j = 0; j < 9; ++j) {
+            const float key =
+                f32s_key(wv[f32s_off(j, pitch)], ip0, ip1, ip2, b0, b1, b2, at, Ap, j, kmask);
+            if (j & 1)
+                f32x_track2(K1, K2, pend, key);
+            else if (j == 8)
+                f32x_track(K1, K2, key);
+            else
+                pend = key;
+        }
+        jb = int(__float_as_uint(K1) & 15u);
+        const float4 cb = wv[f32s_off(jb, pitch)];
+        const float qb = f32s_q(cb, ip0, ip1, ip2);
+        const float sb = __fadd_rn(at, f32_sqrt_approx(qb));
+        const float m = fmaxf(mw, fmaxf(fabsf(ip0), fmaxf(fabsf(ip1), fabsf(ip2))));
+        const float F = kF * __fmaf_rn(m, m, eps32);
+        const float lim = K1 + __fmaf_rn(2.0f * G * qb, f32_rcp_approx(__fmul_rn(sb, sb)), F);
+        r.why = 4;
+        if (!(K1 < kInf) || !(m < kMaxMag)) return r;
+        if (K2 <= lim) {
+            float wc = 0.0f;
+            bool wSet = false;
+            jb = f32s_close(wv, pitch, ip0, ip1, ip2, at, b0, b1, b2, Ap, lim, kmask, ja, jb, eps,
+                            &wc, &wSet);
+            r.why = 5;
+            if (jb < 0) return r;
+            if (wSet) {
+                r.ok = true;
+                r.why = 6;
+                r.jb = jb;
+                r.w = wc;
+                return r;
+            }
+        }
+    }
+    const float4 cb = wv[f32s_off(jb, pitch)];
+    bool wok = false;
+    r.w = weight_fast_lean(ip0, ip1, ip2, ca, cb, eps, &wok);
+    if (!wok) r.w = f32s_weight_ieee(ip0, ip1, ip2, ca, cb, eps);
+    r.ok = true;
+    r.jb = jb;
+    return r;
+}
+
 __device__ inline Filter32Result filter32x_pixel(const float4 (&c)[9], const float* ip, float epsf,
                                                  double eps) {
     constexpr float kU = 5.9604645e-08f, kE = 64.0f * kU, kOneMinusE = 1.0f - kE;

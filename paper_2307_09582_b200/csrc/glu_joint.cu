@@ -791,16 +791,19 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
         if (t.S == 3) {
             // the window inside V (off-grid cells are the staged +inf cells)
             const float4* wv = ss.win + (cy - 1 - g.vy0) * g.vw + (cx - 1 - g.vx0);
-            float4 c[9];
+            Filter32Result fr;
+            if (t.mode == GLU_MODE_EXACT) {
+                float4 c[9];
 #pragma unroll
-            for (int k = 0; k < 9; ++k) c[k] = wv[(k / 3) * g.vw + k % 3];
-            const Filter32Result fr =
-                t.mode == GLU_MODE_EXACT
-                    ? filter32x_pixel(c, ip, float(t.eps), t.eps)
-                    : t.mode == GLU_MODE_GNU ? filter32_pixel(c, ip, float(t.eps), t.eps, true)
-                                             : filter32k_pixel(c, ip, float(t.eps), t.eps);
+                for (int k = 0; k < 9; ++k) c[k] = wv[(k / 3) * g.vw + k % 3];
+                fr = filter32x_pixel(c, ip, float(t.eps), t.eps);
+            } else if (t.mode == GLU_MODE_GNU) {
+                fr = filter32_smem<true>(wv, g.vw, ip, float(t.eps), t.eps);
+            } else {
+                fr = filter32_smem<false>(wv, g.vw, ip, float(t.eps), t.eps);
+            }
 #ifdef GLU_SCHED_TRACE
-            for (int k = 0; k < 9; ++k) c_dbg[k] = c[k];
+            for (int k = 0; k < 9; ++k) c_dbg[k] = wv[(k / 3) * g.vw + k % 3];
             if (fr.ok && fr.why == 6) atomicAdd(&g_phase[16], 1ull);
 #endif
             if (fr.ok) {

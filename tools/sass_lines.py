@@ -30,7 +30,7 @@ for l in open(dis):
     if m:
         cur = f"{m.group(1)}:{m.group(2)}"
         continue
-    m = re.match(r"\s*/\*[0-9a-f]{4}\*/\s+(.*?);", l)
+    m = re.match(r"\s*/\*[0-9a-f]{4,}\*/\s+(.*?);", l)
     if m:
         insts.append((cur, m.group(1).strip()))
 assert len(insts) == len(execd), (len(insts), len(execd))
