@@ -668,8 +668,19 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
         // conflicting successors among the next NT trials (loads overlap the
         // staging above)
         const int j = sc.self + 1 + tid;
-        if (j < sc.ncomp && boxes_conflict(sc.box, sc.boxes[j], sc.reach))
+        if (j < sc.ncomp && boxes_conflict(sc.box, sc.boxes[j], sc.reach)) {
             sc.list[atomicAdd(sc.count, 1)] = j;
+            // a successor waiting on this trial alone: speculate it now (valid
+            // iff this trial is rejected); the release pushes the others when
+            // their last predecessor is left
+            if (sc.specQ && uint32_t(ld_relaxed64(sc.pred + j)) == 1u &&
+                atomicCAS(sc.specState + j, 0, 7) == 0) {
+                st_release(sc.specQ + atomicAdd(sc.specTail, 1), j);
+#ifdef GLU_SCHED_TRACE
+                atomicAdd(&g_phase[19], 1ull);
+#endif
+            }
+        }
         if (tid == 0)
             *sc.more = sc.self + 1 + NT < sc.ncomp && sc.sufTop[sc.self + 1 + NT] <= sc.box.w + sc.reach;
     }
@@ -1184,18 +1195,101 @@ __global__ void __launch_bounds__(1024) k_suffix_top(const int4* __restrict__ bo
 }
 
 // pred[j] = number of earlier trials j conflicts with (one warp per trial i
-// walks its successors j > i).
+// walks its successors j > i); first[i] = i's first conflicting successor (-1:
+// none).
 __global__ void k_trial_preds(const int4* __restrict__ boxes, const int* __restrict__ sufTop,
-                              int n, int reach, unsigned long long* __restrict__ pred) {
+                              int n, int reach, unsigned long long* __restrict__ pred,
+                              int* __restrict__ first) {
     const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (i >= n) return;
     const int4 bi = boxes[i];
     const int lim = bi.w + reach;
+    int f = -1;
     for (int base = i + 1; base < n; base += 32) {
         if (sufTop[base] > lim) break;
         const int j = base + lane;
-        if (j < n && boxes_conflict(bi, boxes[j], reach)) atomicAdd(pred + j, 1ull);
+        const bool c = j < n && boxes_conflict(bi, boxes[j], reach);
+        if (c) atomicAdd(pred + j, 1ull);
+        const unsigned m = __ballot_sync(0xffffffffu, c);
+        if (f < 0 && m) f = base + __ffs(m) - 1;
     }
+    if (lane == 0) first[i] = f;
+}
+
+// Seeds ordered by priority (one CTA; n <= kPrioMax): trials with no earlier
+// conflict, longest chain first.  A trial's chain length L(i) = 1 + L(first[i])
+// -- the path through first successors, a lower bound of its height in the
+// conflict DAG that tracks it closely (C4: correlation 0.999 over the seeds) --
+// comes from pointer jumping in shared memory.  Index order (k_trial_seed)
+// started the C4 critical chain ~300 us late: CTAs keep to their own chains,
+// so a seed past the first grid-full waits for one to end.
+constexpr int kPrioMax = 12288;
+constexpr int kPrioPer = kPrioMax / 1024;
+constexpr int kPrioBuckets = 1024;
+__global__ void __launch_bounds__(1024) k_trial_seed_prio(const unsigned long long* __restrict__ pred,
+                                                          const int* __restrict__ first, int n,
+                                                          int* __restrict__ queue,
+                                                          int* __restrict__ qTail) {
+    extern __shared__ int dynp[];
+    int* len = dynp;
+    int* nxt = dynp + n;
+    __shared__ int hist[kPrioBuckets];
+    const int tid = threadIdx.x;
+    for (int i = tid; i < n; i += 1024) {
+        len[i] = 1;
+        nxt[i] = first[i];
+    }
+    for (int b = tid; b < kPrioBuckets; b += 1024) hist[b] = 0;
+    __syncthreads();
+    for (;;) {
+        int nl[kPrioPer], nn[kPrioPer];
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < kPrioPer; ++k) {
+            const int i = tid + 1024 * k;
+            nl[k] = 0;
+            nn[k] = -1;
+            if (i < n && nxt[i] >= 0) {
+                const int x = nxt[i];
+                nl[k] = len[i] + len[x];
+                nn[k] = nxt[x];
+                any = true;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kPrioPer; ++k) {
+            const int i = tid + 1024 * k;
+            if (i < n && nxt[i] >= 0) {
+                len[i] = nl[k];
+                nxt[i] = nn[k];
+            }
+        }
+        if (!__syncthreads_or(any)) break;
+    }
+    // counting sort of the seeds by descending L (clamped to the buckets)
+    int key[kPrioPer];
+#pragma unroll
+    for (int k = 0; k < kPrioPer; ++k) {
+        const int i = tid + 1024 * k;
+        key[k] = -1;
+        if (i < n && uint32_t(pred[i]) == 0u) {
+            key[k] = kPrioBuckets - 1 - min(len[i], kPrioBuckets - 1);
+            atomicAdd(hist + key[k], 1);
+        }
+    }
+    __syncthreads();
+    using Scan = cub::BlockScan<int, 1024>;
+    __shared__ typename Scan::TempStorage tmp;
+    int total = 0, pos = 0;
+    Scan(tmp).ExclusiveSum(hist[tid], pos, total);
+    __syncthreads();
+    hist[tid] = pos;
+    if (tid == 0) *qTail = total;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kPrioPer; ++k)
+        if (key[k] >= 0) queue[atomicAdd(hist + key[k], 1)] = tid + 1024 * k;
 }
 
 // Trials with no earlier conflict start ready, in index order within a warp.
@@ -1210,6 +1304,7 @@ __global__ void k_trial_seed(const unsigned long long* __restrict__ pred, int n,
     base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
     if (ready) queue[base + __popc(m & ((1u << lane) - 1))] = j;
 }
+
 
 // Persistent conflict-aware trial scheduler (see the file comment): a
 // dependency-counting dataflow schedule with speculation.
@@ -1619,7 +1714,7 @@ int run_sched(glu_ctx* ctx, const TrialState& t, const JointScratch& js, const g
     char* ctaBufs = static_cast<char*>(scratch(ctx, S_SCHED, per * grid));
     // boxes (int4) | pred (u64: accepted << 32 | unfinished) | counters (16) | sufTop |
     // queue | specState | specSnap | specQ | parkOff (n + 1)
-    char* meta = static_cast<char*>(scratch(ctx, S_SCHED_META, n * 48 + 128));
+    char* meta = static_cast<char*>(scratch(ctx, S_SCHED_META, n * 52 + 128));
     if (!ctaBufs || !meta) return GLU_ENOMEM;
     int4* boxes = reinterpret_cast<int4*>(meta);
     unsigned long long* pred = reinterpret_cast<unsigned long long*>(meta + n * 16);
@@ -1643,8 +1738,22 @@ int run_sched(glu_ctx* ctx, const TrialState& t, const JointScratch& js, const g
         off, px, ids, int(n), g.highW, g.scale, g.lowW, g.lowH, cfg.windowSide / 2,
         cfg.literalComponentUpdate, 0, boxes);
     k_suffix_top<<<1, 1024, 0, st>>>(boxes, int(n), sufTop);
-    k_trial_preds<<<blocks_for(n * 32, 256), 256, 0, st>>>(boxes, sufTop, int(n), reach, pred);
-    k_trial_seed<<<blocks_for(n, 256), 256, 0, st>>>(pred, int(n), queue, qTail);
+    int* first = reinterpret_cast<int*>(parkOff + n + 1);
+    k_trial_preds<<<blocks_for(n * 32, 256), 256, 0, st>>>(boxes, sufTop, int(n), reach, pred,
+                                                           first);
+#ifndef GLU_SEED_PRIO
+#define GLU_SEED_PRIO 1
+#endif
+    if (GLU_SEED_PRIO && n <= size_t(kPrioMax)) {
+        const int smemP = int(n) * 8;
+        // (static + dynamic shared memory above 48 KB needs the opt-in)
+        static const cudaError_t prioAttr = cudaFuncSetAttribute(
+            k_trial_seed_prio, cudaFuncAttributeMaxDynamicSharedMemorySize, kPrioMax * 8);
+        if (prioAttr != cudaSuccess) return fail_cuda(prioAttr, "trial schedule");
+        k_trial_seed_prio<<<1, 1024, smemP, st>>>(pred, first, int(n), queue, qTail);
+    } else {
+        k_trial_seed<<<blocks_for(n, 256), 256, 0, st>>>(pred, int(n), queue, qTail);
+    }
     ctx->launches += 4;
     uint32_t* parkBuf = nullptr;
     uint32_t parkCap = 0;
