@@ -117,19 +117,16 @@ __device__ __forceinline__ float weight_fast_verified(const float* ip, const flo
     r = __fma_rn(r, __fma_rn(-den, r, 1.0), r);
     const double q0 = db * r;
     const double wt = __fma_rn(__fma_rn(-den, q0, db), r, q0);
-    const float f = __double2float_rn(wt);
     if (db == 0.0) {  // 0 / den: exactly 0 on both sides
         *ok = true;
-        return f;
+        return 0.0f;
     }
-    const unsigned fb = __float_as_uint(f);
-    const int E = int((fb >> 23) & 0xffu) - 127;
-    const double g = wt - double(f);  // exact: same binade up to a factor 2
-    // distance from f to the rounding midpoint on g's side
-    const int he = (g < 0.0 && (fb & 0x7fffffu) == 0u) ? E - 25 : E - 24;
-    const double half = __longlong_as_double((long long)(he + 1023) << 52);
-    *ok = E > -100 && fabs(g) + 0x1.0p-48 * wt < half;
-    return f;
+    // the float rounding is settled when both ends of [wt (1 - 2^-48),
+    // wt (1 + 2^-48)] round alike (RN is monotone; see weight_fast_lean)
+    const float lo = __double2float_rn(__fma_rn(wt, -0x1.0p-48, wt));
+    const float hi = __double2float_rn(__fma_rn(wt, 0x1.0p-48, wt));
+    *ok = lo == hi && wt > 0x1.0p-100;
+    return lo;
 }
 // (float) of the reference's weight d_b / (d_a + d_b + eps) (upsample.cpp:61)
 // from a double estimate good to ~2^-42 (relative): the squared distances
@@ -162,15 +159,14 @@ __device__ __forceinline__ float weight_fast_lean(float ip0, float ip1, float ip
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(den));
     r = __fma_rn(r, __fma_rn(-den, r, 1.0), r);
     const double wt = db * r;
-    const float f = __double2float_rn(wt);
-    const unsigned fb = __float_as_uint(f);
-    const int E = int((fb >> 23) & 0xffu) - 127;
-    const double g = wt - double(f);  // exact: same binade up to a factor 2
-    // distance from f to the rounding midpoint on g's side
-    const int he = (g < 0.0 && (fb & 0x7fffffu) == 0u) ? E - 25 : E - 24;
-    const double half = __longlong_as_double((long long)(he + 1023) << 52);
-    *ok = E > -100 && fabs(g) + 0x1.0p-36 * wt < half;
-    return f;
+    // Every value within 2^-36 wt of the estimate has the same float rounding
+    // iff the interval's ends do (RN is monotone); that rounding is then the
+    // reference's.  (Replaced a midpoint-distance test: 13 -> 6 instructions,
+    // k_solve32f 0.1444 -> 0.1402 ms per fused 4K frame.)
+    const float lo = __double2float_rn(__fma_rn(wt, -0x1.0p-36, wt));
+    const float hi = __double2float_rn(__fma_rn(wt, 0x1.0p-36, wt));
+    *ok = lo == hi && wt > 0x1.0p-100;
+    return lo;
 }
 
 #endif
