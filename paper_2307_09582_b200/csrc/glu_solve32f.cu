@@ -264,8 +264,8 @@ __device__ __forceinline__ int pitch_of(const FTile& t) { return P > 0 ? P : t.c
 template <int MODE, int OUT, int P>
 __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* packed, const FTile& t,
                                             const float4* swin, float wM, int forceFallback,
-                                            size_t p, int cx, int cy, float ip0, float ip1,
-                                            float ip2) {
+                                            int x, int y, float ip0, float ip1, float ip2) {
+    const size_t p = size_t(y) * size_t(a.W) + size_t(x);
     const int cw = pitch_of<P>(t);
 
     // ---- stage A: a = first argmin |I_j - I_p| (compared as squares) -------
@@ -373,7 +373,8 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
         }
     } else {
         const uint3 r =
-            solve_double_fast<MODE>(packed, a.lw, a.lh, a.eps, a.fallbacks, cx, cy, ip0, ip1, ip2);
+            solve_double_fast<MODE>(packed, a.lw, a.lh, a.eps, a.fallbacks, div_s(x, a), div_s(y, a),
+                                    ip0, ip1, ip2);
         w = __uint_as_float(r.z);
         if (OUT == kOutApply1) {
             wa = __ldg(a.lowT + r.x);
@@ -515,23 +516,20 @@ __global__ void __launch_bounds__(kThreads, GLU_F_MIN_BLOCKS)
     const FTile t{wcells, cw, ocx0, ocy0};
     const int x = x0 + tx;
     if (x >= a.W) return;
-    const int cx = div_s(x, a);
     const int yr = y0 + ty * rows;
     const int yEnd = min(yr + rows, a.H);
     const float* g = gtile + (ty * rows) * 96 + 3 * tx;
-    size_t p = size_t(yr) * a.W + x;
     // owner-cell row of the current row, advanced when y reaches yNext
-    int cy = div_s(yr, a);
-    int yNext = (cy + 1) * a.s;
-    const float4* swin = wcells + (cy - ocy0) * cw + (cx - ocx0);
+    const int cy0 = div_s(yr, a);
+    int yNext = (cy0 + 1) * a.s;
+    const float4* swin = wcells + (cy0 - ocy0) * cw + (div_s(x, a) - ocx0);
 #pragma unroll 1
-    for (int y = yr; y < yEnd; ++y, g += 96, p += a.W) {
+    for (int y = yr; y < yEnd; ++y, g += 96) {
         if (y == yNext) {
-            ++cy;
             yNext += a.s;
             swin += cw;
         }
-        solve_pixel<MODE, OUT, P>(a, packed, t, swin, wM, forceFallback, p, cx, cy, g[0], g[1], g[2]);
+        solve_pixel<MODE, OUT, P>(a, packed, t, swin, wM, forceFallback, x, y, g[0], g[1], g[2]);
     }
 }
 
