@@ -122,3 +122,73 @@ def test_c3_frame_matches_reference(glu, reference, mode):
     f = glu.optimize_field(dev, lo, grid, None, md)
     gp = _host_params(f.params)
     assert _same(gp, field), _first_diff(gp, field)
+
+
+def test_beyond_4gib_image_sampled_rows(glu, oracle):
+    """A 20480 x 20480 guide (4.7 GiB of RGB fp32, 419 M pixels): byte offsets
+    pass 2^31 and 2^32, so every 32-bit index product in the solve, the apply
+    and the frame path would show.  grid_downsample is compared whole; the
+    solve (Fast), the RGB apply and the video path's fused solve + matte apply
+    on LR cell rows around both thresholds and at the edges, each against the
+    oracle on a crop of the cell row with its LR neighbours (a pixel's window
+    only reaches one LR row either side, so the crop solve is the full solve)."""
+    from oracle import low_dims
+    from paper_2307_09582_b200 import workloads
+    W = H = 20480
+    s = 16
+    img = workloads.scene(W, H, 41)
+    dev = torch.from_numpy(img).cuda()
+    low, grid = glu.grid_downsample(dev, s)
+    lo = low.cpu().numpy()
+    assert _same(lo, oracle.grid_downsample(img, s))
+    lw, lh = low_dims(W, H, s)
+    field = glu.optimize_field(dev, low, grid)
+    rec = glu.apply_field(field, low)
+    matte = glu.op_matte(low)
+    video = glu.glu.upsample_frames(dev[None], s, "matte")[0]
+    mat = matte.cpu().numpy()
+    # cell rows holding HR rows whose byte offsets cross 2^31 and 2^32
+    rows = sorted({0, (2**31 // 12) // W // s, (2**32 // 12) // W // s, lh // 2, lh - 1})
+    for cy in rows:
+        r0, r1 = max(0, cy - 1), min(lh, cy + 2)  # LR rows of the crop
+        y0, y1 = r0 * s, min(H, r1 * s)             # its HR rows
+        want = oracle.optimize_field(img[y0:y1], lo[r0:r1], s)
+        hy0, hy1 = cy * s - y0, min(H, cy * s + s) - y0  # the cell row inside the crop
+        want = want[hy0:hy1]
+        got = _host_params(field.params[cy * s:cy * s + (hy1 - hy0)])
+        shifted = want.copy()
+        shifted["a"] += np.uint32(r0 * lw)
+        shifted["b"] += np.uint32(r0 * lw)
+        assert _same(got, shifted), (cy, _first_diff(got, shifted))
+        ref_rgb = oracle.apply_field(want, lo[r0:r1])
+        assert _same(rec[cy * s:cy * s + (hy1 - hy0)].cpu().numpy(), ref_rgb), cy
+        ref_m = oracle.apply_field(want, np.repeat(mat[r0:r1, :, None], 3, axis=2))
+        assert _same(video[cy * s:cy * s + (hy1 - hy0)].cpu().numpy(),
+                     np.ascontiguousarray(ref_m[..., 0])), cy
+
+
+@pytest.mark.parametrize("mode", ["exact", "gnu"])
+def test_beyond_4gib_image_other_modes(glu, oracle, mode):
+    """The same 20480 x 20480 guide through optimize_field in Exact and GNU
+    mode (k_solve32x, k_solve32f<GNU>), checked on the LR cell row whose HR
+    byte offsets cross 2^32 and on the last one."""
+    from oracle import low_dims
+    from paper_2307_09582_b200 import workloads
+    W = H = 20480
+    s = 16
+    img = workloads.scene(W, H, 43)
+    dev = torch.from_numpy(img).cuda()
+    low, grid = glu.grid_downsample(dev, s)
+    lo = low.cpu().numpy()
+    lw, lh = low_dims(W, H, s)
+    field = glu.optimize_field(dev, low, grid, None, glu.mode_from_name(mode))
+    for cy in ((2**32 // 12) // W // s, lh - 1):
+        r0, r1 = max(0, cy - 1), min(lh, cy + 2)
+        y0, y1 = r0 * s, min(H, r1 * s)
+        want = oracle.optimize_field(img[y0:y1], lo[r0:r1], s, mode=mode)
+        hy0, hy1 = cy * s - y0, min(H, cy * s + s) - y0
+        want = want[hy0:hy1].copy()
+        want["a"] += np.uint32(r0 * lw)
+        want["b"] += np.uint32(r0 * lw)
+        got = _host_params(field.params[cy * s:cy * s + (hy1 - hy0)])
+        assert _same(got, want), (mode, cy, _first_diff(got, want))
