@@ -458,6 +458,60 @@ __device__ __noinline__ float f32s_weight_ieee(float ip0, float ip1, float ip2, 
     return float(dB / (dA + dB + eps));
 }
 
+// A trial's re-solve of a pixel whose a and b (slots sa, sb of its 3 x 3 window
+// `wv`) are not among the replaced cells (bits of `msk`): only the replaced
+// candidates changed, so the reference's new pick is the old one iff none of
+// them now beats it -- every replaced candidate strictly farther than a in
+// double (stage A; a tie in distance could move a to an earlier index) and,
+// in Fast mode unless I_a == I_p (b = a then), every replaced candidate's
+// objective strictly above b's (stage B: keys are lower bounds of the
+// reference's objectives, key_b + 2 G q_b / s_b^2 + F an upper bound of b's,
+// DESIGN.md section 3).  true: a, b and w are the reference's new ones, and
+// with a's and b's colours unchanged so is the error.  false: solve in full.
+template <bool GNU>
+__device__ __forceinline__ bool f32s_unchanged(const float4* wv, int pitch, const float* ip, int sa,
+                                               int sb, uint32_t msk, float epsf) {
+    constexpr float kU = 5.9604645e-08f, kCA = 32.0f, kG = 96.0f * kU, kF = 5.684342e-14f;
+    constexpr float kInf = __builtin_huge_valf();
+    constexpr float kMaxMag = 536870912.0f;  // 2^29 (k_solve32f)
+    const float ip0 = ip[0], ip1 = ip[1], ip2 = ip[2];
+    const float4 ca = wv[f32s_off(sa, pitch)];
+    const float qa = f32s_q(ca, ip0, ip1, ip2);
+    const bool exactA = ca.x == ip0 && ca.y == ip1 && ca.z == ip2;
+    if (!(qa >= 1e-27f || exactA)) return false;  // NaN, underflow-sized distances
+    const float thr = __fmaf_rn(qa, kCA * kU, qa) + 1e-36f;
+    float m = fmaxf(fmaxf(ca.w, fabsf(ip0)), fmaxf(fabsf(ip1), fabsf(ip2)));
+    for (uint32_t r = msk; r; r &= r - 1) {
+        const float4 v = wv[f32s_off(__ffs(r) - 1, pitch)];
+        if (!(f32s_q(v, ip0, ip1, ip2) > thr)) return false;
+        m = fmaxf(m, v.w);
+    }
+    if (GNU || exactA) return true;
+    const float4 cb = wv[f32s_off(sb, pitch)];
+    m = fmaxf(m, cb.w);
+    if (!(m < kMaxMag)) return false;
+    const unsigned kmask = 0xfffffff0u | (__float_as_uint(epsf) >> 31);  // opaque: a register
+    const float da = f32_sqrt_approx(qa);
+    const float at = da + epsf;
+    const float A = __fadd_rn(__fmaf_rn(at, at, qa), epsf);
+    const float B = at + at;
+    const float G = kG * __fmaf_rn(B, da, A);
+    const float Ap = A - G;
+    const float b0 = B * (ca.x - ip0), b1 = B * (ca.y - ip1), b2 = B * (ca.z - ip2);
+    const float kb = f32s_key(cb, ip0, ip1, ip2, b0, b1, b2, at, Ap, sb, kmask);
+    if (!(kb < kInf)) return false;
+    const float qb = f32s_q(cb, ip0, ip1, ip2);
+    const float sbb = __fadd_rn(at, f32_sqrt_approx(qb));
+    const float F = kF * __fmaf_rn(m, m, epsf);
+    const float lim = kb + __fmaf_rn(2.0f * G * qb, f32_rcp_approx(__fmul_rn(sbb, sbb)), F);
+    for (uint32_t r = msk; r; r &= r - 1) {
+        const int j = __ffs(r) - 1;
+        if (!(f32s_key(wv[f32s_off(j, pitch)], ip0, ip1, ip2, b0, b1, b2, at, Ap, j, kmask) > lim))
+            return false;
+    }
+    return true;
+}
+
 template <bool GNU>
 __device__ __forceinline__ Filter32Result filter32_smem(const float4* wv, int pitch,
                                                         const float* ip, float epsf, double eps) {

@@ -43,6 +43,9 @@ namespace {
 #ifndef GLU_SCHED_THREADS
 #define GLU_SCHED_THREADS 512
 #endif
+#ifndef GLU_TRIAL_INCR
+#define GLU_TRIAL_INCR 1  // trial re-solves keep provably unchanged pixels (Fast / GNU, S = 3)
+#endif
 constexpr int kSchedThreads = GLU_SCHED_THREADS;  // CTA size of the parallel trial scheduler
 // A scheduled trial can run on a cluster of kCS CTAs (one per SM): each CTA
 // stages the trial's window and offsets itself, the re-solve and the commit
@@ -92,7 +95,7 @@ __device__ __forceinline__ void cluster_bcast(T* var, T v) {
 // %globaltimer stamps, dumped by run_sched to $GLU_SCHED_TRACE_FILE, and SM
 // cycles per run_trial phase (thread 0, after the phase's barrier).
 __device__ unsigned long long* g_trace;
-__device__ unsigned long long g_phase[24];
+__device__ unsigned long long g_phase[26];
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long v;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
@@ -159,6 +162,7 @@ struct TrialSmem {
     double e0;
     int verdict;
     uint32_t logCells, logPixels;  // change-log bases of this trial
+    uint32_t nFull;                // run_trial_smem: pixels listed for a full re-solve
 };
 
 // One trial (jointopt.cpp:114-180) executed by the whole CTA.  Returns the
@@ -463,7 +467,7 @@ constexpr int kSS = kSchedThreads > 512 ? kSchedThreads : 512;  // successors fo
 constexpr uint32_t kParkWords = 128u << 20;  // speculative-record arena (512 MB)
 constexpr size_t kTrialSmemBytes = size_t(kSQ) * 8 + size_t(kSW) * 16 + size_t(kSC) * 16 +
                                    size_t(kSW + 1) * 4 + size_t(kSW) * 4 + size_t(kSQ) * 4 +
-                                   size_t(kSQ) * 12;
+                                   size_t(kSQ) * 12 + size_t(kSW) * 2;
 
 struct TrialShared {
     unsigned long long* key;  // [kSQ] worst-pixel key per box cell, 0: untouched
@@ -473,6 +477,7 @@ struct TrialShared {
     uint32_t* cellOf;         // [kSW] affected cells in order, (y << 16) | x
     uint32_t* touched;        // [kSQ] replaced cells (box-local index, raster order)
     float* old;               // [3 kSQ] their previous colours
+    uint16_t* rmask;          // [kSW] S = 3: replaced slots of each D cell's 3 x 3 window
     __device__ static TrialShared carve(char* base) {
         TrialShared s;
         s.key = reinterpret_cast<unsigned long long*>(base);
@@ -482,6 +487,7 @@ struct TrialShared {
         s.cellOf = s.pre + kSW + 1;
         s.touched = s.cellOf + kSW;
         s.old = reinterpret_cast<float*>(s.touched + kSQ);
+        s.rmask = reinterpret_cast<uint16_t*>(s.old + 3 * kSQ);
         return s;
     }
 };
@@ -616,6 +622,7 @@ struct PixIn {
     uint32_t p;
     int cx, cy;
     float oe, i0, i1, i2;
+    glu_pixel_params old;  // the current params (S = 3, Fast / GNU)
 };
 
 template <int NT>
@@ -687,8 +694,27 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
     __syncthreads();
     GLU_PHASE(0)
     // C. replace the touched cells; affected-pixel offsets over D (76-110)
+    // Fast / GNU at S = 3: a pixel whose a and b are not replaced keeps them
+    // when no replaced candidate provably beats them (f32s_unchanged).  Worth
+    // its extra pass from about three rounds of pixels per thread (C4: ~5;
+    // C2: ~1.3, where it measured slower); decided from the box geometry so
+    // the footprint scan below can record the replaced slots on the way.
+    const bool incr = t.S == 3 && t.mode != GLU_MODE_EXACT && GLU_TRIAL_INCR && kCS == 1 &&
+                      size_t(nd) * size_t(t.s) * size_t(t.s) > size_t(3 * NT);
     auto footprint = [&](int k) -> uint32_t {  // affected pixels of D cell k (0: not affected)
         const int x = g.dx0 + k % g.dw, y = g.dy0 + k / g.dw;
+        if (incr) {
+            // also which slots of the cell's 3 x 3 window hold a replaced cell
+            uint32_t m = 0;
+            for (int yy = max(y - 1, g.qy0); yy <= min(y + 1, g.qy0 + g.qh - 1); ++yy)
+                for (int xx = max(x - 1, g.qx0); xx <= min(x + 1, g.qx0 + g.qw - 1); ++xx)
+                    if (ss.key[(yy - g.qy0) * g.qw + (xx - g.qx0)])
+                        m |= 1u << ((yy - y + 1) * 3 + (xx - x + 1));
+            ss.rmask[k] = uint16_t(m);
+            return m ? uint32_t(min(x * t.s + t.s, t.W) - x * t.s) *
+                           uint32_t(min(y * t.s + t.s, t.H) - y * t.s)
+                     : 0u;
+        }
         for (int yy = max(y - h, g.qy0); yy <= min(y + h, g.qy0 + g.qh - 1); ++yy)
             for (int xx = max(x - h, g.qx0); xx <= min(x + h, g.qx0 + g.qw - 1); ++xx)
                 if (ss.key[(yy - g.qy0) * g.qw + (xx - g.qx0)])
@@ -763,7 +789,10 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
             __syncthreads();
         }
     }
-    if (tid == 0) ss.pre[nd] = na;
+    if (tid == 0) {
+        ss.pre[nd] = na;
+        sm.nFull = 0;
+    }
     __syncthreads();
     GLU_PHASE(2)
     // D. backup + e0, re-solve + e1 (jointopt.cpp:150-165, optimize_pixels 159).
@@ -776,21 +805,19 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
         q.i0 = t.high[3 * size_t(q.p)];
         q.i1 = t.high[3 * size_t(q.p) + 1];
         q.i2 = t.high[3 * size_t(q.p) + 2];
+        if (incr) q.old = t.field[q.p];
         return q;
     };
     constexpr uint32_t kStride = uint32_t(kCS) * NT;
-    PixIn cur{};
-    if (rank * NT + tid < na) cur = load(rank * NT + tid);
     double part0 = 0, part1 = 0;
     bool changed = false;
-    for (uint32_t i = rank * NT + tid; i < na; i += kStride) {
-        PixIn nxt{};
-        if (i + kStride < na) nxt = load(i + kStride);
-        const uint32_t p = cur.p;
-        const int cx = cur.cx, cy = cur.cy;
-        const float oe = cur.oe;
-        part0 += double(oe);
-        const float ip[3] = {cur.i0, cur.i1, cur.i2};
+    // the full re-solve of pixel i (its e0 term already summed): the fp32
+    // filter, else the exact double path; new params and error out, e1 term
+    auto solve_full = [&](uint32_t i, const PixIn& q) {
+        const uint32_t p = q.p;
+        const int cx = q.cx, cy = q.cy;
+        const float oe = q.oe;
+        const float ip[3] = {q.i0, q.i1, q.i2};
         const int x0 = max(0, cx - h), y0 = max(0, cy - h);
         const int nwx = min(t.lw - 1, cx + h) - x0 + 1, nwy = min(t.lh - 1, cy + h) - y0 + 1;
         int ax, ay, bx, by;
@@ -867,7 +894,75 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
             b.bkE[i] = e;
         changed |= __float_as_uint(e) != __float_as_uint(oe);
         part1 += double(e);
-        cur = nxt;
+    };
+    if (incr) {
+        // Pass 1: every pixel's unchanged test (cheap); the pixels that fail
+        // it are listed (this CTA's aff buffer) and re-solved in full in pass
+        // 2, so full solves fill whole warps instead of diverging from the
+        // ~90 % of pixels that keep their params (C4).
+        PixIn cur{};
+        if (tid < na) cur = load(tid);
+        for (uint32_t i = tid; i < na; i += NT) {
+            PixIn nxt{};
+            if (i + NT < na) nxt = load(i + NT);
+            const int cx = cur.cx, cy = cur.cy;
+            const float oe = cur.oe;
+            part0 += double(oe);
+            const float ip[3] = {cur.i0, cur.i1, cur.i2};
+            // slots of the current a and b in the window (both lie in it)
+            const uint32_t o = uint32_t(cy - 1) * uint32_t(t.lw) + uint32_t(cx - 1);
+            const uint32_t lw = uint32_t(t.lw);
+            auto slot = [&](uint32_t idx) {
+                const uint32_t d = idx - o;
+                const uint32_t r = d >= 2 * lw ? 2u : (d >= lw ? 1u : 0u);
+                return int(r * 3 + (d - r * lw));
+            };
+            const int sa = slot(cur.old.a), sb = slot(cur.old.b);
+            const uint32_t msk = ss.rmask[(cy - g.dy0) * g.dw + (cx - g.dx0)];
+            const float4* wv = ss.win + (cy - 1 - g.vy0) * g.vw + (cx - 1 - g.vx0);
+            if (!((msk >> sa) & 1u) && !((msk >> sb) & 1u) &&
+                (t.mode == GLU_MODE_GNU
+                     ? f32s_unchanged<true>(wv, g.vw, ip, sa, sb, msk, float(t.eps))
+                     : f32s_unchanged<false>(wv, g.vw, ip, sa, sb, msk, float(t.eps)))) {
+                // same a, b and w: the same params and, with a's and b's colours
+                // unchanged, the same error
+                if (parkPix) {
+                    uint32_t* op = parkPix + 5 * size_t(i);
+                    op[0] = cur.p;
+                    op[1] = cur.old.a;
+                    op[2] = cur.old.b;
+                    op[3] = __float_as_uint(cur.old.w);
+                    op[4] = __float_as_uint(oe);
+                } else {
+                    b.bkParams[i] = cur.old;
+                    b.bkE[i] = oe;
+                }
+                part1 += double(oe);
+#ifdef GLU_SCHED_TRACE
+                atomicAdd(&g_phase[24], 1ull);
+#endif
+            } else {
+                b.aff[atomicAdd(&sm.nFull, 1u)] = i;
+            }
+            cur = nxt;
+        }
+        __syncthreads();
+        const uint32_t nf = sm.nFull;
+        // Pass 2: the listed pixels' full re-solves
+        for (uint32_t k = tid; k < nf; k += NT) {
+            const uint32_t i = b.aff[k];
+            solve_full(i, load(i));
+        }
+    } else {
+        PixIn cur{};
+        if (rank * NT + tid < na) cur = load(rank * NT + tid);
+        for (uint32_t i = rank * NT + tid; i < na; i += kStride) {
+            PixIn nxt{};
+            if (i + kStride < na) nxt = load(i + kStride);
+            part0 += double(cur.oe);
+            solve_full(i, cur);
+            cur = nxt;
+        }
     }
     GLU_PHASE(4)
 #pragma unroll
@@ -1685,13 +1780,13 @@ void trace_end(glu_ctx* ctx, unsigned long long* trace, const int4* boxes, size_
             fclose(fp);
         }
     }
-    unsigned long long ph[24];
+    unsigned long long ph[26];
     cudaMemcpyFromSymbol(ph, g_phase, sizeof(ph));
-    const unsigned long long z[24] = {};
+    const unsigned long long z[26] = {};
     cudaMemcpyToSymbol(g_phase, z, sizeof(z));
     if (const char* f = getenv("GLU_SCHED_TRACE_FILE")) {
         if (FILE* fp = fopen((std::string(f) + ".phases").c_str(), "a")) {
-            for (int k = 0; k < 24; ++k) fprintf(fp, "%llu ", ph[k]);
+            for (int k = 0; k < 26; ++k) fprintf(fp, "%llu ", ph[k]);
             fprintf(fp, "%zu\n", n);
             fclose(fp);
         }

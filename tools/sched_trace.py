@@ -129,6 +129,9 @@ def show_phases(path):
         if len(v) > 24:
             print(f"   spec pushes at start {v[19]}, at release {v[20]}, pops {v[21]}, "
                   f"finalizer saw in-flight {v[22]}, still queued {v[23]}")
+        if len(v) > 25:
+            print(f"   re-solved pixels kept unchanged (incremental test) {v[24]} "
+                  f"({100.0 * v[24] / max(1, v[10] + v[24]):.1f} % of affected pixels)")
         if len(v) > 17:
             print("   fallback rule: nan %d, no-a/tiny %d, a-tie %d, zero-b %d, b-tie %d; "
                   "b close calls settled in double %d" % tuple(v[11:17]))
