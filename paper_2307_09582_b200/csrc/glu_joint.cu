@@ -1839,7 +1839,8 @@ int run_sched(glu_ctx* ctx, const TrialState& t, const JointScratch& js, const g
 #ifndef GLU_SEED_PRIO
 #define GLU_SEED_PRIO 1
 #endif
-    if (GLU_SEED_PRIO && n <= size_t(kPrioMax)) {
+    // (with no more trials than CTAs every seed starts at once: no order needed)
+    if (GLU_SEED_PRIO && n <= size_t(kPrioMax) && n > size_t(grid)) {
         const int smemP = int(n) * 8;
         // (static + dynamic shared memory above 48 KB needs the opt-in)
         static const cudaError_t prioAttr = cudaFuncSetAttribute(
