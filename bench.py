@@ -309,7 +309,8 @@ def run_c5(args, ws, rank, dist, hbm_gbs):
         "broadcast_bytes_per_target": grid.lowW * grid.lowH * 12 if ws > 1 else 0,
         "fused_operator": {"value": total_px / (ms_f * 1e-3) / 1e6, "ms_per_pass": ms_f,
                            "api": "glu_cu_apply_operator_field_band (no broadcast)"},
-        "apply_kernel": {"kernel": "k_op_pack_target4 + k_apply3v", "ms_mean": k_ms,
+        "apply_kernel": {"kernel": "k_op_pack_target4 + k_apply3b (bulk-copy tiles; k_apply3v for "
+                                   "a sub-tile tail)", "ms_mean": k_ms,
                          "algorithmic_bytes_per_launch": nbytes,
                          "hbm_gbs": nbytes / (k_ms * 1e-3) / 1e9,
                          "hbm_frac": nbytes / (k_ms * 1e-3) / 1e9 / hbm_gbs if hbm_gbs else None,
