@@ -449,3 +449,37 @@ def test_nonfinite_inputs_match_oracle(glu, oracle, S):
                 ctx.set_solver(0)
                 got = host_params(f.params)
                 assert same(got, want), (s, m, solver, int((got != want).sum()))
+
+
+@pytest.mark.parametrize("mode", ["fast", "gnu"])
+@pytest.mark.parametrize("image", ["scene", "quantised", "noise"])
+@pytest.mark.parametrize("s", [16, 12])
+def test_joint_unchanged_pixel_pass_matches_oracle(glu, oracle, mode, image, s):
+    """Scales where a trial's box spans about three rounds of pixels per CTA
+    thread, so the on-chip trials screen their affected pixels with the
+    unchanged-pixel certificate (f32s_unchanged) and re-solve the rest in a
+    compacted pass: every schedule against the oracle (itself pinned to the
+    reference) -- including quantised colours, whose exact distance ties must
+    fail the certificate and go to the full solve."""
+    from paper_2307_09582_b200 import workloads
+    W, H = 640, 480
+    img = workloads.scene(W, H, 57)
+    if image == "quantised":
+        img = (np.round(img * 4) / 4).astype(np.float32)
+    elif image == "noise":
+        img = np.random.default_rng(5).random((H, W, 3), dtype=np.float32)
+    img = np.ascontiguousarray(img)
+    o = oracle.joint_optimize(img, s, mode=mode)
+    ctx = glu.glu.context()
+    try:
+        for trials in (0, 2, 1):
+            ctx.set_trials(trials)
+            r = glu.joint_optimize(dev(img), s, None, mode_of(glu, mode))
+            assert [r.iterations, r.trialsAccepted, r.trialsRejected] == \
+                [o["iterations"], o["accepted"], o["rejected"]], trials
+            assert r.low.cpu().numpy().tobytes() == o["low"].tobytes(), trials
+            assert host_params(r.field.params).tobytes() == o["field"].tobytes(), trials
+            assert r.errors.cpu().numpy().tobytes() == o["errors"].tobytes(), trials
+    finally:
+        ctx.set_trials(0)
+    assert o["accepted"] + o["rejected"] > 0
