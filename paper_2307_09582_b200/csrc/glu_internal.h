@@ -7,6 +7,26 @@
 
 #include "glu_cuda.h"
 
+// Bounds / invariant checks of the device code, compiled in with
+// -DGLU_DEBUG_CHECKS (tools/debug_checks.sh): a failed check prints where and
+// traps, so the test that ran it fails loudly.  (compute-sanitizer is not
+// available on the GPU pool; this build stands in for its memcheck.)
+#ifdef GLU_DEBUG_CHECKS
+#include <cstdio>
+#define GLU_DCHECK(cond)                                                                     \
+    do {                                                                                     \
+        if (!(cond)) {                                                                       \
+            printf("GLU_DCHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__,    \
+                   __LINE__, int(blockIdx.x), int(threadIdx.x));                             \
+            __trap();                                                                        \
+        }                                                                                    \
+    } while (0)
+#else
+#define GLU_DCHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
+
 struct glu_ctx {
     int device = 0;
     cudaStream_t own = nullptr;

@@ -163,6 +163,7 @@ struct TrialSmem {
     int verdict;
     uint32_t logCells, logPixels;  // change-log bases of this trial
     uint32_t nFull;                // run_trial_smem: pixels listed for a full re-solve
+    uint32_t parkWords;            // the speculative record's capacity (GLU_DCHECK)
 };
 
 // One trial (jointopt.cpp:114-180) executed by the whole CTA.  Returns the
@@ -651,6 +652,9 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
     //    over ascending pixels = max of (E, -index) (jointopt.cpp:56-72,
     //    130-142).  Keys are zero on entry (the previous trial cleared them).
     const int nv = g.vw * g.vh, nq = g.qw * g.qh, nd = g.dw * g.dh;
+    GLU_DCHECK(nv <= kSW && nq <= kSQ && nd <= kSW && n <= uint32_t(kSC));
+    GLU_DCHECK(g.dx0 - g.vx0 >= h && g.dy0 - g.vy0 >= h &&
+               g.dx0 + g.dw + h <= g.vx0 + g.vw && g.dy0 + g.dh + h <= g.vy0 + g.vh);
     for (int k = tid; k < nv; k += NT) {
         const int y = g.vy0 + k / g.vw, x = g.vx0 + k % g.vw;
         if (x >= 0 && y >= 0 && x < t.lw && y < t.lh) {
@@ -676,13 +680,17 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
         // staging above)
         const int j = sc.self + 1 + tid;
         if (j < sc.ncomp && boxes_conflict(sc.box, sc.boxes[j], sc.reach)) {
-            sc.list[atomicAdd(sc.count, 1)] = j;
+            const int at = atomicAdd(sc.count, 1);
+            GLU_DCHECK(at < kSS);
+            sc.list[at] = j;
             // a successor waiting on this trial alone: speculate it now (valid
             // iff this trial is rejected); the release pushes the others when
             // their last predecessor is left
             if (sc.specQ && uint32_t(ld_relaxed64(sc.pred + j)) == 1u &&
                 atomicCAS(sc.specState + j, 0, 7) == 0) {
-                st_release(sc.specQ + atomicAdd(sc.specTail, 1), j);
+                const int at = atomicAdd(sc.specTail, 1);
+                GLU_DCHECK(at < sc.ncomp);
+                st_release(sc.specQ + at, j);
 #ifdef GLU_SCHED_TRACE
                 atomicAdd(&g_phase[19], 1ull);
 #endif
@@ -789,6 +797,7 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
             __syncthreads();
         }
     }
+    GLU_DCHECK(na <= kCtaPixels && nt <= uint32_t(kSQ));
     if (tid == 0) {
         ss.pre[nd] = na;
         sm.nFull = 0;
@@ -805,6 +814,8 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
         q.i0 = t.high[3 * size_t(q.p)];
         q.i1 = t.high[3 * size_t(q.p) + 1];
         q.i2 = t.high[3 * size_t(q.p) + 2];
+        GLU_DCHECK(q.cx >= g.dx0 && q.cx < g.dx0 + g.dw && q.cy >= g.dy0 && q.cy < g.dy0 + g.dh &&
+                   q.p < uint32_t(t.W) * uint32_t(t.H));
         if (incr) q.old = t.field[q.p];
         return q;
     };
@@ -918,6 +929,7 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
                 return int(r * 3 + (d - r * lw));
             };
             const int sa = slot(cur.old.a), sb = slot(cur.old.b);
+            GLU_DCHECK(sa >= 0 && sa < 9 && sb >= 0 && sb < 9);
             const uint32_t msk = ss.rmask[(cy - g.dy0) * g.dw + (cx - g.dx0)];
             const float4* wv = ss.win + (cy - 1 - g.vy0) * g.vw + (cx - 1 - g.vx0);
             if (!((msk >> sa) & 1u) && !((msk >> sb) & 1u) &&
@@ -942,7 +954,9 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
                 atomicAdd(&g_phase[24], 1ull);
 #endif
             } else {
-                b.aff[atomicAdd(&sm.nFull, 1u)] = i;
+                const uint32_t at = atomicAdd(&sm.nFull, 1u);
+                GLU_DCHECK(at < na);
+                b.aff[at] = i;
             }
             cur = nxt;
         }
@@ -1051,6 +1065,7 @@ __device__ int run_trial_smem(const TrialState& t, const TrialBuffers& b, TrialS
         sm.base = na;
     }
     if (park && rank == 0) {
+        GLU_DCHECK(3 + 5 * size_t(na) + 4 * size_t(nt) <= size_t(sm.parkWords));
         if (tid == 0) {
             park[0] = uint32_t(verdict);
             park[1] = nt;
@@ -1516,6 +1531,7 @@ __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
         cluster_barrier();
         const int i = sIdx, mode = sMode;
         if (mode == kExit) break;
+        GLU_DCHECK(i >= 0 && i < ncomp);
         __threadfence();  // acquire: the predecessors' committed writes are visible
         const int4 bi = boxes[i];
         const bool isBig = bi.x < 0;
@@ -1530,6 +1546,7 @@ __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
             if (threadIdx.x == 0) g_trace[3 * ncomp + 2 * i] = gtimer();
 #endif
             if (onChip) {
+                if (threadIdx.x == 0) sm.parkWords = parkOff[i + 1] - parkOff[i];
                 run_trial_smem<kSchedThreads>(t, local, sm, ss, geo, px + off[c], n, noScan,
                                               parkBuf + parkOff[i]);
 #ifdef GLU_SCHED_TRACE
@@ -1610,9 +1627,13 @@ __global__ void __launch_bounds__(kSchedThreads) k_trial_sched(
             const int left = int(uint32_t(atomicAdd(pred + j, delta)));
             if (left == 1 && atomicCAS(&sNext, -1, j) != -1) {
                 __threadfence();
-                st_release(queue + atomicAdd(qTail, 1), j);
+                const int at = atomicAdd(qTail, 1);
+                GLU_DCHECK(at < ncomp);
+                st_release(queue + at, j);
             } else if (left == 2 && spec && atomicCAS(specState + j, 0, 7) == 0) {
-                st_release(specQ + atomicAdd(specTail, 1), j);  // one predecessor to go
+                const int at = atomicAdd(specTail, 1);  // one predecessor to go
+                GLU_DCHECK(at < ncomp);
+                st_release(specQ + at, j);
 #ifdef GLU_SCHED_TRACE
                 atomicAdd(&g_phase[20], 1ull);
 #endif

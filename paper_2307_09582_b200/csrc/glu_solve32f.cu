@@ -472,6 +472,7 @@ __global__ void __launch_bounds__(kThreads, GLU_F_MIN_BLOCKS)
     const int ncw = div_s(min(x0 + kTX - 1, a.W - 1), a) - ocx0 + 1;
     const int nch = div_s(min(y0 + tileH - 1, a.H - 1), a) - ocy0 + 1;
     const int cw = P > 0 ? P : ncw + 2;
+    GLU_DCHECK(ncw + 2 <= cw && nch <= (kTY * rows - 1) / a.s + 2);
     // packed cell (c - 1) of the LR grid is at padded index c
     float m = 0.0f;
     for (int k = threadIdx.x; k < cw * (nch + 2); k += kThreads) {
@@ -529,6 +530,7 @@ __global__ void __launch_bounds__(kThreads, GLU_F_MIN_BLOCKS)
             yNext += a.s;
             swin += cw;
         }
+        GLU_DCHECK(swin - wcells >= 0 && swin - wcells + 2 * cw + 2 < cw * (nch + 2));
         solve_pixel<MODE, OUT, P>(a, packed, t, swin, wM, forceFallback, x, y, g[0], g[1], g[2]);
     }
 }
