@@ -19,4 +19,5 @@ echo "== debug-checks build: $(date)"
 python -m pytest tests -m gpu -q -p no:cacheprovider 2>&1 | tail -3
 for m in fast gnu exact; do python tools/bench_joint.py --config 2 4 --reps 1 --mode $m 2>&1 | grep -c '"config"'; done
 python tools/bench_joint.py --config 2 4 --reps 1 --trials 2 2>&1 | grep -c '"config"'
+python tools/sanitize_joint.py --size 2048 2>&1 | tail -1
 cp /tmp/glu_release/* $L/

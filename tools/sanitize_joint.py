@@ -1,5 +1,7 @@
-"""Run the joint loop (every trial schedule) and the C3 solve kernels once, for
-compute-sanitizer (one tool per gpurun call):
+"""Run the joint loop (every trial schedule) and the C3 solve kernels once, as
+a checking workload: under the -DGLU_DEBUG_CHECKS build (tools/debug_checks.sh)
+or, where a pool allows it, compute-sanitizer (one tool per call; the B200
+pool used for this repo has it closed):
 
     compute-sanitizer --tool memcheck python tools/sanitize_joint.py --size 2048
     compute-sanitizer --tool racecheck python tools/sanitize_joint.py --size 384
