@@ -458,9 +458,15 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS)
     const int tj = pr - (ti * 8 - ti * (ti - 1) / 2) + ti + 1;
     const int oi = (ti / 3) * cw + ti % 3, oj = (tj / 3) * cw + tj % 3;
     constexpr int kCellStep = kThreads / kPairs;  // cells per pass (the last threads idle)
+    // (cell -> (ly, lx) advanced incrementally: kCellStep < ncw or one row step
+    // at a time, no division per cell)
+    int ly = 0, lx = int(threadIdx.x) / kPairs;
+    while (lx >= ncw) {
+        lx -= ncw;
+        ++ly;
+    }
     for (int cell = int(threadIdx.x) / kPairs; cell < ncw * nch && threadIdx.x < kCellStep * kPairs;
          cell += kCellStep) {
-        const int ly = cell / ncw, lx = cell - ly * ncw;
         const float4* w = wcells + ly * cw + lx;
         const float4 ci = w[oi], cj = w[oj];
         const float d0 = ci.x - cj.x, d1 = ci.y - cj.y, d2 = ci.z - cj.z;
@@ -468,6 +474,11 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS)
         // D' = D / sqrt(den): then obj_ij = q_j - (e_j . D')^2
         const float r = rsqrt_approx(den);
         table[cell * kCellStride + pr] = make_float4(d0 * r, d1 * r, d2 * r, 0.0f);
+        lx += kCellStep;
+        while (lx >= ncw) {
+            lx -= ncw;
+            ++ly;
+        }
     }
     __syncthreads();
     if (useTma) {
