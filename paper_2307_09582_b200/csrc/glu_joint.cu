@@ -1863,8 +1863,9 @@ int run_sched(glu_ctx* ctx, const TrialState& t, const JointScratch& js, const g
     // (with no more trials than CTAs every seed starts at once: no order needed)
     if (GLU_SEED_PRIO && n <= size_t(kPrioMax) && n > size_t(grid)) {
         const int smemP = int(n) * 8;
-        // (static + dynamic shared memory above 48 KB needs the opt-in)
-        static const cudaError_t prioAttr = cudaFuncSetAttribute(
+        // (static + dynamic shared memory above 48 KB needs the opt-in; a
+        // function attribute is per device, so set on every call)
+        const cudaError_t prioAttr = cudaFuncSetAttribute(
             k_trial_seed_prio, cudaFuncAttributeMaxDynamicSharedMemorySize, kPrioMax * 8);
         if (prioAttr != cudaSuccess) return fail_cuda(prioAttr, "trial schedule");
         k_trial_seed_prio<<<1, 1024, smemP, st>>>(pred, first, int(n), queue, qTail);
