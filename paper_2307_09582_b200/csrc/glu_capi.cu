@@ -534,6 +534,10 @@ int frame_kernels(glu_ctx* ctx, const float* frame, const glu_grid* g, const glu
 // side stream into buffer set k % 2 while frame k - 1 is solved on the
 // context stream (the prep is a small grid: it fills the solve's last wave).
 // Prep k waits for solve k - 2 (its buffers); solve k waits for prep k.
+#ifndef GLU_FRAME_BATCH
+#define GLU_FRAME_BATCH 1
+#endif
+
 int frames_pipelined(glu_ctx* ctx, const float* frames, int count, const glu_grid* g,
                      const glu_config* cfg, int mode, int targetOp, float* out,
                      glu_pixel_params* paramsOut) {
@@ -583,6 +587,65 @@ int frames_pipelined(glu_ctx* ctx, const float* frames, int count, const glu_gri
     return GLU_OK;
 }
 
+// Fast / GNU, S = 3, matte target, no params: the frames go through
+// k_solve32f in batches of up to kFrameBatch per launch (grid z = frame), so
+// the SMs never drain between frames; one batched prep launch per batch, the
+// next batch's on the side stream while this one solves.
+constexpr int kFrameBatch = 16;
+
+int frames_batched(glu_ctx* ctx, const float* frames, int count, const glu_grid* g,
+                   const glu_config* cfg, int mode, float* out) {
+    const size_t n = npx_of(g), ln = lown_of(g);
+    const int h = cfg->windowSide / 2;
+    const size_t cells = size_t(g->lowW + 2 * h) * (g->lowH + 2 * h);
+    // per frame: low (3 ln floats) | matte (ln floats) | packed (cells float4)
+    const size_t offMatte = (ln * 12 + 255) & ~size_t(255);
+    const size_t offPacked = offMatte + ((ln * 4 + 255) & ~size_t(255));
+    const size_t set = (offPacked + cells * 16 + 255) & ~size_t(255);
+    const int B = std::min(count, kFrameBatch);
+    char* base = static_cast<char*>(scratch(ctx, S_SPARE2, 2 * size_t(B) * set + 2 * B * 4 + 64));
+    if (!base) return GLU_ENOMEM;
+    unsigned* flagBase = reinterpret_cast<unsigned*>(base + 2 * size_t(B) * set);
+    if (!ctx->side) {
+        GLU_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking), "stream");
+        for (cudaEvent_t& ev : ctx->pev)
+            GLU_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+    }
+    cudaEvent_t* prepped = ctx->pev;     // [2] per batch buffer group
+    cudaEvent_t* solved = ctx->pev + 2;  // [2]
+    GLU_CUDA(cudaEventRecord(ctx->pev[4], ctx->stream), "pipeline");
+    GLU_CUDA(cudaStreamWaitEvent(ctx->side, ctx->pev[4], 0), "pipeline");
+    for (int k0 = 0, bi = 0; k0 < count; k0 += B, ++bi) {
+        const int nb = std::min(B, count - k0), grp = bi & 1;
+        char* gb = base + size_t(grp) * B * set;
+        unsigned* flags = flagBase + grp * B;
+        SolveArgs a = solve_args(frames + size_t(k0) * n * 3, reinterpret_cast<float*>(gb), g,
+                                 cfg, mode);
+        a.params = nullptr;
+        a.lowT = reinterpret_cast<float*>(gb + offMatte);
+        a.channels = 1;
+        a.clamp = 1;
+        a.out = out + size_t(k0) * n;
+        a.fallbacks = ctx->d_counters;
+        FrameBatch fb;
+        fb.frames = nb;
+        fb.high = n * 3;
+        fb.px = n;
+        fb.lowT = set / 4;
+        fb.packed = set / 16;
+        if (bi >= 2) GLU_CUDA(cudaStreamWaitEvent(ctx->side, solved[grp], 0), "pipeline");
+        GLU_CUDA(launch_frame_prep_batch(ctx, ctx->side, a, fb, gb, set, offMatte, offPacked, flags),
+                 "upsample_frames");
+        GLU_CUDA(cudaEventRecord(prepped[grp], ctx->side), "pipeline");
+        GLU_CUDA(cudaStreamWaitEvent(ctx->stream, prepped[grp], 0), "pipeline");
+        GLU_CUDA(launch_prepped_solve32f_batch(ctx, a, reinterpret_cast<float4*>(gb + offPacked),
+                                               ctx->solver == 2, flags, fb),
+                 "upsample_frames");
+        GLU_CUDA(cudaEventRecord(solved[grp], ctx->stream), "pipeline");
+    }
+    return GLU_OK;
+}
+
 int check_frames(glu_ctx* ctx, int count, const glu_grid* g, const glu_config* cfg, int mode,
                  int targetOp) {
     if (!ctx) return einval("ctx must not be null");
@@ -605,6 +668,9 @@ int glu_cu_upsample_frames(glu_ctx* ctx, const float* frames, int count, const g
     GLU_TRY(check_frames(ctx, count, g, cfg, mode, targetOp));
     const size_t n = npx_of(g), ln = lown_of(g);
     const int ch = targetOp == GLU_TARGET_MATTE ? 1 : 3;
+    if (count > 1 && ctx->solver != 1 && !paramsOut && targetOp == GLU_TARGET_MATTE &&
+        solve32f_supported(mode, cfg->windowSide) && GLU_FRAME_BATCH)
+        return frames_batched(ctx, frames, count, g, cfg, mode, out);
     if (count > 1 && ctx->solver != 1 && solve32_supported(mode, cfg->windowSide, g->scale))
         return frames_pipelined(ctx, frames, count, g, cfg, mode, targetOp, out, paramsOut);
     float* low = dev<float>(ctx, S_LOW, ln * 3);

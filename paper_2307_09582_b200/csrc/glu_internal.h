@@ -111,10 +111,29 @@ cudaError_t launch_frame_prep(glu_ctx* ctx, cudaStream_t st, const SolveArgs& a,
                               float* matte, float4* packed, unsigned* nanFlag);
 cudaError_t launch_prepped_solve32(glu_ctx* ctx, const SolveArgs& a, const float4* packed,
                                    int forceFallback, const unsigned* nanFlag);
+// A batch of video frames in ONE solve launch (glu_cu_upsample_frames, 1-ch
+// matte target): frame f = blockIdx.z reads the guide at high + f * high,
+// its packed LR at packed + f * packed, its NaN flag at nanFlag[f] and its
+// target at lowT + f * lowT, and writes out + f * px.  frames = 1: one frame.
+struct FrameBatch {
+    int frames = 1;
+    size_t high = 0, px = 0, lowT = 0, packed = 0;
+};
 // glu_solve32f.cu: Fast, S = 3 (tile-staged, keyed closed-form stage B).
 bool solve32f_supported(int mode, int S);
 cudaError_t launch_solve32f(glu_ctx* ctx, const SolveArgs& a, const float4* packed,
-                            int forceFallback, const unsigned* nanFlag);
+                            int forceFallback, const unsigned* nanFlag,
+                            const FrameBatch& fb = FrameBatch{});
+// k_frame_prep for fb.frames frames in one launch (frame f: the guide at
+// a.high + f * fb.high; low / matte / packed / flag at their bases + f * the
+// set stride `set` bytes), on stream st.
+cudaError_t launch_frame_prep_batch(glu_ctx* ctx, cudaStream_t st, const SolveArgs& a,
+                                    const FrameBatch& fb, char* base, size_t set,
+                                    size_t offMatte, size_t offPacked, unsigned* flags);
+// The batch's solve (k_solve32f over fb.frames frames; a = frame 0's args).
+cudaError_t launch_prepped_solve32f_batch(glu_ctx* ctx, const SolveArgs& a, const float4* packed,
+                                          int forceFallback, const unsigned* flags,
+                                          const FrameBatch& fb);
 bool solve32x_supported(int mode, int S, int s);
 cudaError_t launch_solve32x(glu_ctx* ctx, const SolveArgs& a, const float4* packed,
                             int forceFallback, const unsigned* nanFlag);

@@ -389,7 +389,53 @@ __global__ void k_frame_prep(const float* __restrict__ high, int W, int H, int s
     packed[i] = v;
 }
 
+// k_frame_prep over a batch of frames: frame blockIdx.y; its buffers live in
+// one set per frame (low at +0, matte at +offMatte, packed at +offPacked).
+__global__ void k_frame_prep_batch(const float* __restrict__ high, size_t highStride, int W, int H,
+                                   int s, int lw, int lh, int h, char* base, size_t set,
+                                   size_t offMatte, size_t offPacked, unsigned* flags) {
+    const int f = blockIdx.y;
+    char* b = base + size_t(f) * set;
+    const int pw = lw + 2 * h, ph = lh + 2 * h;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= pw * ph) return;
+    const float* hf = high + size_t(f) * highStride;
+    float* low = reinterpret_cast<float*>(b);
+    float* matte = reinterpret_cast<float*>(b + offMatte);
+    float4* packed = reinterpret_cast<float4*>(b + offPacked);
+    const int cy = i / pw - h, cx = i % pw - h;
+    float4 v = make_float4(kInf, kInf, kInf, 0.0f);
+    if (cx >= 0 && cy >= 0 && cx < lw && cy < lh) {
+        const int x = min(cx * s + s / 2, W - 1), y = min(cy * s + s / 2, H - 1);
+        const float* src = hf + 3 * (size_t(y) * W + x);
+        v = make_float4(src[0], src[1], src[2],
+                        fmaxf(fabsf(src[0]), fmaxf(fabsf(src[1]), fabsf(src[2]))));
+        const size_t c = size_t(cy) * lw + cx;
+        low[3 * c] = v.x;
+        low[3 * c + 1] = v.y;
+        low[3 * c + 2] = v.z;
+        const double Y = 0.299 * v.x + 0.587 * v.y + 0.114 * v.z;
+        matte[c] = float(1.0 / (1.0 + exp(-10.0 * (Y - 0.5))));
+        if (v.x != v.x || v.y != v.y || v.z != v.z) atomicOr(flags + f, 1u);
+    }
+    packed[i] = v;
+}
+
 }  // namespace
+
+cudaError_t launch_frame_prep_batch(glu_ctx* ctx, cudaStream_t st, const SolveArgs& a0,
+                                    const FrameBatch& fb, char* base, size_t set,
+                                    size_t offMatte, size_t offPacked, unsigned* flags) {
+    const SolveArgs a = prepared(a0);
+    const int h = a.S / 2;
+    const size_t cells = size_t(a.lw + 2 * h) * (a.lh + 2 * h);
+    cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(unsigned) * size_t(fb.frames), st);
+    if (e != cudaSuccess) return e;
+    k_frame_prep_batch<<<dim3(unsigned((cells + 255) / 256), unsigned(fb.frames)), 256, 0, st>>>(
+        a.high, fb.high, a.W, a.H, a.s, a.lw, a.lh, h, base, set, offMatte, offPacked, flags);
+    ++ctx->launches;
+    return cudaGetLastError();
+}
 
 cudaError_t launch_solve32(glu_ctx* ctx, const SolveArgs& a0, int forceFallback) {
     const SolveArgs a = prepared(a0);
@@ -422,6 +468,12 @@ cudaError_t launch_frame_prep(glu_ctx* ctx, cudaStream_t st, const SolveArgs& a0
 cudaError_t launch_prepped_solve32(glu_ctx* ctx, const SolveArgs& a0, const float4* packed,
                                    int forceFallback, const unsigned* nanFlag) {
     return dispatch(ctx, prepared(a0), packed, forceFallback, nanFlag);
+}
+
+cudaError_t launch_prepped_solve32f_batch(glu_ctx* ctx, const SolveArgs& a0, const float4* packed,
+                                          int forceFallback, const unsigned* flags,
+                                          const FrameBatch& fb) {
+    return launch_solve32f(ctx, prepared(a0), packed, forceFallback, flags, fb);
 }
 
 cudaError_t launch_frame_solve32(glu_ctx* ctx, const SolveArgs& a0, float* low, float* matte,

@@ -264,8 +264,10 @@ __device__ __forceinline__ int pitch_of(const FTile& t) { return P > 0 ? P : t.c
 template <int MODE, int OUT, int P>
 __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* packed, const FTile& t,
                                             const float4* swin, float wM, int forceFallback,
-                                            int x, int y, float ip0, float ip1, float ip2) {
-    const size_t p = size_t(y) * size_t(a.W) + size_t(x);
+                                            int x, int y, float ip0, float ip1, float ip2,
+                                            size_t fo, size_t th) {
+    // (fo / th: this frame's output / target offsets in a batched launch)
+    const size_t p = size_t(y) * size_t(a.W) + size_t(x) + fo;
     const int cw = pitch_of<P>(t);
 
     // ---- stage A: a = first argmin |I_j - I_p| (compared as squares) -------
@@ -377,8 +379,8 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
                                     ip0, ip1, ip2);
         w = __uint_as_float(r.z);
         if (OUT == kOutApply1) {
-            wa = __ldg(a.lowT + r.x);
-            wb = __ldg(a.lowT + r.y);
+            wa = __ldg(a.lowT + th + r.x);
+            wb = __ldg(a.lowT + th + r.y);
         } else {
             wa = __uint_as_float(r.x);
             wb = __uint_as_float(r.y);
@@ -411,12 +413,12 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
         if (a.lowT) {
             const bool clamp = a.clamp != 0;
             if (a.channels == 1) {
-                a.out[p] = lerp_clamp(w, __ldg(a.lowT + ia), __ldg(a.lowT + ib), clamp);
+                a.out[p] = lerp_clamp(w, __ldg(a.lowT + th + ia), __ldg(a.lowT + th + ib), clamp);
             } else {
 #pragma unroll
                 for (int k = 0; k < 3; ++k)
-                    a.out[3 * p + k] = lerp_clamp(w, __ldg(a.lowT + 3 * size_t(ia) + k),
-                                                  __ldg(a.lowT + 3 * size_t(ib) + k), clamp);
+                    a.out[3 * p + k] = lerp_clamp(w, __ldg(a.lowT + th + 3 * size_t(ia) + k),
+                                                  __ldg(a.lowT + th + 3 * size_t(ib) + k), clamp);
             }
         }
         if (a.errOut) {  // pixel_error of the clamped self reconstruction (jointopt.cpp:190)
@@ -442,10 +444,19 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 // Dynamic shared memory: [guide: tileH x 96 floats][cells: P x (nch + 2)].
 // `tmap` is a 2-D tensor map of the guide (3 W floats x H rows, box 96 x
 // tileH) when useTma != 0.
-template <int MODE, int OUT, int P>
+template <int MODE, int OUT, int P, bool BATCH>
 __global__ void __launch_bounds__(kThreads, GLU_F_MIN_BLOCKS)
     k_solve32f(const __grid_constant__ CUtensorMap tmap, SolveArgs a, const float4* packed,
-               int forceFallback, const unsigned* nanFlag, int rows, int useTma) {
+               int forceFallback, const unsigned* nanFlag, int rows, int useTma, FrameBatch fb) {
+    // BATCH: frame blockIdx.z of a batch of frames (glu_cu_upsample_frames);
+    // the single-frame instantiation compiles the offsets out
+    const int fz = BATCH ? int(blockIdx.z) : 0;
+    if (BATCH) {
+        packed += size_t(fz) * fb.packed;
+        nanFlag += fz;
+    }
+    const size_t fo = BATCH ? size_t(fz) * fb.px : 0, th = BATCH ? size_t(fz) * fb.lowT : 0,
+                 hh = BATCH ? size_t(fz) * fb.high : 0;
     extern __shared__ __align__(1024) float smem[];
     __shared__ __align__(8) unsigned long long bar;
     __shared__ float warpMax[kTY];
@@ -460,11 +471,19 @@ __global__ void __launch_bounds__(kThreads, GLU_F_MIN_BLOCKS)
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)),
                      "r"(unsigned(tileH * 96 * 4))
                      : "memory");
-        asm volatile(
-            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-            " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(gtile)),
-            "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(3 * x0), "r"(y0), "r"(smem_u32(&bar))
-            : "memory");
+        if (BATCH)  // a 3-D map over the batch's frames
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(gtile)),
+                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(3 * x0), "r"(y0), "r"(fz),
+                "r"(smem_u32(&bar))
+                : "memory");
+        else
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(gtile)),
+                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(3 * x0), "r"(y0), "r"(smem_u32(&bar))
+                : "memory");
     }
     forceFallback |= int(__ldg(nanFlag));
     const int pw = a.lw + 2;  // h = 1
@@ -483,7 +502,7 @@ __global__ void __launch_bounds__(kThreads, GLU_F_MIN_BLOCKS)
             const int lx = ocx0 + c - 1, ly = ocy0 + r - 1;
             const bool in = lx >= 0 && ly >= 0 && lx < a.lw && ly < a.lh;
             const unsigned li = in ? unsigned(ly) * unsigned(a.lw) + unsigned(lx) : 0u;
-            v.w = OUT == kOutApply1 ? (in ? __ldg(a.lowT + li) : 0.0f) : __uint_as_float(li);
+            v.w = OUT == kOutApply1 ? (in ? __ldg(a.lowT + th + li) : 0.0f) : __uint_as_float(li);
             wcells[k] = v;
         }
     }
@@ -492,7 +511,7 @@ __global__ void __launch_bounds__(kThreads, GLU_F_MIN_BLOCKS)
             const int r = k / 96, c = k - r * 96;
             const int y = y0 + r;
             gtile[k] = (y < a.H && x0 * 3 + c < a.W * 3)
-                           ? __ldg(a.high + 3 * (size_t(y) * a.W + x0) + c)
+                           ? __ldg(a.high + hh + 3 * (size_t(y) * a.W + x0) + c)
                            : 0.0f;
         }
     }
@@ -531,7 +550,8 @@ __global__ void __launch_bounds__(kThreads, GLU_F_MIN_BLOCKS)
             swin += cw;
         }
         GLU_DCHECK(swin - wcells >= 0 && swin - wcells + 2 * cw + 2 < cw * (nch + 2));
-        solve_pixel<MODE, OUT, P>(a, packed, t, swin, wM, forceFallback, x, y, g[0], g[1], g[2]);
+        solve_pixel<MODE, OUT, P>(a, packed, t, swin, wM, forceFallback, x, y, g[0], g[1], g[2], fo,
+                                  th);
     }
 }
 
@@ -562,7 +582,7 @@ int max_pitch(int s) { return (kTX - 1) / s + 4; }
 
 template <int MODE, int OUT, int P>
 cudaError_t launch_fp(glu_ctx* ctx, const SolveArgs& a, const float4* packed, int forceFallback,
-                      const unsigned* nanFlag) {
+                      const unsigned* nanFlag, const FrameBatch& fb) {
     // Rows per thread: the count minimising waves x (rows + staging cost),
     // as k_solve32x.
     int dev = 0;
@@ -581,8 +601,8 @@ cudaError_t launch_fp(glu_ctx* ctx, const SolveArgs& a, const float4* packed, in
         float best = -1.0f;
         for (int r = 1; r <= kMaxRows; ++r) {
             int per = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_solve32f<MODE, OUT, P>, kThreads,
-                                                          smem_of(r));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_solve32f<MODE, OUT, P, false>,
+                                                          kThreads, smem_of(r));
             const long slots = long(max(per, 1)) * nsm;
             const long tiles = tilesX * ((a.H + kTY * r - 1) / (kTY * r));
             const float cost = float((tiles + slots - 1) / slots) * (float(r) + kStageCost);
@@ -611,58 +631,68 @@ cudaError_t launch_fp(glu_ctx* ctx, const SolveArgs& a, const float4* packed, in
 #endif
     if (GLU_F_TMA && a.W % 4 == 0 && (reinterpret_cast<uintptr_t>(a.high) & 15u) == 0) {
         if (auto enc = tensor_map_encoder()) {
-            const cuuint64_t dims[2] = {cuuint64_t(3) * a.W, cuuint64_t(a.H)};
-            const cuuint64_t strides[1] = {cuuint64_t(12) * a.W};
-            const cuuint32_t box[2] = {96u, cuuint32_t(tileH)};
-            const cuuint32_t estr[2] = {1u, 1u};
-            useTma = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a.high), dims,
-                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            // (a batch: a third dimension over its frames, fb.high floats apart)
+            const cuuint32_t rank = fb.frames > 1 ? 3u : 2u;
+            const cuuint64_t dims[3] = {cuuint64_t(3) * a.W, cuuint64_t(a.H),
+                                        cuuint64_t(fb.frames)};
+            const cuuint64_t strides[2] = {cuuint64_t(12) * a.W, cuuint64_t(4) * fb.high};
+            const cuuint32_t box[3] = {96u, cuuint32_t(tileH), 1u};
+            const cuuint32_t estr[3] = {1u, 1u, 1u};
+            useTma = (fb.frames == 1 || (fb.high * 4) % 16 == 0) &&
+                     enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<float*>(a.high),
+                         dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
         }
     }
     const size_t smem = smem_of(rows);
+    // (only the 1-ch video output is launched as a batch)
+    constexpr bool kCanBatch = OUT == kOutApply1;
+    const bool batch = kCanBatch && fb.frames > 1;
+    auto kern = batch ? k_solve32f<MODE, OUT, P, kCanBatch> : k_solve32f<MODE, OUT, P, false>;
+    if (fb.frames > 1 && !batch) return cudaErrorInvalidValue;
     if (smem > 48 * 1024) {
-        const cudaError_t e = cudaFuncSetAttribute(
-            k_solve32f<MODE, OUT, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        const cudaError_t e =
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return e;
     }
-    dim3 grid(unsigned(tilesX), (a.H + tileH - 1) / tileH);
-    k_solve32f<MODE, OUT, P><<<grid, kThreads, smem, ctx->stream>>>(tmap, a, packed, forceFallback,
-                                                                    nanFlag, rows, useTma);
+    dim3 grid(unsigned(tilesX), (a.H + tileH - 1) / tileH, unsigned(fb.frames));
+    kern<<<grid, kThreads, smem, ctx->stream>>>(tmap, a, packed, forceFallback, nanFlag, rows,
+                                                useTma, fb);
     ++ctx->launches;
     return cudaGetLastError();
 }
 
 template <int MODE, int OUT>
 cudaError_t launch_fo(glu_ctx* ctx, const SolveArgs& a, const float4* packed, int forceFallback,
-                      const unsigned* nanFlag) {
+                      const unsigned* nanFlag, const FrameBatch& fb) {
     switch (max_pitch(a.s)) {  // s = 8 (C3, C2): 7; s = 16 (C4): 5; s >= 32: 4
-        case 4: return launch_fp<MODE, OUT, 4>(ctx, a, packed, forceFallback, nanFlag);
-        case 5: return launch_fp<MODE, OUT, 5>(ctx, a, packed, forceFallback, nanFlag);
-        case 7: return launch_fp<MODE, OUT, 7>(ctx, a, packed, forceFallback, nanFlag);
-        default: return launch_fp<MODE, OUT, 0>(ctx, a, packed, forceFallback, nanFlag);
+        case 4: return launch_fp<MODE, OUT, 4>(ctx, a, packed, forceFallback, nanFlag, fb);
+        case 5: return launch_fp<MODE, OUT, 5>(ctx, a, packed, forceFallback, nanFlag, fb);
+        case 7: return launch_fp<MODE, OUT, 7>(ctx, a, packed, forceFallback, nanFlag, fb);
+        default: return launch_fp<MODE, OUT, 0>(ctx, a, packed, forceFallback, nanFlag, fb);
     }
 }
 
 template <int MODE>
 cudaError_t launch_f(glu_ctx* ctx, const SolveArgs& a, const float4* packed, int forceFallback,
-                     const unsigned* nanFlag) {
+                     const unsigned* nanFlag, const FrameBatch& fb) {
     if (a.params && !a.lowT && !a.errOut)
-        return launch_fo<MODE, kOutParams>(ctx, a, packed, forceFallback, nanFlag);
+        return launch_fo<MODE, kOutParams>(ctx, a, packed, forceFallback, nanFlag, fb);
     if (a.params && !a.lowT && a.errOut)
-        return launch_fo<MODE, kOutParamsErr>(ctx, a, packed, forceFallback, nanFlag);
+        return launch_fo<MODE, kOutParamsErr>(ctx, a, packed, forceFallback, nanFlag, fb);
     if (!a.params && a.lowT && a.channels == 1 && !a.errOut)
-        return launch_fo<MODE, kOutApply1>(ctx, a, packed, forceFallback, nanFlag);
-    return launch_fo<MODE, kOutGeneric>(ctx, a, packed, forceFallback, nanFlag);
+        return launch_fo<MODE, kOutApply1>(ctx, a, packed, forceFallback, nanFlag, fb);
+    return launch_fo<MODE, kOutGeneric>(ctx, a, packed, forceFallback, nanFlag, fb);
 }
 
 }  // namespace
 
 cudaError_t launch_solve32f(glu_ctx* ctx, const SolveArgs& a, const float4* packed,
-                            int forceFallback, const unsigned* nanFlag) {
-    return a.mode == GLU_MODE_GNU ? launch_f<GLU_MODE_GNU>(ctx, a, packed, forceFallback, nanFlag)
-                                  : launch_f<GLU_MODE_FAST>(ctx, a, packed, forceFallback, nanFlag);
+                            int forceFallback, const unsigned* nanFlag, const FrameBatch& fb) {
+    return a.mode == GLU_MODE_GNU
+               ? launch_f<GLU_MODE_GNU>(ctx, a, packed, forceFallback, nanFlag, fb)
+               : launch_f<GLU_MODE_FAST>(ctx, a, packed, forceFallback, nanFlag, fb);
 }
 
 }  // namespace glu_cu

@@ -146,6 +146,17 @@ def test_beyond_4gib_image_sampled_rows(glu, oracle):
     rec = glu.apply_field(field, low)
     matte = glu.op_matte(low)
     video = glu.glu.upsample_frames(dev[None], s, "matte")[0]
+    # two frames through the batched launch (3-D tensor map; frame 1's guide
+    # starts 4.7 GiB in): frame 1 (a mirrored copy) must match its own solve
+    mirrored = torch.flip(dev, dims=[1]).contiguous()
+    pair = torch.stack([dev, mirrored])
+    video2 = glu.glu.upsample_frames(pair, s, "matte")
+    del pair
+    assert torch.equal(video2[0], video)
+    lowm, gridm = glu.grid_downsample(mirrored, s)
+    fieldm = glu.optimize_field(mirrored, lowm, gridm)
+    assert torch.equal(video2[1], glu.apply_field(fieldm, glu.op_matte(lowm)))
+    del video2, fieldm, mirrored
     mat = matte.cpu().numpy()
     # cell rows holding HR rows whose byte offsets cross 2^31 and 2^32
     rows = sorted({0, (2**31 // 12) // W // s, (2**32 // 12) // W // s, lh // 2, lh - 1})

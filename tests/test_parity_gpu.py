@@ -483,3 +483,22 @@ def test_joint_unchanged_pixel_pass_matches_oracle(glu, oracle, mode, image, s):
     finally:
         ctx.set_trials(0)
     assert o["accepted"] + o["rejected"] > 0
+
+
+@pytest.mark.parametrize("W,H,s,mode", [(200, 136, 8, "fast"), (198, 131, 6, "fast"),
+                                        (256, 96, 4, "gnu")])
+def test_frame_batches_match_single_frames(glu, W, H, s, mode):
+    """glu_cu_upsample_frames with a 1-channel matte launches k_solve32f over
+    batches of up to 16 frames (grid z = frame; a 3-D tensor map when the rows
+    are 16-byte aligned, else the threads stage each frame's guide); 35 frames
+    = batches of 16, 16 and 3 on two buffer groups.  Every frame equals its
+    own single-frame solve + apply, bit for bit."""
+    from paper_2307_09582_b200 import workloads
+    frames = np.stack([workloads.scene(W, H, 70 + k, k) for k in range(35)])
+    md = mode_of(glu, mode)
+    got = glu.glu.upsample_frames(dev(frames), s, "matte", mode=md)
+    for k in range(frames.shape[0]):
+        f = dev(frames[k])
+        low, grid = glu.grid_downsample(f, s)
+        want, _ = glu.solve_apply(f, low, grid, glu.op_matte(low), None, md)
+        assert torch.equal(got[k], want), k
