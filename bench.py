@@ -446,25 +446,20 @@ def run_ours(args, ws, rank, local):
 
     def step(events=None, md=mode, dst=out):
         """One pass over the frames through the public frame API
-        (glu_cu_upsample_frames: k_frame_prep = grid_downsample + matte + LR
-        packing, then k_solve32f fused with the 1-ch apply).  Timed steps make
-        ONE call for all frames (the next frame's prep overlaps the current
-        solve on a side stream); with `events`, one call per frame bracketed by
-        events on the context stream (the per-launch kernel time)."""
-        if events is None:
-            G.N.check(lib.glu_cu_upsample_frames(ctx.handle, C.c_void_p(frames.data_ptr()), nf,
-                                                 C.byref(gc), C.byref(cc), int(md), 1,
-                                                 C.c_void_p(dst.data_ptr()), None))
-            return
-        # (events bracket the batch of per-frame calls: the host runs ahead of
-        # the device, so per-call host gaps stay out of the average)
-        events[0].record()
-        for f in range(nf):
-            fr = frames[f]
-            G.N.check(lib.glu_cu_upsample_frames(ctx.handle, C.c_void_p(fr.data_ptr()), 1,
-                                                 C.byref(gc), C.byref(cc), int(md), 1,
-                                                 C.c_void_p(dst[f].data_ptr()), None))
-        events[1].record()
+        (glu_cu_upsample_frames: the 16 frames' k_frame_prep_batch =
+        grid_downsample + matte + LR packing in one launch, then ONE k_solve32f
+        launch over all 16 frames (grid z = frame) fused with the 1-ch apply;
+        Exact mode: per frame, the next frame's prep overlapping on a side
+        stream).  With `events`: the same call bracketed by events on the
+        context stream (the launch time of the dominant kernel, its prep
+        included)."""
+        if events is not None:
+            events[0].record()
+        G.N.check(lib.glu_cu_upsample_frames(ctx.handle, C.c_void_p(frames.data_ptr()), nf,
+                                             C.byref(gc), C.byref(cc), int(md), 1,
+                                             C.c_void_p(dst.data_ptr()), None))
+        if events is not None:
+            events[1].record()
 
     for _ in range(args.warmup):
         step()
@@ -491,7 +486,7 @@ def run_ours(args, ws, rank, local):
         t = torch.tensor([elapsed_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed_ms = float(t.item())
-    # per-launch kernel time (roofline): the same frames, one call per frame
+    # per-launch kernel time (roofline): the batched launch (with its prep), / frames
     kreps = max(1, min(args.steps, 3))
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(kreps)]
     for k in range(kreps):
@@ -553,10 +548,11 @@ def run_ours(args, ws, rank, local):
         "executed_fp32": cap.get("executed_fp32"), "capture_stale": cap["stale"],
         "kernel": {"fast": "k_solve32f<Fast, Apply1>", "gnu": "k_solve32f<Gnu, Apply1>",
                    "exact": "k_solve32x<Apply1>"}[args.mode] +
-                  " (fused optimize_field + 1-ch apply_field) with its k_frame_prep launch "
-                  "(downsample + matte + LR packing, ~4 % of kernel_ms)",
-        "kernel_ms_basis": "CUDA events around 16 back-to-back per-frame calls (prep + solve "
-                           "each, not overlapped), / 16",
+                  " (fused optimize_field + 1-ch apply_field), Fast / GNU: one launch over "
+                  "the 16 frames (grid z = frame) after one batched k_frame_prep launch "
+                  "(downsample + matte + LR packing)",
+        "kernel_ms_basis": "CUDA events around one 16-frame glu_cu_upsample_frames call (the "
+                           "batched prep launch, then the batched solve launch), / 16",
         "fp64_verify_fraction": fallback_px / (args.steps * px_step),
         "kernel_ms": k_ms,
         "kernel_share_of_step": nf * k_ms / (elapsed_ms / args.steps),
@@ -592,8 +588,9 @@ def run_ours(args, ws, rank, local):
         xcap = capture_of("solve_apply_exact_c3", x_ms, fp32_tflops, nominal)
         xach = xflops / (x_ms * 1e-3) / 1e12
         roofline["pair_search"] = {
-            "mode": "exact", "kernel": "k_solve32x (fused optimize_field + 1-ch apply_field) "
-            "with its k_frame_prep launch", "kernel_ms": x_ms,
+            "mode": "exact", "kernel": "k_solve32x (fused optimize_field + 1-ch apply_field), "
+            "per frame, the next frame's k_frame_prep overlapping on a side stream (one 16-frame "
+            "call / 16)", "kernel_ms": x_ms,
             "algorithmic_flops_per_launch": xflops,
             "achieved": xach, "unit": "TFLOP/s",
             "frac": xach / fp32_tflops, "frac_of_nominal": xach / nominal,
@@ -672,7 +669,7 @@ def run_ours(args, ws, rank, local):
                        "scale": SCALE, "window": 3, "mode": args.mode,
                        "parallelism": f"frames sharded, {ws} rank(s)",
                        "l2": "inputs 1.6 GB/rank > 126 MB L2; no flush",
-                       "step": "one glu_cu_upsample_frames call for the 16 frames (frame k+1 prep overlaps frame k solve)"},
+                       "step": "one glu_cu_upsample_frames call for the 16 frames (one batched prep launch, one batched k_solve32f launch)"},
             "e2e": {"value": e2e_value, "unit": "HR Mpix/s",
                     "h2d_bytes_per_step": nf * W_ * H_ * 12,
                     "d2h_bytes_per_step": nf * W_ * H_ * 4,

@@ -591,7 +591,10 @@ int frames_pipelined(glu_ctx* ctx, const float* frames, int count, const glu_gri
 // k_solve32f in batches of up to kFrameBatch per launch (grid z = frame), so
 // the SMs never drain between frames; one batched prep launch per batch, the
 // next batch's on the side stream while this one solves.
-constexpr int kFrameBatch = 16;
+#ifndef GLU_FRAME_BATCH_MAX
+#define GLU_FRAME_BATCH_MAX 16
+#endif
+constexpr int kFrameBatch = GLU_FRAME_BATCH_MAX;
 
 int frames_batched(glu_ctx* ctx, const float* frames, int count, const glu_grid* g,
                    const glu_config* cfg, int mode, float* out) {

@@ -23,6 +23,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+FRAMES = 1  # frames per captured launch (--frames: a batched launch's numbers / frame)
 
 
 def short(name: str) -> str:
@@ -160,12 +161,15 @@ def kernel(rep: str, out: str, traffic_key: str | None, kid: int = 0,
         import hashlib
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         d = json.load(open(tp)) if os.path.exists(tp) else {}
-        d[traffic_key] = dram_r + dram_w
+        fr = FRAMES
+        d[traffic_key] = (dram_r + dram_w) / fr
         if tot:  # executed warp instructions per launch (bench.py's issue bound)
-            d[traffic_key + "_warp_instr"] = tot
+            d[traffic_key + "_warp_instr"] = tot / fr
         if fp32_exec is not None:
-            d[traffic_key + "_fp32_flop_executed"] = fp32_exec
-            d[traffic_key + "_fp64_flop_executed"] = fp64_exec
+            d[traffic_key + "_fp32_flop_executed"] = fp32_exec / fr
+            d[traffic_key + "_fp64_flop_executed"] = fp64_exec / fr
+        if fr > 1:
+            d[traffic_key + "_frames_per_launch"] = fr
         if sources:  # bench.py flags the numbers stale when these files change
             h = hashlib.sha256()
             for f in sources:
@@ -178,6 +182,8 @@ if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3])
     else:
+        if "--frames" in sys.argv:  # a batched launch: per-frame numbers for traffic.json
+            FRAMES = int(sys.argv[sys.argv.index("--frames") + 1])
         key = sys.argv[sys.argv.index("--traffic-key") + 1] if "--traffic-key" in sys.argv else None
         kid = int(sys.argv[sys.argv.index("--id") + 1]) if "--id" in sys.argv else 0
         srcs = (sys.argv[sys.argv.index("--sources") + 1].split(",")

@@ -8,6 +8,7 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_2307_09582_b200 as glu  # noqa: E402
@@ -21,7 +22,17 @@ p.add_argument("--width", type=int, default=3840)
 p.add_argument("--height", type=int, default=2160)
 p.add_argument("--scale", type=int, default=8)
 p.add_argument("--window", type=int, default=3)
+p.add_argument("--frames", type=int, default=0,
+               help="> 1: the batched video path (glu_cu_upsample_frames over N frames)")
 a = p.parse_args()
+if a.frames > 1:
+    fr = torch.from_numpy(np.stack([workloads.scene(a.width, a.height, 3, k)
+                                    for k in range(a.frames)])).cuda()
+    for _ in range(a.iters):
+        vid = glu.glu.upsample_frames(fr, a.scale, "matte", mode=glu.mode_from_name(a.mode))
+    torch.cuda.synchronize()
+    print("ok", tuple(vid.shape))
+    sys.exit(0)
 
 img = torch.from_numpy(workloads.scene(a.width, a.height, 3, 0)).cuda()
 ctx = glu.glu.context()
