@@ -621,7 +621,12 @@ cudaError_t launch_fp(glu_ctx* ctx, const SolveArgs& a, const float4* packed, in
 #ifndef GLU_F_ROWS
 #define GLU_F_ROWS 0  // 0: picked per launch (A/B builds force a count)
 #endif
-    const int rows = GLU_F_ROWS > 0 ? GLU_F_ROWS : memo[5];
+#ifndef GLU_F_BATCH_ROWS
+#define GLU_F_BATCH_ROWS 12  // a batch has no wave tail to fit: taller tiles (8..16: 12 best)
+#endif
+    const int rows = GLU_F_ROWS > 0 ? GLU_F_ROWS
+                                    : (OUT == kOutApply1 && fb.frames > 1 ? GLU_F_BATCH_ROWS
+                                                                          : memo[5]);
     const int tileH = kTY * rows;
     // TMA needs 16-byte aligned rows (3 W floats) and base; else the threads stage the guide.
     CUtensorMap tmap{};
