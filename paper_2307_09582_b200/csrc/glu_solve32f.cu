@@ -50,7 +50,10 @@ namespace {
 #define GLU_F_TY 4  // warps per CTA (rows of a tile per row step); 8 measured 1.3 % slower
 #endif
 constexpr int kTX = 32, kTY = GLU_F_TY, kThreads = kTX * kTY;
-constexpr int kMaxRows = 8;
+#ifndef GLU_F_MAX_ROWS
+#define GLU_F_MAX_ROWS 8
+#endif
+constexpr int kMaxRows = GLU_F_MAX_ROWS;
 constexpr float kStageCost = 0.3f;  // a tile's staging, in units of one row of pixels
 constexpr float kU = 5.9604645e-08f;  // 2^-24
 constexpr float kCA = 32.0f;          // stage A relative margin (in u)
