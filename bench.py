@@ -632,33 +632,26 @@ def run_ours(args, ws, rank, local):
             hbm_gbs = json.load(fh)["hbm_gbs"]
     except Exception:
         pass
-    c5 = None
-    if not args.no_c5:
-        del frames
-        torch.cuda.empty_cache()
-        try:
-            c5 = run_c5(args, ws, rank, dist, hbm_gbs)
-        except Exception as e:  # reported, never silently replaced
-            c5 = {"error": f"{type(e).__name__}: {e}"}
+    # Multi-rank runs: the C5 / C4 extras below exchange data between ranks.  If
+    # one of them stalls (a peer died, a collective never completes), the
+    # headline -- already measured -- must still be printed: a watchdog thread
+    # prints the line without the stalled extras and ends this rank.
+    partial = {"c5": None, "c4": None}
+    watchdog = None
+    if ws > 1:
+        limit_s = float(os.environ.get("GLU_BENCH_EXTRAS_TIMEOUT", "420"))
 
-    c4 = None
-    if not args.no_c4:
-        torch.cuda.empty_cache()
-        try:
-            c4 = run_c4(args, ws, rank, dist)
-        except Exception as e:  # reported, never silently replaced
-            c4 = {"error": f"{type(e).__name__}: {e}"}
+        def give_up():
+            if rank == 0:
+                note = {"error": f"no result within {limit_s:.0f} s (multi-rank extras timed out)"}
+                print(json.dumps(make_line(partial["c5"] or note, partial["c4"] or note, None)),
+                      flush=True)
+            os._exit(0)
+        watchdog = threading.Timer(limit_s, give_up)
+        watchdog.daemon = True
 
-    cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        try:
-            cpu = cpu_reference_sample(frames_np, args.mode, args.cpu_seconds,
-                                       gpu_out=out.cpu().numpy())
-        except Exception as e:  # reported, never silently replaced
-            cpu = {"value": None, "error": f"{type(e).__name__}: {e}"}
-
-    if rank == 0:
-        line = {
+    def make_line(c5, c4, cpu):
+        return {
             "metric": METRIC, "value": value, "unit": "HR Mpix/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
@@ -687,9 +680,46 @@ def run_ours(args, ws, rank, local):
             "c5": c5,
             "c4": c4,
         }
-        print(json.dumps(line), flush=True)
+
+    if watchdog:
+        watchdog.start()
+    c5 = None
+    if not args.no_c5:
+        del frames
+        torch.cuda.empty_cache()
+        try:
+            c5 = run_c5(args, ws, rank, dist, hbm_gbs)
+        except Exception as e:  # reported, never silently replaced
+            c5 = {"error": f"{type(e).__name__}: {e}"}
+        partial["c5"] = c5
+
+    c4 = None
+    if not args.no_c4:
+        torch.cuda.empty_cache()
+        try:
+            c4 = run_c4(args, ws, rank, dist)
+        except Exception as e:  # reported, never silently replaced
+            c4 = {"error": f"{type(e).__name__}: {e}"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_sample(frames_np, args.mode, args.cpu_seconds,
+                                       gpu_out=out.cpu().numpy())
+        except Exception as e:  # reported, never silently replaced
+            cpu = {"value": None, "error": f"{type(e).__name__}: {e}"}
+
+    if watchdog:
+        watchdog.cancel()
+    if rank == 0:
+        print(json.dumps(make_line(c5, c4, cpu)), flush=True)
     if dist:
+        # (the line is out: a teardown that waits on a lost peer must not hold the job)
+        bye = threading.Timer(60.0, lambda: os._exit(0))
+        bye.daemon = True
+        bye.start()
         dist.destroy_process_group()
+        bye.cancel()
 
 
 def main():
