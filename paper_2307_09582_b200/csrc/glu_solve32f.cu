@@ -81,6 +81,58 @@ __device__ __forceinline__ float fmax_nan(float a, float b) {  // NaN if either 
     return r;
 }
 
+// Packed fp32 pairs (sm_100 FADD2 / FMUL2 / FFMA2): two IEEE round-to-nearest
+// operations per issued instruction, each lane bit-identical to the scalar
+// add / mul / fma -- the kernel is bound by instruction issue, not by the FP32
+// pipe.  A pair lives in an aligned 64-bit register pair (lo = first).
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk2(float lo, float hi) {
+    f32x2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void upk2(f32x2 v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+    f32x2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ float key_pack(float t, int j, unsigned mask) {  // (t & mask) | j
+    unsigned r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEC;" : "=r"(r) : "r"(__float_as_uint(t)), "r"(unsigned(j)),
+        "r"(mask));
+    return __uint_as_float(r);
+}
+
+// Pair table (compile-time pitches, s >= 8): per owner cell of the tile its 9
+// window candidates as 5 slots of two candidates (2k, 2k + 1; slot 4 = {8, 8}):
+// float4 {x0, x1, y0, y1} x 5, then float2 {z0, z1} x 5, so a pixel reads a
+// slot with LDS.128 + LDS.64 straight into packed operands.  9 float4 per cell
+// (144 B: the cells a warp reads at once fall in different banks), at a pitch
+// of P - 2 owner cells per row.
+constexpr int kCellF4 = 9;
+// (GNU mode -- stage A only -- measured 2.5 % slower with the table: scalar)
+template <int MODE, int P>
+__host__ __device__ constexpr bool use_pairs() { return P > 0 && MODE == GLU_MODE_FAST; }
+#ifndef GLU_F_PK_A
+#define GLU_F_PK_A 1  // stage A in packed pairs (A/B knob)
+#endif
+#ifndef GLU_F_PK_B
+#define GLU_F_PK_B 1  // stage B in packed pairs (A/B knob)
+#endif
+
 __device__ __forceinline__ int div_s(int v, const SolveArgs& a) {
     return a.sdiv ? int(__umulhi(unsigned(v), a.sdiv)) : v / a.s;
 }
@@ -108,10 +160,7 @@ __device__ __forceinline__ float fast_key(float e0, float e1, float e2, float qj
     const float nl = __fmaf_rn(dj, bc, __fmul_rn(Ap, qj));
     const float sj = __fadd_rn(at, dj);
     const float t = __fmul_rn(nl, rcp_approx(__fmul_rn(sj, sj)));
-    unsigned r;
-    asm("lop3.b32 %0, %1, %2, %3, 0xEC;" : "=r"(r) : "r"(__float_as_uint(t)), "r"(unsigned(j)),
-        "r"(mask));
-    return __uint_as_float(r);
+    return key_pack(t, j, mask);
 }
 
 // Smallest (K1) and second smallest (K2) key; NaN keys change neither.
@@ -266,9 +315,9 @@ __device__ __forceinline__ int pitch_of(const FTile& t) { return P > 0 ? P : t.c
 // `wM` = the tile's largest |channel|.
 template <int MODE, int OUT, int P>
 __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* packed, const FTile& t,
-                                            const float4* swin, float wM, int forceFallback,
-                                            int x, int y, float ip0, float ip1, float ip2,
-                                            size_t fo, size_t th) {
+                                            const float4* swin, const float4* ptab, float wM,
+                                            int forceFallback, int x, int y, float ip0, float ip1,
+                                            float ip2, size_t fo, size_t th) {
     // (fo / th: this frame's output / target offsets in a batched launch)
     const size_t p = size_t(y) * size_t(a.W) + size_t(x) + fo;
     const int cw = pitch_of<P>(t);
@@ -280,21 +329,53 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
     // smallest) screens for the near ties that need the exact check below.
     const unsigned kmask = 0xfffffff0u | (unsigned(a.W) >> 31);  // opaque: a register
     float K1a = kInf, K2a = kInf, pa = 0.0f;
+    // (P > 0) the candidates two at a time from the owner cell's pair table:
+    // e = I_j - I_p and q_j for slot k's two candidates in packed registers,
+    // lane for lane the scalar operations below
+    f32x2 E0[5], E1[5], E2[5], Q[5];
+    if (use_pairs<MODE, P>()) {
+        const f32x2 n0 = pk2(-ip0, -ip0), n1 = pk2(-ip1, -ip1), n2 = pk2(-ip2, -ip2);
 #pragma unroll
-    for (int j = 0; j < 9; ++j) {
-        const float4 v = swin[woff(j, cw)];
-        const float d0 = v.x - ip0, d1 = v.y - ip1, d2 = v.z - ip2;
-        const float qq = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmul_rn(d0, d0)));
-        unsigned kb;
-        asm("lop3.b32 %0, %1, %2, %3, 0xEC;" : "=r"(kb) : "r"(__float_as_uint(qq)), "r"(unsigned(j)),
-            "r"(kmask));
-        const float key = __uint_as_float(kb);
-        if (j & 1)
-            track_key2(K1a, K2a, pa, key);
-        else if (j == 8)
-            track_key(K1a, K2a, key);
-        else
-            pa = key;
+        for (int k = 0; k < 5; ++k) {
+            const ulonglong2 sxy = *reinterpret_cast<const ulonglong2*>(ptab + k);
+            const f32x2 sz = reinterpret_cast<const f32x2*>(ptab + 5)[k];
+            float q0, q1;
+            if (GLU_F_PK_A) {
+                E0[k] = add2(sxy.x, n0);
+                E1[k] = add2(sxy.y, n1);
+                E2[k] = add2(sz, n2);
+                Q[k] = fma2(E2[k], E2[k], fma2(E1[k], E1[k], mul2(E0[k], E0[k])));
+                upk2(Q[k], q0, q1);
+            } else {
+                float x0, x1, y0, y1, z0, z1;
+                upk2(sxy.x, x0, x1);
+                upk2(sxy.y, y0, y1);
+                upk2(sz, z0, z1);
+                x0 -= ip0, x1 -= ip0, y0 -= ip1, y1 -= ip1, z0 -= ip2, z1 -= ip2;
+                q0 = __fmaf_rn(z0, z0, __fmaf_rn(y0, y0, __fmul_rn(x0, x0)));
+                q1 = __fmaf_rn(z1, z1, __fmaf_rn(y1, y1, __fmul_rn(x1, x1)));
+                E0[k] = pk2(x0, x1), E1[k] = pk2(y0, y1), E2[k] = pk2(z0, z1), Q[k] = pk2(q0, q1);
+            }
+            const float k0 = key_pack(q0, 2 * k, kmask);
+            if (k < 4)
+                track_key2(K1a, K2a, k0, key_pack(q1, 2 * k + 1, kmask));
+            else
+                track_key(K1a, K2a, k0);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 9; ++j) {
+            const float4 v = swin[woff(j, cw)];
+            const float d0 = v.x - ip0, d1 = v.y - ip1, d2 = v.z - ip2;
+            const float qq = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmul_rn(d0, d0)));
+            const float key = key_pack(qq, j, kmask);
+            if (j & 1)
+                track_key2(K1a, K2a, pa, key);
+            else if (j == 8)
+                track_key(K1a, K2a, key);
+            else
+                pa = key;
+        }
     }
     const int ja = int(__float_as_uint(K1a) & 15u);
     const float4 ca = swin[woff(ja, cw)];
@@ -331,18 +412,52 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
         const float Ap = A - G;
         const float b0 = B * ea0, b1 = B * ea1, b2 = B * ea2;
         float K1 = kInf, K2 = kInf, pend = 0.0f;
+        if (use_pairs<MODE, P>()) {  // fast_key for two candidates per instruction
+            const f32x2 B0 = pk2(b0, b0), B1 = pk2(b1, b1), B2 = pk2(b2, b2);
+            const f32x2 at2 = pk2(at, at), Ap2 = pk2(Ap, Ap);
 #pragma unroll
-        for (int j = 0; j < 9; ++j) {
-            const float4 v = swin[woff(j, cw)];
-            const float d0 = v.x - ip0, d1 = v.y - ip1, d2 = v.z - ip2;
-            const float qj = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmul_rn(d0, d0)));
-            const float key = fast_key(d0, d1, d2, qj, b0, b1, b2, at, Ap, j, kmask);
-            if (j & 1)
-                track_key2(K1, K2, pend, key);
-            else if (j == 8)
-                track_key(K1, K2, key);
-            else
-                pend = key;
+            for (int k = 0; k < 5; ++k) {
+                float q0, q1;
+                upk2(Q[k], q0, q1);
+                float k0, k1 = 0.0f;
+                if (GLU_F_PK_B) {
+                    const f32x2 bc = fma2(E2[k], B2, fma2(E1[k], B1, mul2(E0[k], B0)));
+                    const f32x2 dj = pk2(fast_sqrt(q0), k < 4 ? fast_sqrt(q1) : 0.0f);
+                    const f32x2 nl = fma2(dj, bc, mul2(Ap2, Q[k]));
+                    const f32x2 sj = add2(at2, dj);
+                    float s0, s1;
+                    upk2(mul2(sj, sj), s0, s1);
+                    float t0, t1;
+                    upk2(mul2(nl, pk2(rcp_approx(s0), k < 4 ? rcp_approx(s1) : 0.0f)), t0, t1);
+                    k0 = key_pack(t0, 2 * k, kmask);
+                    if (k < 4) k1 = key_pack(t1, 2 * k + 1, kmask);
+                } else {
+                    float x0, x1, y0, y1, z0, z1;
+                    upk2(E0[k], x0, x1);
+                    upk2(E1[k], y0, y1);
+                    upk2(E2[k], z0, z1);
+                    k0 = fast_key(x0, y0, z0, q0, b0, b1, b2, at, Ap, 2 * k, kmask);
+                    if (k < 4) k1 = fast_key(x1, y1, z1, q1, b0, b1, b2, at, Ap, 2 * k + 1, kmask);
+                }
+                if (k < 4)
+                    track_key2(K1, K2, k0, k1);
+                else
+                    track_key(K1, K2, k0);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 9; ++j) {
+                const float4 v = swin[woff(j, cw)];
+                const float d0 = v.x - ip0, d1 = v.y - ip1, d2 = v.z - ip2;
+                const float qj = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmul_rn(d0, d0)));
+                const float key = fast_key(d0, d1, d2, qj, b0, b1, b2, at, Ap, j, kmask);
+                if (j & 1)
+                    track_key2(K1, K2, pend, key);
+                else if (j == 8)
+                    track_key(K1, K2, key);
+                else
+                    pend = key;
+            }
         }
         jb = int(__float_as_uint(K1) & 15u);
         // the winner's upper bound: K1 + 2 G q_b / s_b^2 + F
@@ -444,7 +559,8 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 
-// Dynamic shared memory: [guide: tileH x 96 floats][cells: P x (nch + 2)].
+// Dynamic shared memory: [guide: tileH x 96 floats][cells: P x (mch + 2)]
+// [Fast mode, P > 0: pair table, (P - 2) x mch owner cells x kCellF4 float4].
 // `tmap` is a 2-D tensor map of the guide (3 W floats x H rows, box 96 x
 // tileH) when useTma != 0.
 template <int MODE, int OUT, int P, bool BATCH>
@@ -509,6 +625,25 @@ __global__ void __launch_bounds__(kThreads, GLU_F_MIN_BLOCKS)
             wcells[k] = v;
         }
     }
+    float4* ptab = nullptr;
+    if (use_pairs<MODE, P>()) {
+        // the pair table from the packed image (no barrier between the two
+        // stagings): owner cell (r, c)'s slots at kCellF4 * (r * (P - 2) + c)
+        const int mch = (tileH - 1) / a.s + 2;
+        ptab = wcells + P * (mch + 2);
+        for (int k = threadIdx.x; k < (P - 2) * nch * 5; k += kThreads) {
+            const int cell = k / 5, sl = k - 5 * cell;
+            const int r = cell / (P - 2), c = cell - r * (P - 2);
+            if (c < ncw) {
+                const int j0 = 2 * sl, j1 = sl < 4 ? j0 + 1 : j0;
+                const int r0 = (j0 * 11) >> 5, r1 = (j1 * 11) >> 5;
+                const float4 v0 = __ldg(packed + size_t(ocy0 + r + r0) * pw + (ocx0 + c + j0 - 3 * r0));
+                const float4 v1 = __ldg(packed + size_t(ocy0 + r + r1) * pw + (ocx0 + c + j1 - 3 * r1));
+                ptab[kCellF4 * cell + sl] = make_float4(v0.x, v1.x, v0.y, v1.y);
+                reinterpret_cast<float2*>(ptab + kCellF4 * cell + 5)[sl] = make_float2(v0.z, v1.z);
+            }
+        }
+    }
     if (!useTma) {  // the guide rows are not 16-byte aligned: staged by the threads
         for (int k = threadIdx.x; k < tileH * 96; k += kThreads) {
             const int r = k / 96, c = k - r * 96;
@@ -545,16 +680,22 @@ __global__ void __launch_bounds__(kThreads, GLU_F_MIN_BLOCKS)
     // owner-cell row of the current row, advanced when y reaches yNext
     const int cy0 = div_s(yr, a);
     int yNext = (cy0 + 1) * a.s;
-    const float4* swin = wcells + (cy0 - ocy0) * cw + (div_s(x, a) - ocx0);
+    // the owner cell's offset in the staged cells (its window's top-left
+    // candidate) and of its slots in the pair table
+    const int cxr = div_s(x, a) - ocx0;
+    int co = (cy0 - ocy0) * cw + cxr;
+    const float4* pt =
+        use_pairs<MODE, P>() ? ptab + kCellF4 * ((cy0 - ocy0) * (P - 2) + cxr) : ptab;
 #pragma unroll 1
     for (int y = yr; y < yEnd; ++y, g += 96) {
         if (y == yNext) {
             yNext += a.s;
-            swin += cw;
+            co += cw;
+            if (use_pairs<MODE, P>()) pt += kCellF4 * (P - 2);
         }
-        GLU_DCHECK(swin - wcells >= 0 && swin - wcells + 2 * cw + 2 < cw * (nch + 2));
-        solve_pixel<MODE, OUT, P>(a, packed, t, swin, wM, forceFallback, x, y, g[0], g[1], g[2], fo,
-                                  th);
+        GLU_DCHECK(co >= 0 && co + 2 * cw + 2 < cw * (nch + 2));
+        solve_pixel<MODE, OUT, P>(a, packed, t, wcells + co, pt, wM, forceFallback, x, y, g[0], g[1],
+                                  g[2], fo, th);
     }
 }
 
@@ -594,7 +735,8 @@ cudaError_t launch_fp(glu_ctx* ctx, const SolveArgs& a, const float4* packed, in
     const long tilesX = (a.W + kTX - 1) / kTX;
     auto smem_of = [&](int r) {
         const int mch = (kTY * r - 1) / a.s + 2;
-        return sizeof(float) * size_t(kTY * r) * 96 + sizeof(float4) * size_t(pitch) * (mch + 2);
+        return sizeof(float) * size_t(kTY * r) * 96 + sizeof(float4) * size_t(pitch) * (mch + 2) +
+               (use_pairs<MODE, P>() ? sizeof(float4) * size_t(kCellF4) * (P - 2) * mch : 0);
     };
     thread_local int memo[6] = {-1, 0, 0, 0, -1, 1};  // device, s, W, H, MODE/OUT/P -> rows
     const int key = (MODE * 4 + OUT) * 64 + P;
@@ -625,11 +767,12 @@ cudaError_t launch_fp(glu_ctx* ctx, const SolveArgs& a, const float4* packed, in
 #define GLU_F_ROWS 0  // 0: picked per launch (A/B builds force a count)
 #endif
 #ifndef GLU_F_BATCH_ROWS
-#define GLU_F_BATCH_ROWS 12  // a batch has no wave tail to fit: taller tiles (8..16: 12 best)
+#define GLU_F_BATCH_ROWS 10  // a batch has no wave tail to fit: taller tiles (8 / 10 / 12 / 14 / 16: 67.8 / 68.8 / 67.9 / 66.2 / 63.9 k HR Mpix/s)
 #endif
     const int rows = GLU_F_ROWS > 0 ? GLU_F_ROWS
-                                    : (OUT == kOutApply1 && fb.frames > 1 ? GLU_F_BATCH_ROWS
-                                                                          : memo[5]);
+                                    : (OUT == kOutApply1 && fb.frames > 1
+                                           ? (MODE == GLU_MODE_FAST ? GLU_F_BATCH_ROWS : 12)
+                                           : memo[5]);
     const int tileH = kTY * rows;
     // TMA needs 16-byte aligned rows (3 W floats) and base; else the threads stage the guide.
     CUtensorMap tmap{};
