@@ -88,6 +88,45 @@ __device__ __forceinline__ void track_key2(float& K1, float& K2, float a, float 
     K1 = fminf(fminf(K1, a), b);
 }
 
+// Packed fp32 pairs (sm_100 FMUL2 / FFMA2: two IEEE round-to-nearest
+// operations per issued instruction, each lane bit-identical to the scalar
+// mul / fma; glu_solve32f.cu).
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk2(float lo, float hi) {
+    f32x2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void upk2(f32x2 v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+    f32x2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
+// The pair table of one owner cell: D'_ij (i < j) column by column (column j's
+// j entries start at j (j - 1) / 2), rows two at a time: for even i with
+// i + 1 < j the two float4 slots of (i, j) and (i + 1, j) hold {x_i, x_i+1,
+// y_i, y_i+1} and {z_i, z_i+1, -, -} (packed operands for one LDS.128 + one
+// LDS.64); an odd column's last row (j - 1, j) is a plain {x, y, z, -}.
+__device__ __forceinline__ constexpr int col_base(int j) { return j * (j - 1) / 2; }
+__device__ __forceinline__ float3 tab_pair(const float4* tab, int i, int j) {
+    const int b = col_base(j);
+    if (!(i & 1) && i + 1 == j) {
+        const float4 d = tab[b + i];
+        return make_float3(d.x, d.y, d.z);
+    }
+    const float* f = reinterpret_cast<const float*>(tab + b + (i & ~1)) + (i & 1);
+    return make_float3(f[0], f[2], f[4]);
+}
+
 // Lexicographic pair k (i <= j over 9 candidates: rows start at 0, 9, 17,
 // 24, 30, 35, 39, 42, 44) -> (i, j).
 __device__ __forceinline__ void lex_pair(int k, int& i, int& j) {
@@ -151,7 +190,7 @@ __device__ __noinline__ ClosePick resolve_close(const float4* swin, const float4
         for (int i = 0; i <= j; ++i) {
             float key;
             if (i < j) {
-                const float4 d = tab[i * 8 - i * (i - 1) / 2 + (j - i - 1)];
+                const float3 d = tab_pair(tab, i, j);
                 const float dn = __fmaf_rn(e0, d.x, __fmaf_rn(e1, d.y, e2 * d.z));
                 key = pack_key(__fmaf_rn(-dn, dn, qm), i, kmask);
             } else {
@@ -276,15 +315,24 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
         qmin = fminf(qmin, qj);
         const float k1in = K1;
         float pend = 0.0f;  // keys are tracked two at a time: (0, 1), (2, 3), ...
+        // rows (i, i + 1) of column j in packed pairs (e_j broadcast)
+        const f32x2 E0 = pk2(e0, e0), E1 = pk2(e1, e1), E2 = pk2(e2, e2), Qm = pk2(qm, qm);
 #pragma unroll
-        for (int i = 0; i < j; ++i) {
-            const float4 d = tab[i * 8 - i * (i - 1) / 2 + (j - i - 1)];
-            const float dn = __fmaf_rn(e0, d.x, __fmaf_rn(e1, d.y, e2 * d.z));
-            const float key = pack_key(__fmaf_rn(-dn, dn, qm), i, kmask);
-            if (i & 1)
-                track_key2(K1, K2, pend, key);
-            else
-                pend = key;
+        for (int i = 0; i < j; i += 2) {
+            const float4* slot = tab + col_base(j) + i;
+            if (i + 1 < j) {
+                const ulonglong2 dxy = *reinterpret_cast<const ulonglong2*>(slot);
+                const f32x2 dz = *reinterpret_cast<const f32x2*>(slot + 1);
+                const f32x2 dn = fma2(E0, dxy.x, fma2(E1, dxy.y, mul2(E2, dz)));
+                float n0, n1, t0, t1;
+                upk2(dn, n0, n1);
+                upk2(fma2(pk2(-n0, -n1), dn, Qm), t0, t1);
+                track_key2(K1, K2, pack_key(t0, i, kmask), pack_key(t1, i + 1, kmask));
+            } else {
+                const float4 d = *slot;
+                const float dn = __fmaf_rn(e0, d.x, __fmaf_rn(e1, d.y, e2 * d.z));
+                pend = pack_key(__fmaf_rn(-dn, dn, qm), i, kmask);
+            }
         }
         const float kd = pack_key(qm, j, kmask);  // (j, j): w = 0, obj = q_j
         if (j & 1)
@@ -473,7 +521,15 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS)
         const float den = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmaf_rn(d0, d0, eps)));
         // D' = D / sqrt(den): then obj_ij = q_j - (e_j . D')^2
         const float r = rsqrt_approx(den);
-        table[cell * kCellStride + pr] = make_float4(d0 * r, d1 * r, d2 * r, 0.0f);
+        float4* slot = table + cell * kCellStride + col_base(tj) + (ti & ~1);
+        if (!(ti & 1) && ti + 1 == tj) {
+            *slot = make_float4(d0 * r, d1 * r, d2 * r, 0.0f);
+        } else {  // lane ti & 1 of the two-row slots
+            float* f = reinterpret_cast<float*>(slot) + (ti & 1);
+            f[0] = d0 * r;
+            f[2] = d1 * r;
+            f[4] = d2 * r;
+        }
         lx += kCellStep;
         while (lx >= ncw) {
             lx -= ncw;

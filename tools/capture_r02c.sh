@@ -1,9 +1,9 @@
 #!/bin/bash
 # On the GPU box: the end-of-round evidence set (round 2), each command run
 # plain first and then under ncu (one process per ncu run; 1 GPU).
-#   bash tools/capture_r02c.sh
+#   bash tools/capture_r02c.sh [tag]
 cd "$(dirname "$0")/.."
-T=r02c
+T=${1:-r02c}
 bash tools/capture_c3.sh $T
 python bench.py > gpurun_out/${T}_bench.log 2>&1; echo "bench rc=$?"
 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/${T}_bench_ref.log 2>&1; echo "ref rc=$?"
