@@ -111,6 +111,7 @@ def kernel(rep: str, out: str, traffic_key: str | None, kid: int = 0,
             dedup.append(blk)
     srows = [["Kernel Name"]] + (dedup[kid] if kid < len(dedup) else [])
     mix = collections.Counter()
+    packed_flop = [0]  # warp-level flop lanes of the packed fp32 instructions
     if len(srows) > 2:
         h2 = srows[1]
         ie, isrc = h2.index("Instructions Executed"), h2.index("Source")
@@ -124,6 +125,12 @@ def kernel(rep: str, out: str, traffic_key: str | None, kid: int = 0,
                 continue
             op = toks[1] if toks[0].startswith("@") and len(toks) > 1 else toks[0]
             mix[op.split(".")[0]] += n
+            # packed fp32 pairs (FADD2 / FMUL2 / FFMA2): ncu's per-opcode thread
+            # counters below do not include them; lanes = 2 when an operand is a
+            # register pair (.F32x2), 1 for the all-scalar form
+            if op.split(".")[0] in ("FADD2", "FMUL2", "FFMA2"):
+                lanes = 2 if "F32x2" in r[isrc] else 1
+                packed_flop[0] += n * lanes * (2 if op.startswith("FFMA2") else 1)
     lines = [f"# ncu --set full: `{kname}` ({os.path.basename(rep)})", "",
              "| metric | value |", "|---|---|"]
     for k in WANT:
@@ -151,9 +158,16 @@ def kernel(rep: str, out: str, traffic_key: str | None, kid: int = 0,
     f32 = [thread_ops(o) for o in ("ffma", "fadd", "fmul")]
     f64 = [thread_ops(o) for o in ("dfma", "dadd", "dmul")]
     fp32_exec = 2 * f32[0] + f32[1] + f32[2] if None not in f32 else None
+    if fp32_exec is not None and packed_flop[0]:
+        try:  # warp-level counts x the kernel's average active threads per warp
+            act = float(vals["Avg. Active Threads Per Warp"][0])
+        except (KeyError, ValueError):
+            act = 32.0
+        fp32_exec += packed_flop[0] * act
     fp64_exec = 2 * f64[0] + f64[1] + f64[2] if None not in f64 else None
     if fp32_exec is not None:
-        extra = [f"| executed FP32 flop (2 FFMA + FADD + FMUL, thread-level) | {fp32_exec:.4g} |",
+        extra = [f"| executed FP32 flop (2 FFMA + FADD + FMUL, thread-level; packed FFMA2 / FADD2 "
+                 f"/ FMUL2 lanes included) | {fp32_exec:.4g} |",
                  f"| executed FP64 flop (2 DFMA + DADD + DMUL) | {fp64_exec:.4g} |"]
         lines[4:4] = extra
         open(out, "w").write("\n".join(lines) + "\n")
