@@ -702,6 +702,9 @@ __global__ void __launch_bounds__(kThreads, GLU_F_MIN_BLOCKS)
         }
         const float4* swin = kCarryPtr ? swinp : wcells + co;
         GLU_DCHECK(swin - wcells >= 0 && swin - wcells + 2 * cw + 2 < cw * (nch + 2));
+        constexpr bool kPairs = use_pairs<MODE, P>();  // (no commas inside the macro)
+        GLU_DCHECK(!kPairs || (pt - ptab >= 0 && pt - ptab < kCellF4 * (P - 2) * nch &&
+                               (pt - ptab) / kCellF4 % (P - 2) < ncw));
         solve_pixel<MODE, OUT, P>(a, packed, t, swin, pt, wM, forceFallback, x, y, g[0], g[1], g[2],
                                   fo, th);
     }

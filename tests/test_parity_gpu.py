@@ -155,6 +155,13 @@ CASES = [  # (W, H, s, S, seed): ragged sizes, every supported window class
     # k_solve32f's tile shapes at the extremes: s = 32 (5 x 3 LR grid), a 40 x 3
     # image at s = 2 (one tile row, 2-row LR grid)
     (129, 77, 32, 3, 28), (40, 3, 2, 3, 29),
+    # the pair-table path (packed fp32 pairs) at every compile-time pitch and
+    # its edges: s = 8 / 9 / 10 (pitch 7), 11 / 15 (generic), 16 / 17 / 31
+    # (pitch 5), 33 / 40 (pitch 4); widths off the 32-pixel tile, heights off
+    # the tile rows, LR grids narrower than the pitch
+    (333, 219, 9, 3, 30), (650, 411, 10, 3, 31), (407, 230, 11, 3, 32), (500, 300, 15, 3, 33),
+    (523, 389, 17, 3, 34), (700, 500, 31, 3, 35), (431, 303, 33, 3, 36), (90, 650, 40, 3, 37),
+    (27, 500, 8, 3, 38), (1040, 17, 8, 3, 39), (47, 49, 16, 3, 40),
 ]
 
 
