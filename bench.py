@@ -548,7 +548,7 @@ def run_ours(args, ws, rank, local):
         "executed_fp32": cap.get("executed_fp32"), "capture_stale": cap["stale"],
         "kernel": {"fast": "k_solve32f<Fast, Apply1>", "gnu": "k_solve32f<Gnu, Apply1>",
                    "exact": "k_solve32x<Apply1>"}[args.mode] +
-                  " (fused optimize_field + 1-ch apply_field), Fast / GNU: one launch over "
+                  " (fused optimize_field + 1-ch apply_field): one launch over "
                   "the 16 frames (grid z = frame) after one batched k_frame_prep launch "
                   "(downsample + matte + LR packing)",
         "kernel_ms_basis": "CUDA events around one 16-frame glu_cu_upsample_frames call (the "
@@ -589,8 +589,8 @@ def run_ours(args, ws, rank, local):
         xach = xflops / (x_ms * 1e-3) / 1e12
         roofline["pair_search"] = {
             "mode": "exact", "kernel": "k_solve32x (fused optimize_field + 1-ch apply_field), "
-            "per frame, the next frame's k_frame_prep overlapping on a side stream (one 16-frame "
-            "call / 16)", "kernel_ms": x_ms,
+            "one launch over the 16 frames (grid z = frame) after one batched k_frame_prep launch "
+            "(one 16-frame call / 16)", "kernel_ms": x_ms,
             "algorithmic_flops_per_launch": xflops,
             "achieved": xach, "unit": "TFLOP/s",
             "frac": xach / fp32_tflops, "frac_of_nominal": xach / nominal,

@@ -534,6 +534,9 @@ int frame_kernels(glu_ctx* ctx, const float* frame, const glu_grid* g, const glu
 // side stream into buffer set k % 2 while frame k - 1 is solved on the
 // context stream (the prep is a small grid: it fills the solve's last wave).
 // Prep k waits for solve k - 2 (its buffers); solve k waits for prep k.
+#ifndef GLU_FRAME_BATCH_EXACT
+#define GLU_FRAME_BATCH_EXACT 1  // Exact mode (k_solve32x) also in one launch per batch
+#endif
 #ifndef GLU_FRAME_BATCH
 #define GLU_FRAME_BATCH 1
 #endif
@@ -587,8 +590,9 @@ int frames_pipelined(glu_ctx* ctx, const float* frames, int count, const glu_gri
     return GLU_OK;
 }
 
-// Fast / GNU, S = 3, matte target, no params: the frames go through
-// k_solve32f in batches of up to kFrameBatch per launch (grid z = frame), so
+// Fast / GNU / Exact, S = 3, matte target, no params: the frames go through
+// k_solve32f (Exact: k_solve32x) in batches of up to kFrameBatch per launch
+// (grid z = frame), so
 // the SMs never drain between frames; one batched prep launch per batch, the
 // next batch's on the side stream while this one solves.
 #ifndef GLU_FRAME_BATCH_MAX
@@ -672,7 +676,9 @@ int glu_cu_upsample_frames(glu_ctx* ctx, const float* frames, int count, const g
     const size_t n = npx_of(g), ln = lown_of(g);
     const int ch = targetOp == GLU_TARGET_MATTE ? 1 : 3;
     if (count > 1 && ctx->solver != 1 && !paramsOut && targetOp == GLU_TARGET_MATTE &&
-        solve32f_supported(mode, cfg->windowSide) && GLU_FRAME_BATCH)
+        (solve32f_supported(mode, cfg->windowSide) ||
+         (GLU_FRAME_BATCH_EXACT && solve32x_supported(mode, cfg->windowSide, g->scale))) &&
+        GLU_FRAME_BATCH)
         return frames_batched(ctx, frames, count, g, cfg, mode, out);
     if (count > 1 && ctx->solver != 1 && solve32_supported(mode, cfg->windowSide, g->scale))
         return frames_pipelined(ctx, frames, count, g, cfg, mode, targetOp, out, paramsOut);

@@ -131,12 +131,14 @@ cudaError_t launch_frame_prep_batch(glu_ctx* ctx, cudaStream_t st, const SolveAr
                                     const FrameBatch& fb, char* base, size_t set,
                                     size_t offMatte, size_t offPacked, unsigned* flags);
 // The batch's solve (k_solve32f over fb.frames frames; a = frame 0's args).
+// (Fast / GNU: k_solve32f; Exact: k_solve32x)
 cudaError_t launch_prepped_solve32f_batch(glu_ctx* ctx, const SolveArgs& a, const float4* packed,
                                           int forceFallback, const unsigned* flags,
                                           const FrameBatch& fb);
 bool solve32x_supported(int mode, int S, int s);
 cudaError_t launch_solve32x(glu_ctx* ctx, const SolveArgs& a, const float4* packed,
-                            int forceFallback, const unsigned* nanFlag);
+                            int forceFallback, const unsigned* nanFlag,
+                            const FrameBatch& fb = FrameBatch{});
 cudaError_t launch_solve_list(glu_ctx* ctx, const SolveArgs& a, const uint32_t* pixels,
                               size_t count);
 cudaError_t launch_apply(glu_ctx* ctx, const glu_pixel_params* field, size_t npx,

@@ -473,7 +473,9 @@ cudaError_t launch_prepped_solve32(glu_ctx* ctx, const SolveArgs& a0, const floa
 cudaError_t launch_prepped_solve32f_batch(glu_ctx* ctx, const SolveArgs& a0, const float4* packed,
                                           int forceFallback, const unsigned* flags,
                                           const FrameBatch& fb) {
-    return launch_solve32f(ctx, prepared(a0), packed, forceFallback, flags, fb);
+    const SolveArgs a = prepared(a0);
+    if (a.mode == GLU_MODE_EXACT) return launch_solve32x(ctx, a, packed, forceFallback, flags, fb);
+    return launch_solve32f(ctx, a, packed, forceFallback, flags, fb);
 }
 
 cudaError_t launch_frame_solve32(glu_ctx* ctx, const SolveArgs& a0, float* low, float* matte,

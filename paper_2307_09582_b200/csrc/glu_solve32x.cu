@@ -280,7 +280,9 @@ template <int OUT, int P>
 __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* packed, const XTile& t,
                                             const float4* swin, const float4* tab,
                                             int forceFallback, size_t p, int cx, int cy, float ip0,
-                                            float ip1, float ip2) {
+                                            float ip1, float ip2, size_t th) {
+    // (p: the output index, th: the target offset -- both include this frame's
+    // offset in a batched launch, which only the 1-ch video output uses)
     const int cw = P > 0 ? P : t.cw;
 
     // j-outer scan: pair (i, j) needs only e_j = I_j - I_p and q_j = |e_j|^2
@@ -394,8 +396,8 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
         const uint3 r = solve_double(packed, a.lw, a.lh, a.eps, a.fallbacks, cx, cy, ip0, ip1, ip2);
         w = __uint_as_float(r.z);
         if (OUT == kOutApply1) {
-            wa = __ldg(a.lowT + r.x);
-            wb = __ldg(a.lowT + r.y);
+            wa = __ldg(a.lowT + th + r.x);
+            wb = __ldg(a.lowT + th + r.y);
         } else {
             wa = __uint_as_float(r.x);
             wb = __uint_as_float(r.y);
@@ -444,10 +446,20 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) {
 // owns rows [ty * rows, (ty + 1) * rows).  Dynamic shared memory: [guide:
 // tileH x 96 floats, one TMA (cp.async.bulk.tensor.2d) when useTma][pair
 // table: maxCells x kCellStride][candidate cells: pitch x (mch + 2)].
-template <int OUT, int P>
+template <int OUT, int P, bool BATCH>
 __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS)
     k_solve32x(const __grid_constant__ CUtensorMap tmap, SolveArgs a, const float4* packed,
-               int forceFallback, const unsigned* nanFlag, int maxCells, int rows, int useTma) {
+               int forceFallback, const unsigned* nanFlag, int maxCells, int rows, int useTma,
+               FrameBatch fb) {
+    // BATCH: frame blockIdx.z of a batch of video frames (glu_cu_upsample_frames;
+    // k_solve32f's scheme); the single-frame instantiation compiles the offsets out
+    const int fz = BATCH ? int(blockIdx.z) : 0;
+    if (BATCH) {
+        packed += size_t(fz) * fb.packed;
+        nanFlag += fz;
+    }
+    const size_t fo = BATCH ? size_t(fz) * fb.px : 0, th = BATCH ? size_t(fz) * fb.lowT : 0,
+                 hh = BATCH ? size_t(fz) * fb.high : 0;
     extern __shared__ __align__(1024) float xsm[];
     __shared__ __align__(8) unsigned long long bar;
     const int tileH = kTY * rows;
@@ -462,11 +474,19 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS)
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)),
                      "r"(unsigned(tileH * 96 * 4))
                      : "memory");
-        asm volatile(
-            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-            " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(gtile)),
-            "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(3 * x0), "r"(y0), "r"(smem_u32(&bar))
-            : "memory");
+        if (BATCH)  // a 3-D map over the batch's frames
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(gtile)),
+                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(3 * x0), "r"(y0), "r"(fz),
+                "r"(smem_u32(&bar))
+                : "memory");
+        else
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(gtile)),
+                "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(3 * x0), "r"(y0), "r"(smem_u32(&bar))
+                : "memory");
     }
     forceFallback |= int(__ldg(nanFlag));
     const int pw = a.lw + 2;  // h = 1
@@ -484,7 +504,7 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS)
             const int lx = ocx0 + c - 1, ly = ocy0 + r - 1;
             const bool in = lx >= 0 && ly >= 0 && lx < a.lw && ly < a.lh;
             const unsigned li = in ? unsigned(ly) * unsigned(a.lw) + unsigned(lx) : 0u;
-            v.w = OUT == kOutApply1 ? (in ? __ldg(a.lowT + li) : 0.0f) : __uint_as_float(li);
+            v.w = OUT == kOutApply1 ? (in ? __ldg(a.lowT + th + li) : 0.0f) : __uint_as_float(li);
             wcells[k] = v;
         }
     }
@@ -493,7 +513,7 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS)
             const int r = k / 96, c = k - r * 96;
             const int y = y0 + r;
             gtile[k] = (y < a.H && x0 * 3 + c < a.W * 3)
-                           ? __ldg(a.high + 3 * (size_t(y) * a.W + x0) + c)
+                           ? __ldg(a.high + hh + 3 * (size_t(y) * a.W + x0) + c)
                            : 0.0f;
         }
     }
@@ -552,7 +572,7 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS)
     const int yr = y0 + ty * rows;
     const int yEnd = min(yr + rows, a.H);
     const float* g = gtile + (ty * rows) * 96 + 3 * tx;
-    size_t p = size_t(yr) * a.W + x;
+    size_t p = size_t(yr) * a.W + x + fo;
     // owner-cell row of the current row, advanced when y reaches yNext
     int cy = div_s(yr, a);
     int yNext = (cy + 1) * a.s;
@@ -566,7 +586,7 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS)
             swin += cw;
             tab += ncw * kCellStride;
         }
-        solve_pixel<OUT, P>(a, packed, t, swin, tab, forceFallback, p, cx, cy, g[0], g[1], g[2]);
+        solve_pixel<OUT, P>(a, packed, t, swin, tab, forceFallback, p, cx, cy, g[0], g[1], g[2], th);
     }
 }
 
@@ -588,7 +608,7 @@ int max_pitch(int s) { return (kTX - 1) / s + 4; }
 
 template <int OUT, int P>
 cudaError_t launch_xp(glu_ctx* ctx, const SolveArgs& a, const float4* packed, int forceFallback,
-                      const unsigned* nanFlag) {
+                      const unsigned* nanFlag, const FrameBatch& fb) {
     // Rows per thread: more rows amortise a tile's staging (cells, pair
     // table, guide, two barriers) over more pixels, fewer rows give more
     // tiles and a smaller partial last wave.  Pick the count minimising waves
@@ -613,10 +633,11 @@ cudaError_t launch_xp(glu_ctx* ctx, const SolveArgs& a, const float4* packed, in
         for (int r = 1; r <= kMaxRows; ++r) {
             const size_t sm = smem_of(r);
             if (r > 1 && sm > kSmemCap) break;
-            cudaFuncSetAttribute(k_solve32x<OUT, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(sm));
+            cudaFuncSetAttribute(k_solve32x<OUT, P, false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
             int per = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_solve32x<OUT, P>, kThreads, sm);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_solve32x<OUT, P, false>, kThreads,
+                                                          sm);
             const long slots = long(max(per, 1)) * nsm;
             const long tiles = tilesX * ((a.H + kTY * r - 1) / (kTY * r));
             const float cost = float((tiles + slots - 1) / slots) * (float(r) + kStageCost);
@@ -640,35 +661,44 @@ cudaError_t launch_xp(glu_ctx* ctx, const SolveArgs& a, const float4* packed, in
     int useTma = 0;
     if (a.W % 4 == 0 && (reinterpret_cast<uintptr_t>(a.high) & 15u) == 0) {
         if (auto enc = tensor_map_encoder()) {
-            const cuuint64_t dims[2] = {cuuint64_t(3) * a.W, cuuint64_t(a.H)};
-            const cuuint64_t strides[1] = {cuuint64_t(12) * a.W};
-            const cuuint32_t box[2] = {96u, cuuint32_t(tileH)};
-            const cuuint32_t estr[2] = {1u, 1u};
-            useTma = enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(a.high), dims,
-                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            // (a batch: a third dimension over its frames, fb.high floats apart)
+            const cuuint32_t rank = fb.frames > 1 ? 3u : 2u;
+            const cuuint64_t dims[3] = {cuuint64_t(3) * a.W, cuuint64_t(a.H),
+                                        cuuint64_t(fb.frames)};
+            const cuuint64_t strides[2] = {cuuint64_t(12) * a.W, cuuint64_t(4) * fb.high};
+            const cuuint32_t box[3] = {96u, cuuint32_t(tileH), 1u};
+            const cuuint32_t estr[3] = {1u, 1u, 1u};
+            useTma = (fb.frames == 1 || (fb.high * 4) % 16 == 0) &&
+                     enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<float*>(a.high),
+                         dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
         }
     }
     const size_t smem = smem_of(rows);
-    cudaError_t e = cudaFuncSetAttribute(k_solve32x<OUT, P>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    // (only the 1-ch video output is launched as a batch)
+    constexpr bool kCanBatch = OUT == kOutApply1;
+    const bool batch = kCanBatch && fb.frames > 1;
+    if (fb.frames > 1 && !batch) return cudaErrorInvalidValue;
+    auto kern = batch ? k_solve32x<OUT, P, kCanBatch> : k_solve32x<OUT, P, false>;
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    dim3 grid(unsigned(tilesX), (a.H + tileH - 1) / tileH);
-    k_solve32x<OUT, P><<<grid, kThreads, smem, ctx->stream>>>(tmap, a, packed, forceFallback,
-                                                              nanFlag, maxCells, rows, useTma);
+    dim3 grid(unsigned(tilesX), (a.H + tileH - 1) / tileH, unsigned(fb.frames));
+    kern<<<grid, kThreads, smem, ctx->stream>>>(tmap, a, packed, forceFallback, nanFlag, maxCells,
+                                                rows, useTma, fb);
     ++ctx->launches;
     return cudaGetLastError();
 }
 
 template <int OUT>
 cudaError_t launch_xo(glu_ctx* ctx, const SolveArgs& a, const float4* packed, int forceFallback,
-                      const unsigned* nanFlag) {
+                      const unsigned* nanFlag, const FrameBatch& fb) {
     switch (max_pitch(a.s)) {  // s = 8: 7; s = 16: 5; s >= 32: 4
-        case 4: return launch_xp<OUT, 4>(ctx, a, packed, forceFallback, nanFlag);
-        case 5: return launch_xp<OUT, 5>(ctx, a, packed, forceFallback, nanFlag);
-        case 7: return launch_xp<OUT, 7>(ctx, a, packed, forceFallback, nanFlag);
-        default: return launch_xp<OUT, 0>(ctx, a, packed, forceFallback, nanFlag);
+        case 4: return launch_xp<OUT, 4>(ctx, a, packed, forceFallback, nanFlag, fb);
+        case 5: return launch_xp<OUT, 5>(ctx, a, packed, forceFallback, nanFlag, fb);
+        case 7: return launch_xp<OUT, 7>(ctx, a, packed, forceFallback, nanFlag, fb);
+        default: return launch_xp<OUT, 0>(ctx, a, packed, forceFallback, nanFlag, fb);
     }
 }
 
@@ -679,12 +709,12 @@ bool solve32x_supported(int mode, int S, int s) {
 }
 
 cudaError_t launch_solve32x(glu_ctx* ctx, const SolveArgs& a, const float4* packed,
-                            int forceFallback, const unsigned* nanFlag) {
+                            int forceFallback, const unsigned* nanFlag, const FrameBatch& fb) {
     if (a.params && !a.lowT && !a.errOut)
-        return launch_xo<kOutParams>(ctx, a, packed, forceFallback, nanFlag);
+        return launch_xo<kOutParams>(ctx, a, packed, forceFallback, nanFlag, fb);
     if (!a.params && a.lowT && a.channels == 1 && !a.errOut)
-        return launch_xo<kOutApply1>(ctx, a, packed, forceFallback, nanFlag);
-    return launch_xo<kOutGeneric>(ctx, a, packed, forceFallback, nanFlag);
+        return launch_xo<kOutApply1>(ctx, a, packed, forceFallback, nanFlag, fb);
+    return launch_xo<kOutGeneric>(ctx, a, packed, forceFallback, nanFlag, fb);
 }
 
 }  // namespace glu_cu

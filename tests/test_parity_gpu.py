@@ -493,9 +493,11 @@ def test_joint_unchanged_pixel_pass_matches_oracle(glu, oracle, mode, image, s):
 
 
 @pytest.mark.parametrize("W,H,s,mode", [(200, 136, 8, "fast"), (198, 131, 6, "fast"),
-                                        (256, 96, 4, "gnu")])
+                                        (256, 96, 4, "gnu"), (200, 136, 8, "exact"),
+                                        (198, 131, 5, "exact"), (320, 200, 16, "exact")])
 def test_frame_batches_match_single_frames(glu, W, H, s, mode):
-    """glu_cu_upsample_frames with a 1-channel matte launches k_solve32f over
+    """glu_cu_upsample_frames with a 1-channel matte launches k_solve32f (Exact
+    mode: k_solve32x) over
     batches of up to 16 frames (grid z = frame; a 3-D tensor map when the rows
     are 16-byte aligned, else the threads stage each frame's guide); 35 frames
     = batches of 16, 16 and 3 on two buffer groups.  Every frame equals its
