@@ -653,7 +653,10 @@ cudaError_t launch_xp(glu_ctx* ctx, const SolveArgs& a, const float4* packed, in
         memo[4] = key;
         memo[5] = rows;
     }
-    const int rows = memo[5];
+#ifndef GLU_X_BATCH_ROWS
+#define GLU_X_BATCH_ROWS 6  // rows per thread of a batched launch (no wave tail to fit; 5 / 6 / 7 / 8: 0.2042 / 0.2000 / 0.2007 / 0.2029 ms per 4K frame)
+#endif
+    const int rows = GLU_X_BATCH_ROWS > 0 && fb.frames > 1 ? GLU_X_BATCH_ROWS : memo[5];
     const int tileH = kTY * rows;
     const int mch = (tileH - 1) / a.s + 2;
     const int maxCells = mcw * mch;
