@@ -656,9 +656,11 @@ cudaError_t launch_xp(glu_ctx* ctx, const SolveArgs& a, const float4* packed, in
 #ifndef GLU_X_BATCH_ROWS
 #define GLU_X_BATCH_ROWS 6  // rows per thread of a batched launch (no wave tail to fit; 5 / 6 / 7 / 8: 0.2042 / 0.2000 / 0.2007 / 0.2029 ms per 4K frame)
 #endif
-    // (never more than the single-frame pick, which respects kSmemCap)
-    const int rows =
-        GLU_X_BATCH_ROWS > 0 && fb.frames > 1 ? min(GLU_X_BATCH_ROWS, memo[5]) : memo[5];
+    // (as long as the taller tile respects kSmemCap: small scales keep the single-frame pick)
+    const int rows = GLU_X_BATCH_ROWS > 0 && fb.frames > 1 && GLU_X_BATCH_ROWS <= kMaxRows &&
+                             smem_of(GLU_X_BATCH_ROWS) <= kSmemCap
+                         ? GLU_X_BATCH_ROWS
+                         : memo[5];
     const int tileH = kTY * rows;
     const int mch = (tileH - 1) / a.s + 2;
     const int maxCells = mcw * mch;
