@@ -206,6 +206,9 @@ int glu_ctx_create(int device, glu_ctx** out) {
     e = cudaEventCreateWithFlags(&c->switchEv, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_counters, 8 * sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMemset(c->d_counters, 0, 8 * sizeof(unsigned long long));
+    if (e == cudaSuccess)
+        e = cudaHostAlloc(reinterpret_cast<void**>(&c->h_rb), 16 * sizeof(uint32_t),
+                          cudaHostAllocDefault);
     if (e != cudaSuccess) {
         cudaStreamDestroy(c->own);
         delete c;
@@ -224,6 +227,7 @@ int glu_ctx_destroy(glu_ctx* ctx) {
     for (void* h : ctx->hbuf)
         if (h) cudaFreeHost(h);
     cudaFree(ctx->d_counters);
+    if (ctx->h_rb) cudaFreeHost(ctx->h_rb);
     for (cudaEvent_t ev : ctx->ev)
         if (ev) cudaEventDestroy(ev);
     if (ctx->switchEv) cudaEventDestroy(ctx->switchEv);

@@ -249,10 +249,11 @@ int ccl_sparse(glu_ctx* ctx, const float* errors, int W, int H, float thr, size_
         k_sel_write<<<unsigned(nch), kSelWords, 0, st>>>(selBits, coff, mp);
         e = cudaGetLastError();
     }
-    uint32_t m = 0;
-    if (e == cudaSuccess) e = cudaMemcpyAsync(&m, coff + nch, 4, cudaMemcpyDeviceToHost, st);
+    // (read-backs through the context's pinned words)
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ctx->h_rb, coff + nch, 4, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return fail_cuda(e, "ccl select");
+    const uint32_t m = ctx->h_rb[0];
     ctx->launches += 4;
     // parent | isRoot | rank | keys | keys2 | vals2 (m words each)
     uint32_t* w = static_cast<uint32_t*>(scratch(ctx, S_CCL_MISC, size_t(m) * 24 + 64));
@@ -281,7 +282,7 @@ int ccl_sparse(glu_ctx* ctx, const float* errors, int W, int H, float thr, size_
     if (!temp) return GLU_ENOMEM;
     uint32_t* off = reinterpret_cast<uint32_t*>(static_cast<char*>(temp) + ((tb + 255) & ~size_t(255)));
     e = cub::DeviceScan::ExclusiveSum(temp, tbScan, isRoot, rank, int(m), st);
-    uint32_t tail[2] = {0, 0};
+    uint32_t* tail = ctx->h_rb + 2;
     if (e == cudaSuccess) e = cudaMemcpyAsync(tail, rank + m - 1, 4, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(tail + 1, isRoot + m - 1, 4, cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);

@@ -33,6 +33,10 @@ struct glu_ctx {
     cudaStream_t stream = nullptr;
     unsigned long long launches = 0;
     unsigned long long* d_counters = nullptr;  // [0] = fp64 fallback pixels
+    // Pinned host words for the joint loop's small read-backs (component
+    // counts, sweep verdicts): a device-to-host copy into pageable memory is
+    // staged by the driver and costs several microseconds more per sync.
+    uint32_t* h_rb = nullptr;  // 16 words
     // Grow-only scratch slots (device memory).
     static constexpr int kSlots = 24;
     void* buf[kSlots] = {};

@@ -1942,9 +1942,9 @@ int joint_sweep(glu_ctx* ctx, const float* high, float* low, glu_pixel_params* f
         if (rc) return rc;
         e = cudaSuccess;
     }
-    int res[4];
+    int* res = reinterpret_cast<int*>(ctx->h_rb + 4);  // (pinned: glu_internal.h)
     if (e == cudaSuccess)
-        e = cudaMemcpyAsync(res, js.result, sizeof(res), cudaMemcpyDeviceToHost, ctx->stream);
+        e = cudaMemcpyAsync(res, js.result, 4 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) return fail_cuda(e, "trial sweep");
     *accepted = res[0];
