@@ -1240,11 +1240,30 @@ __global__ void __launch_bounds__(kSeqThreads) k_trial_sweep(TrialState t, Trial
 // affected set exceeds a CTA's private buffers get the whole grid.
 // With raw != 0 the plain cell box is written (for level scheduling); `ids`
 // (optional) lists the components, box k belonging to component ids[k].
+// The scheduler's per-trial state, initialised by the kernel that computes
+// the trial's box (replaces five memsets per sweep): pred = 0 (with the 16
+// counter words behind it), queue = specQ = -1, specState = 0, specSnap =
+// 0x7f7f7f7f.  Null `pred`: boxes only.
+struct SchedInit {
+    unsigned long long* pred;
+    int *queue, *specState, *specQ;
+    uint32_t* specSnap;
+};
+
 __global__ void k_trial_boxes(const uint32_t* __restrict__ off, const uint32_t* __restrict__ px,
                               const uint32_t* __restrict__ ids, int ncomp, int W, int s, int lw,
-                              int lh, int h, int literal, int raw, int4* __restrict__ boxes) {
+                              int lh, int h, int literal, int raw, int4* __restrict__ boxes,
+                              SchedInit si) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (si.pred && blockIdx.x == 0 && threadIdx.x < 8) si.pred[ncomp + threadIdx.x] = 0ull;
     if (warp >= ncomp) return;
+    if (si.pred && lane == 0) {
+        si.pred[warp] = 0ull;
+        si.queue[warp] = -1;
+        si.specState[warp] = 0;
+        si.specSnap[warp] = 0x7f7f7f7fu;
+        si.specQ[warp] = -1;
+    }
     const uint32_t comp = ids ? ids[warp] : uint32_t(warp);
     const uint32_t b0 = off[comp], b1 = off[comp + 1];
     int x0 = lw, y0 = lh, x1 = -1, y1 = -1;
@@ -1843,16 +1862,14 @@ int run_sched(glu_ctx* ctx, const TrialState& t, const JointScratch& js, const g
     int* specQ = reinterpret_cast<int*>(specSnap + n);
     uint32_t* parkOff = reinterpret_cast<uint32_t*>(specQ + n);
     cudaStream_t st = ctx->stream;
-    cudaError_t e = cudaMemsetAsync(pred, 0, n * 8 + 64, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(queue, 0xff, n * sizeof(int), st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(specState, 0, n * sizeof(int), st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(specSnap, 0x7f, n * sizeof(int), st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(specQ, 0xff, n * sizeof(int), st);
-    if (e != cudaSuccess) return fail_cuda(e, "trial schedule");
+    cudaError_t e = cudaSuccess;
     const int reach = 2 * (cfg.windowSide / 2);
+    // (the boxes kernel also initialises pred + the counters, the queues and
+    // the speculation state: five memsets per sweep fewer, C2 2.26 -> 2.24 ms,
+    // C4 2.82 -> 2.78 ms)
     k_trial_boxes<<<blocks_for(n * 32, 256), 256, 0, st>>>(
         off, px, ids, int(n), g.highW, g.scale, g.lowW, g.lowH, cfg.windowSide / 2,
-        cfg.literalComponentUpdate, 0, boxes);
+        cfg.literalComponentUpdate, 0, boxes, SchedInit{pred, queue, specState, specQ, specSnap});
     k_suffix_top<<<1, 1024, 0, st>>>(boxes, int(n), sufTop);
     int* first = reinterpret_cast<int*>(parkOff + n + 1);
     k_trial_preds<<<blocks_for(n * 32, 256), 256, 0, st>>>(boxes, sufTop, int(n), reach, pred,
@@ -2010,7 +2027,7 @@ int component_boxes(glu_ctx* ctx, const uint32_t* off, const uint32_t* px, size_
     if (n == 0) return GLU_OK;
     k_trial_boxes<<<blocks_for(n * 32, 256), 256, 0, ctx->stream>>>(
         off, px, nullptr, int(n), g.highW, g.scale, g.lowW, g.lowH, 0, 0, 1,
-        reinterpret_cast<int4*>(boxes));
+        reinterpret_cast<int4*>(boxes), SchedInit{});
     ++ctx->launches;
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? GLU_OK : fail_cuda(e, "component boxes");
