@@ -304,11 +304,20 @@ def run_c5(args, ws, rank, dist, hbm_gbs):
         "workload": f"C5 (configs[4]): C4 joint field of the 7680x4320 s=16 scene, {nt} RGB "
                     f"channel-mix edits of its 480x270 LR image, HR row bands over {ws} GPU(s)",
         "metric": "HR Mpix/s (apply of every edit to the whole 8K frame)",
-        "value": total_px / (ms_b * 1e-3) / 1e6, "unit": "HR Mpix/s", "n_gpus": ws,
-        "scaling": "strong", "ms_per_pass": ms_b,
-        "broadcast_bytes_per_target": grid.lowW * grid.lowH * 12 if ws > 1 else 0,
+        # configs[4]'s edits are colour-matrix operators, so the headline is the
+        # reference's apply_operator + apply_field as one call per edit and band
+        # (nothing to exchange between ranks); the black-box case (targets held
+        # by rank 0, broadcast per edit) is reported beside it
+        "value": total_px / (ms_f * 1e-3) / 1e6, "unit": "HR Mpix/s", "n_gpus": ws,
+        "scaling": "strong", "ms_per_pass": ms_f,
+        "value_path": "fused_operator",
         "fused_operator": {"value": total_px / (ms_f * 1e-3) / 1e6, "ms_per_pass": ms_f,
                            "api": "glu_cu_apply_operator_field_band (no broadcast)"},
+        "black_box_broadcast": {"value": total_px / (ms_b * 1e-3) / 1e6, "ms_per_pass": ms_b,
+                                "api": "glu_cu_apply_field_band after a per-edit broadcast of "
+                                       "the edited LR target from rank 0",
+                                "broadcast_bytes_per_target":
+                                    grid.lowW * grid.lowH * 12 if ws > 1 else 0},
         "apply_kernel": {"kernel": "k_op_pack_target4 + k_apply3b (bulk-copy tiles; k_apply3v for "
                                    "a sub-tile tail)", "ms_mean": k_ms,
                          "algorithmic_bytes_per_launch": nbytes,
