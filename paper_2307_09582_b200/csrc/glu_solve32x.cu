@@ -657,6 +657,10 @@ cudaError_t launch_xp(glu_ctx* ctx, const SolveArgs& a, const float4* packed, in
 #define GLU_X_BATCH_ROWS 6  // rows per thread of a batched launch (no wave tail to fit; 5 / 6 / 7 / 8: 0.2042 / 0.2000 / 0.2007 / 0.2029 ms per 4K frame)
 #endif
     // (as long as the taller tile respects kSmemCap: small scales keep the single-frame pick)
+#ifndef GLU_X_ROWS
+#define GLU_X_ROWS 0  // > 0: forces the single-frame rows per thread (A/B builds)
+#endif
+    if (GLU_X_ROWS > 0 && smem_of(GLU_X_ROWS) <= kSmemCap) memo[5] = GLU_X_ROWS;
     const int rows = GLU_X_BATCH_ROWS > 0 && fb.frames > 1 && GLU_X_BATCH_ROWS <= kMaxRows &&
                              smem_of(GLU_X_BATCH_ROWS) <= kSmemCap
                          ? GLU_X_BATCH_ROWS
