@@ -35,7 +35,11 @@ namespace {
 #endif
 constexpr int kTX = 32, kTY = GLU_X_TY, kThreads = kTX * kTY;
 constexpr int kPairs = 36;       // i < j over 9 candidates
-constexpr int kCellStride = 37;  // float4 per owner cell (592 B: bank-spread)
+#ifndef GLU_X_COMPACT
+#define GLU_X_COMPACT 1  // the compact pair table (A/B knob; 0: 36 float4 slots per cell)
+#endif
+// float4 per owner cell, bank-spread (compact: 464 B; else 592 B)
+constexpr int kCellStride = GLU_X_COMPACT ? 29 : 37;
 constexpr int kMaxRows = 8;               // pixels per thread (rows y, y + kTY, ...): 1..8
 constexpr int kSmemCap = 40 * 1024;       // per CTA, so that GLU_X_MIN_BLOCKS CTAs fit
 constexpr float kStageCost = 0.3f;        // a tile's staging, in units of one row of pixels
@@ -111,20 +115,39 @@ __device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
     return r;
 }
 
-// The pair table of one owner cell: D'_ij (i < j) column by column (column j's
-// j entries start at j (j - 1) / 2), rows two at a time: for even i with
-// i + 1 < j the two float4 slots of (i, j) and (i + 1, j) hold {x_i, x_i+1,
-// y_i, y_i+1} and {z_i, z_i+1, -, -} (packed operands for one LDS.128 + one
-// LDS.64); an odd column's last row (j - 1, j) is a plain {x, y, z, -}.
-__device__ __forceinline__ constexpr int col_base(int j) { return j * (j - 1) / 2; }
+// The pair table of one owner cell: D'_ij (i < j) column by column, rows two
+// at a time.  Compact layout (28 float4): the 16 two-row slots (column j's
+// floor(j / 2) slots start at floor((j - 1)^2 / 4)) as float4 {x_i, x_i+1,
+// y_i, y_i+1} at [0, 16) and float2 {z_i, z_i+1} at [16, 24) -- packed
+// operands for one LDS.128 + one LDS.64 -- then the odd columns' last rows
+// (j - 1, j) as plain {x, y, z, -} at 24 + (j - 1) / 2.  (The first version
+// kept 36 float4 slots, column j at j (j - 1) / 2: 592 B per cell, 7 CTAs per
+// SM at C3 instead of 8.)
+__device__ __forceinline__ constexpr int col_base(int j) {
+    return GLU_X_COMPACT ? (j - 1) * (j - 1) / 4 : j * (j - 1) / 2;
+}
+struct PairSlot {  // where the rows (i, i + 1), i even, of column j live
+    const float4* xy;
+    const float2* z;
+};
+__device__ __forceinline__ PairSlot pair_slot(const float4* tab, int i, int j) {
+    if (GLU_X_COMPACT) {
+        const int s = col_base(j) + i / 2;
+        return PairSlot{tab + s, reinterpret_cast<const float2*>(tab + 16) + s};
+    }
+    return PairSlot{tab + col_base(j) + i, reinterpret_cast<const float2*>(tab + col_base(j) + i + 1)};
+}
+__device__ __forceinline__ const float4* single_slot(const float4* tab, int j) {  // (j - 1, j), j odd
+    return GLU_X_COMPACT ? tab + 24 + (j - 1) / 2 : tab + col_base(j) + (j - 1);
+}
 __device__ __forceinline__ float3 tab_pair(const float4* tab, int i, int j) {
-    const int b = col_base(j);
     if (!(i & 1) && i + 1 == j) {
-        const float4 d = tab[b + i];
+        const float4 d = *single_slot(tab, j);
         return make_float3(d.x, d.y, d.z);
     }
-    const float* f = reinterpret_cast<const float*>(tab + b + (i & ~1)) + (i & 1);
-    return make_float3(f[0], f[2], f[4]);
+    const PairSlot p = pair_slot(tab, i & ~1, j);
+    const float* f = reinterpret_cast<const float*>(p.xy) + (i & 1);
+    return make_float3(f[0], f[2], reinterpret_cast<const float*>(p.z)[i & 1]);
 }
 
 // Lexicographic pair k (i <= j over 9 candidates: rows start at 0, 9, 17,
@@ -321,17 +344,17 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
         const f32x2 E0 = pk2(e0, e0), E1 = pk2(e1, e1), E2 = pk2(e2, e2), Qm = pk2(qm, qm);
 #pragma unroll
         for (int i = 0; i < j; i += 2) {
-            const float4* slot = tab + col_base(j) + i;
             if (i + 1 < j) {
-                const ulonglong2 dxy = *reinterpret_cast<const ulonglong2*>(slot);
-                const f32x2 dz = *reinterpret_cast<const f32x2*>(slot + 1);
+                const PairSlot ps = pair_slot(tab, i, j);
+                const ulonglong2 dxy = *reinterpret_cast<const ulonglong2*>(ps.xy);
+                const f32x2 dz = *reinterpret_cast<const f32x2*>(ps.z);
                 const f32x2 dn = fma2(E0, dxy.x, fma2(E1, dxy.y, mul2(E2, dz)));
                 float n0, n1, t0, t1;
                 upk2(dn, n0, n1);
                 upk2(fma2(pk2(-n0, -n1), dn, Qm), t0, t1);
                 track_key2(K1, K2, pack_key(t0, i, kmask), pack_key(t1, i + 1, kmask));
             } else {
-                const float4 d = *slot;
+                const float4 d = *single_slot(tab, j);
                 const float dn = __fmaf_rn(e0, d.x, __fmaf_rn(e1, d.y, e2 * d.z));
                 pend = pack_key(__fmaf_rn(-dn, dn, qm), i, kmask);
             }
@@ -541,14 +564,15 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS)
         const float den = __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmaf_rn(d0, d0, eps)));
         // D' = D / sqrt(den): then obj_ij = q_j - (e_j . D')^2
         const float r = rsqrt_approx(den);
-        float4* slot = table + cell * kCellStride + col_base(tj) + (ti & ~1);
+        float4* ctab = table + cell * kCellStride;
         if (!(ti & 1) && ti + 1 == tj) {
-            *slot = make_float4(d0 * r, d1 * r, d2 * r, 0.0f);
+            *const_cast<float4*>(single_slot(ctab, tj)) = make_float4(d0 * r, d1 * r, d2 * r, 0.0f);
         } else {  // lane ti & 1 of the two-row slots
-            float* f = reinterpret_cast<float*>(slot) + (ti & 1);
+            const PairSlot ps = pair_slot(ctab, ti & ~1, tj);
+            float* f = const_cast<float*>(reinterpret_cast<const float*>(ps.xy)) + (ti & 1);
             f[0] = d0 * r;
             f[2] = d1 * r;
-            f[4] = d2 * r;
+            const_cast<float*>(reinterpret_cast<const float*>(ps.z))[ti & 1] = d2 * r;
         }
         lx += kCellStep;
         while (lx >= ncw) {
@@ -654,7 +678,7 @@ cudaError_t launch_xp(glu_ctx* ctx, const SolveArgs& a, const float4* packed, in
         memo[5] = rows;
     }
 #ifndef GLU_X_BATCH_ROWS
-#define GLU_X_BATCH_ROWS 6  // rows per thread of a batched launch (no wave tail to fit; 5 / 6 / 7 / 8: 0.2042 / 0.2000 / 0.2007 / 0.2029 ms per 4K frame)
+#define GLU_X_BATCH_ROWS 8  // rows per thread of a batched launch (no wave tail to fit; compact table: 6 / 7 / 8 = 0.1996 / 0.2007 / 0.1981 ms per 4K frame; 36-slot table: 5 / 6 / 7 / 8 = 0.2042 / 0.2000 / 0.2007 / 0.2029)
 #endif
     // (as long as the taller tile respects kSmemCap: small scales keep the single-frame pick)
 #ifndef GLU_X_ROWS
