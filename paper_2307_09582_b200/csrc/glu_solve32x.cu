@@ -104,6 +104,11 @@ __device__ __forceinline__ f32x2 pk2(float lo, float hi) {
 __device__ __forceinline__ void upk2(f32x2 v, float& lo, float& hi) {
     asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
 }
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+    f32x2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
 __device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
     f32x2 r;
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
@@ -295,6 +300,9 @@ struct XTile {
 };
 
 enum Out { kOutParams = 0, kOutApply1 = 1, kOutGeneric = 2 };
+#ifndef GLU_X_PCELLS
+#define GLU_X_PCELLS 1  // e_j, q_j of candidates (3r, 3r + 1) in packed pairs (A/B knob)
+#endif
 
 // One HR pixel with guide colour (ip0, ip1, ip2): the pair search, tie
 // recovery, weight and the fused epilogues.  `swin` = its owner cell's window
@@ -302,8 +310,12 @@ enum Out { kOutParams = 0, kOutApply1 = 1, kOutGeneric = 2 };
 template <int OUT, int P>
 __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* packed, const XTile& t,
                                             const float4* swin, const float4* tab,
-                                            int forceFallback, size_t p, int cx, int cy, float ip0,
-                                            float ip1, float ip2, size_t th) {
+                                            const float4* pwin, int forceFallback, size_t p, int cx,
+                                            int cy, float ip0, float ip1, float ip2, size_t th) {
+    // (pwin: the window in the pair cells -- position (r, c) holds the colours
+    // of the staged cells (r, c) and (r, c + 1) as {x, x', y, y'}, {z, z'} --
+    // so a window row's first two candidates are differenced and squared in
+    // packed pairs, lane for lane the scalar sequence)
     // (p: the output index, th: the target offset -- both include this frame's
     // offset in a batched launch, which only the 1-ch video output uses)
     const int cw = P > 0 ? P : t.cw;
@@ -331,11 +343,31 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
     const unsigned kmask = 0xfffffff0u | (unsigned(a.W) >> 31);
     float qmin = kInf, K1 = kInf, K2 = kInf;
     int bj = 0;
+    f32x2 PE0 = 0, PE1 = 0, PE2 = 0, PQ = 0;  // candidates (3r, 3r + 1)
 #pragma unroll
     for (int j = 0; j < 9; ++j) {
-        const float4 v = swin[(j / 3) * cw + j % 3];
-        const float e0 = v.x - ip0, e1 = v.y - ip1, e2 = v.z - ip2;
-        const float qj = __fmaf_rn(e2, e2, __fmaf_rn(e1, e1, __fmul_rn(e0, e0)));
+        float e0, e1, e2, qj;
+        if (GLU_X_PCELLS && j % 3 != 2) {
+            if (j % 3 == 0) {
+                const float4* ps = pwin + 2 * ((j / 3) * cw);
+                const ulonglong2 xy = *reinterpret_cast<const ulonglong2*>(ps);
+                const f32x2 z = *reinterpret_cast<const f32x2*>(ps + 1);
+                PE0 = add2(xy.x, pk2(-ip0, -ip0));
+                PE1 = add2(xy.y, pk2(-ip1, -ip1));
+                PE2 = add2(z, pk2(-ip2, -ip2));
+                PQ = fma2(PE2, PE2, fma2(PE1, PE1, mul2(PE0, PE0)));
+            }
+            float o0, o1, o2, oq;  // the other lane
+            if (j % 3 == 0) {
+                upk2(PE0, e0, o0), upk2(PE1, e1, o1), upk2(PE2, e2, o2), upk2(PQ, qj, oq);
+            } else {
+                upk2(PE0, o0, e0), upk2(PE1, o1, e1), upk2(PE2, o2, e2), upk2(PQ, oq, qj);
+            }
+        } else {
+            const float4 v = swin[(j / 3) * cw + j % 3];
+            e0 = v.x - ip0, e1 = v.y - ip1, e2 = v.z - ip2;
+            qj = __fmaf_rn(e2, e2, __fmaf_rn(e1, e1, __fmul_rn(e0, e0)));
+        }
         const float qm = __fmaf_rn(qj, kOneMinusE, -1e-36f);
         qmin = fminf(qmin, qj);
         const float k1in = K1;
@@ -490,6 +522,8 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS)
     float4* table = reinterpret_cast<float4*>(xsm + size_t(tileH) * 96);
     float4* wcells = table + maxCells * kCellStride;
     const int tx = threadIdx.x % kTX, ty = threadIdx.x / kTX;
+    // (pair cells behind the cells: 2 float4 per position, the cells' pitch)
+    float4* pcells = wcells + (P > 0 ? P : (kTX - 1) / a.s + 4) * ((tileH - 1) / a.s + 4);
     const int x0 = blockIdx.x * kTX, y0 = blockIdx.y * tileH;
     if (useTma && threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
@@ -529,6 +563,11 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS)
             const unsigned li = in ? unsigned(ly) * unsigned(a.lw) + unsigned(lx) : 0u;
             v.w = OUT == kOutApply1 ? (in ? __ldg(a.lowT + th + li) : 0.0f) : __uint_as_float(li);
             wcells[k] = v;
+            if (GLU_X_PCELLS && c < ncw + 1) {
+                const float4 v1 = __ldg(packed + size_t(ocy0 + r) * pw + (ocx0 + c + 1));
+                pcells[2 * k] = make_float4(v.x, v1.x, v.y, v1.y);
+                pcells[2 * k + 1] = make_float4(v.z, v1.z, 0.0f, 0.0f);
+            }
         }
     }
     if (!useTma) {  // the guide rows are not 16-byte aligned: staged by the threads
@@ -602,6 +641,7 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS)
     int yNext = (cy + 1) * a.s;
     const float4* swin = wcells + (cy - ocy0) * cw + (cx - ocx0);
     const float4* tab = table + ((cy - ocy0) * ncw + (cx - ocx0)) * kCellStride;
+    const float4* pwin = pcells + 2 * ((cy - ocy0) * cw + (cx - ocx0));
 #pragma unroll 1
     for (int y = yr; y < yEnd; ++y, g += 96, p += a.W) {
         if (y == yNext) {
@@ -609,8 +649,10 @@ __global__ void __launch_bounds__(kThreads, GLU_X_MIN_BLOCKS)
             yNext += a.s;
             swin += cw;
             tab += ncw * kCellStride;
+            pwin += 2 * cw;
         }
-        solve_pixel<OUT, P>(a, packed, t, swin, tab, forceFallback, p, cx, cy, g[0], g[1], g[2], th);
+        solve_pixel<OUT, P>(a, packed, t, swin, tab, pwin, forceFallback, p, cx, cy, g[0], g[1], g[2],
+                            th);
     }
 }
 
@@ -646,7 +688,8 @@ cudaError_t launch_xp(glu_ctx* ctx, const SolveArgs& a, const float4* packed, in
     auto smem_of = [&](int r) {
         const int mch = (kTY * r - 1) / a.s + 2;
         return sizeof(float) * size_t(kTY * r) * 96 +
-               sizeof(float4) * (size_t(mcw * mch) * kCellStride + size_t(pitch) * (mch + 2));
+               sizeof(float4) * (size_t(mcw * mch) * kCellStride +
+                                 (GLU_X_PCELLS ? 3 : 1) * size_t(pitch) * (mch + 2));
     };
     thread_local int memo[6] = {-1, 0, 0, 0, -1, 1};  // device, s, W, H, key -> rows
     const int key = OUT * 64 + P;
