@@ -126,6 +126,16 @@ constexpr int kCellF4 = 9;
 // (GNU mode -- stage A only -- measured 2.5 % slower with the table: scalar)
 template <int MODE, int P>
 __host__ __device__ constexpr bool use_pairs() { return P > 0 && MODE == GLU_MODE_FAST; }
+// GNU mode instead reads a pair-cell copy of the staged cells (position (r, c)
+// = cells (r, c), (r, c + 1) interleaved: {x, x', y, y'}, {z, z'}): a window
+// row's first two candidates in packed pairs, nothing to build per owner cell.
+#ifndef GLU_F_GNU_PCELLS
+#define GLU_F_GNU_PCELLS 1
+#endif
+template <int MODE, int P>
+__host__ __device__ constexpr bool use_pcells() {
+    return GLU_F_GNU_PCELLS && P > 0 && MODE == GLU_MODE_GNU;
+}
 #ifndef GLU_F_PK_A
 #define GLU_F_PK_A 1  // stage A in packed pairs (A/B knob)
 #endif
@@ -333,6 +343,7 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
     // e = I_j - I_p and q_j for slot k's two candidates in packed registers,
     // lane for lane the scalar operations below
     f32x2 E0[5], E1[5], E2[5], Q[5];
+    float keys[9];
     if (use_pairs<MODE, P>()) {
         const f32x2 n0 = pk2(-ip0, -ip0), n1 = pk2(-ip1, -ip1), n2 = pk2(-ip2, -ip2);
 #pragma unroll
@@ -362,6 +373,27 @@ __device__ __forceinline__ void solve_pixel(const SolveArgs& a, const float4* pa
             else
                 track_key(K1a, K2a, k0);
         }
+    } else if (use_pcells<MODE, P>()) {
+        // (ptab = the window in the pair cells)
+        const f32x2 n0 = pk2(-ip0, -ip0), n1 = pk2(-ip1, -ip1), n2 = pk2(-ip2, -ip2);
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            const float4* ps = ptab + 2 * (r * cw);
+            const ulonglong2 sxy = *reinterpret_cast<const ulonglong2*>(ps);
+            const f32x2 sz = *reinterpret_cast<const f32x2*>(ps + 1);
+            const f32x2 e0 = add2(sxy.x, n0), e1 = add2(sxy.y, n1), e2 = add2(sz, n2);
+            float q0, q1;
+            upk2(fma2(e2, e2, fma2(e1, e1, mul2(e0, e0))), q0, q1);
+            keys[3 * r] = key_pack(q0, 3 * r, kmask);
+            keys[3 * r + 1] = key_pack(q1, 3 * r + 1, kmask);
+            const float4 v = swin[r * cw + 2];
+            const float d0 = v.x - ip0, d1 = v.y - ip1, d2 = v.z - ip2;
+            keys[3 * r + 2] = key_pack(
+                __fmaf_rn(d2, d2, __fmaf_rn(d1, d1, __fmul_rn(d0, d0))), 3 * r + 2, kmask);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; j += 2) track_key2(K1a, K2a, keys[j], keys[j + 1]);
+        track_key(K1a, K2a, keys[8]);
     } else {
 #pragma unroll
         for (int j = 0; j < 9; ++j) {
@@ -623,9 +655,16 @@ __global__ void __launch_bounds__(kThreads, GLU_F_MIN_BLOCKS)
             const unsigned li = in ? unsigned(ly) * unsigned(a.lw) + unsigned(lx) : 0u;
             v.w = OUT == kOutApply1 ? (in ? __ldg(a.lowT + th + li) : 0.0f) : __uint_as_float(li);
             wcells[k] = v;
+            if (use_pcells<MODE, P>() && c < ncw + 1) {  // pair cells behind the cells
+                const float4 v1 = __ldg(packed + size_t(ocy0 + r) * pw + (ocx0 + c + 1));
+                float4* pc = wcells + P * ((tileH - 1) / a.s + 4) + 2 * k;
+                pc[0] = make_float4(v.x, v1.x, v.y, v1.y);
+                pc[1] = make_float4(v.z, v1.z, 0.0f, 0.0f);
+            }
         }
     }
     float4* ptab = nullptr;
+    if (use_pcells<MODE, P>()) ptab = wcells + P * ((tileH - 1) / a.s + 4);
     if (use_pairs<MODE, P>()) {
         // the pair table from the packed image (no barrier between the two
         // stagings): owner cell (r, c)'s slots at kCellF4 * (r * (P - 2) + c)
@@ -688,8 +727,9 @@ __global__ void __launch_bounds__(kThreads, GLU_F_MIN_BLOCKS)
     const int cxr = div_s(x, a) - ocx0;
     int co = (cy0 - ocy0) * cw + cxr;
     const float4* swinp = wcells + co;
-    const float4* pt =
-        use_pairs<MODE, P>() ? ptab + kCellF4 * ((cy0 - ocy0) * (P - 2) + cxr) : ptab;
+    const float4* pt = use_pairs<MODE, P>()
+                           ? ptab + kCellF4 * ((cy0 - ocy0) * (P - 2) + cxr)
+                           : (use_pcells<MODE, P>() ? ptab + 2 * co : ptab);
 #pragma unroll 1
     for (int y = yr; y < yEnd; ++y, g += 96) {
         if (y == yNext) {
@@ -699,6 +739,7 @@ __global__ void __launch_bounds__(kThreads, GLU_F_MIN_BLOCKS)
             else
                 co += cw;
             if (use_pairs<MODE, P>()) pt += kCellF4 * (P - 2);
+            if (use_pcells<MODE, P>()) pt += 2 * cw;
         }
         const float4* swin = kCarryPtr ? swinp : wcells + co;
         GLU_DCHECK(swin - wcells >= 0 && swin - wcells + 2 * cw + 2 < cw * (nch + 2));
@@ -747,7 +788,8 @@ cudaError_t launch_fp(glu_ctx* ctx, const SolveArgs& a, const float4* packed, in
     auto smem_of = [&](int r) {
         const int mch = (kTY * r - 1) / a.s + 2;
         return sizeof(float) * size_t(kTY * r) * 96 + sizeof(float4) * size_t(pitch) * (mch + 2) +
-               (use_pairs<MODE, P>() ? sizeof(float4) * size_t(kCellF4) * (P - 2) * mch : 0);
+               (use_pairs<MODE, P>() ? sizeof(float4) * size_t(kCellF4) * (P - 2) * mch : 0) +
+               (use_pcells<MODE, P>() ? 2 * sizeof(float4) * size_t(pitch) * (mch + 2) : 0);
     };
     thread_local int memo[6] = {-1, 0, 0, 0, -1, 1};  // device, s, W, H, MODE/OUT/P -> rows
     const int key = (MODE * 4 + OUT) * 64 + P;
